@@ -1,0 +1,137 @@
+/*
+ * gpp_b200.h — C-ABI of the B200 (sm_100a) stage-executor library `libgpp_b200.so`.
+ *
+ * This is the drop-in boundary below the Python GPP runtime
+ * (paper_2406_17145_b200.runtime).  The reference (arXiv 2406.17145, /root/reference)
+ * ships NO runtime: its executor was FlexFlow on V100 and
+ * SPEC.md:8 puts it out of scope.  The executor's contract is therefore the
+ * simulator's task semantics applied to a configured
+ * `StageGraph` (reference pkg/src/gpp/model.py:278-345).  Each entry point
+ * below replaces one piece of per-task work that the reference models only as
+ * an abstract `CostCurve.evaluate` call (model.py:65-92) inside
+ * `estimate_tps` (cost.py:56-70) and the sim's task durations:
+ *
+ *   gpp_linear_fwd / gpp_linear_dgrad / gpp_linear_wgrad
+ *        the fw / bw(input) / bw(weight) work of a dense operator
+ *        (Operator.fwd_cost / bwd_cost, model.py:100-114; Appendix B
+ *        feed-forward layers)
+ *   gpp_gemm                    generic layout-flagged GEMM (tests, attention glue)
+ *   gpp_rowdot_fwd / _bwd       N=1 regression / CTR heads (CANDLE MSE, DLRM BCE)
+ *   gpp_mse_loss / gpp_bce_loss / gpp_ce_loss   fused loss + dLoss kernels
+ *   gpp_colsum                  bias gradient
+ *   gpp_sgd_step                fused optimizer over a stage's parameters
+ *   gpp_layernorm_fwd / _bwd    MMT pre-LN
+ *   gpp_embbag_fwd / gpp_embbag_bwd_sgd    DLRM embedding-bag with fused sparse update
+ *   gpp_interaction_fwd / _bwd  DLRM dot interaction
+ *   gpp_copy_rows               strided row-block copy (concat slices, DP re-shard,
+ *                               same-device stage edges)
+ *
+ * Conventions:
+ *   - every function returns 0 on success, a nonzero gpp_status otherwise;
+ *     gpp_last_error() returns a thread-local message for the last failure;
+ *   - all device memory is owned by the caller (PyTorch caching allocator);
+ *     the library never allocates or frees user tensors;
+ *   - `stream` is a cudaStream_t passed as void*; every launch is async on it;
+ *   - row-major matrices; `ld*` are leading dimensions in ELEMENTS;
+ *   - dtype: GPP_F32 (SIMT FFMA path, exact fp32) or GPP_BF16 (tcgen05 path,
+ *     bf16 operands, fp32 accumulation in TMEM).
+ */
+#ifndef GPP_B200_H
+#define GPP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum gpp_status {
+  GPP_OK = 0,
+  GPP_ERR_ARG = 1,      /* invalid shape / pointer / alignment */
+  GPP_ERR_CUDA = 2,     /* a CUDA runtime call failed */
+  GPP_ERR_DRIVER = 3,   /* driver entry point (TMA descriptor encode) failed */
+  GPP_ERR_UNSUPPORTED = 4
+};
+
+enum gpp_dtype { GPP_F32 = 0, GPP_BF16 = 1 };
+enum gpp_act { GPP_ACT_NONE = 0, GPP_ACT_RELU = 1, GPP_ACT_GELU = 2 };
+
+/* ---- library ---------------------------------------------------------- */
+int gpp_version(void);
+const char* gpp_last_error(void);
+/* Number of kernels this library has launched since load (evidence counter). */
+uint64_t gpp_launch_count(void);
+
+/* ---- dense operator (Operator fw/bw work, model.py:100-114) ------------- */
+
+/* y[M,N] = act(x[M,K] · w[N,K]^T + bias[N]) (+ residual[M,N] if non-null).
+ * If pre_out != NULL it also stores the pre-activation (needed by GELU bw). */
+int gpp_linear_fwd(void* y, int64_t ldy, const void* x, int64_t ldx, const void* w, int64_t ldw,
+                   const float* bias, const void* residual, int64_t ldres, void* pre_out,
+                   int64_t ldpre, int64_t M, int64_t N, int64_t K, int act, int dtype,
+                   void* stream);
+
+/* dx[M,K] = (dy[M,N] · w[N,K]) ⊙ act'(saved[M,K]).
+ * act is the activation that PRODUCED dx's forward value (the predecessor's):
+ * RELU uses saved = that activation's output (mask saved > 0), GELU uses
+ * saved = its pre-activation; NONE ignores saved. */
+int gpp_linear_dgrad(void* dx, int64_t lddx, const void* dy, int64_t lddy, const void* w,
+                     int64_t ldw, const void* saved, int64_t ldsaved, int64_t M, int64_t N,
+                     int64_t K, int act, int dtype, void* stream);
+
+/* dw[N,K] (+)= dy[M,N]^T · x[M,K]  (fp32 out);  dbias[N] (+)= sum_m dy[m,:]. */
+int gpp_linear_wgrad(float* dw, int64_t lddw, float* dbias, const void* dy, int64_t lddy,
+                     const void* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
+                     int accumulate, int dtype, void* stream);
+
+/* Generic C[M,N] = alpha * sum_k A(m,k) B(n,k) (+ beta*C).
+ * a_mn / b_mn = 0: operand stored [rows][ld] with k contiguous (K-major);
+ *             = 1: operand stored [k][ld] with the row index contiguous (MN-major).
+ * out_f32 selects fp32 vs bf16 C (bf16 inputs); for dtype F32 everything is fp32. */
+int gpp_gemm(void* c, int64_t ldc, const void* a, int64_t lda, int a_mn, const void* b,
+             int64_t ldb, int b_mn, int64_t M, int64_t N, int64_t K, float alpha, float beta,
+             int out_f32, int dtype, void* stream);
+
+/* ---- heads and losses (Appendix B tails; SURVEY.md §2.3 note B) --------- */
+
+/* out[m] = dot(x[m,:K], w[:K]) + bias0   (fp32 out; x in dtype). */
+int gpp_rowdot_fwd(float* out, const void* x, int64_t ldx, const float* w, float bias0, int64_t M,
+                   int64_t K, int dtype, void* stream);
+/* dx[m,k] = dout[m] * w[k] * act'(saved[m,k]);  dw[k] (+)= sum_m dout[m] x[m,k];
+ * dbias[0] (+)= sum_m dout[m]. */
+int gpp_rowdot_bwd(void* dx, int64_t lddx, float* dw, float* dbias, const float* dout,
+                   const void* x, int64_t ldx, const float* w, const void* saved,
+                   int64_t ldsaved, int act, int64_t M, int64_t K, int accumulate, int dtype,
+                   void* stream);
+/* loss_acc[0] += scale * sum (pred-y)^2 ;  dpred = 2*scale*(pred - y). */
+int gpp_mse_loss(float* loss_acc, float* dpred, const float* pred, const float* y, int64_t M,
+                 float scale, void* stream);
+/* BCE-with-logits: loss_acc[0] += scale*sum l(z,y); dz = scale*(sigmoid(z)-y). */
+int gpp_bce_loss(float* loss_acc, float* dlogit, const float* logit, const float* y, int64_t M,
+                 float scale, void* stream);
+/* softmax cross-entropy over C classes: logits [M,C] (dtype), labels int64 [M];
+ * loss_acc[0] += scale*sum -log p[label];  dlogits = scale*(p - onehot) (same dtype). */
+int gpp_ce_loss(float* loss_acc, void* dlogits, int64_t lddl, const void* logits, int64_t ldl,
+                const int64_t* labels, int64_t M, int64_t C, float scale, int dtype,
+                void* stream);
+
+/* colsum: out[n] (+)= sum_m x[m,n] (x in dtype, out fp32). */
+int gpp_colsum(float* out, const void* x, int64_t ldx, int64_t M, int64_t N, int accumulate,
+               int dtype, void* stream);
+
+/* ---- optimizer ----------------------------------------------------------- */
+/* master[i] -= lr * grad[i]; if shadow (bf16) != NULL also shadow[i] = bf16(master[i]). */
+int gpp_sgd_step(float* master, void* shadow_bf16, const float* grad, int64_t n, float lr,
+                 void* stream);
+
+/* ---- data movement ------------------------------------------------------- */
+/* dst[r, :cols] = src[r, :cols] for r < rows (same device; elem_bytes 2 or 4). */
+int gpp_copy_rows(void* dst, int64_t lddst, const void* src, int64_t ldsrc, int64_t rows,
+                  int64_t cols, int elem_bytes, void* stream);
+/* dst_f32[i] = float(src[i]) or dst_bf16[i] = bf16(src_f32[i]). */
+int gpp_cast(void* dst, int dst_dtype, const void* src, int src_dtype, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPP_B200_H */

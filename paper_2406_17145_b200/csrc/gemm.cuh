@@ -1,0 +1,35 @@
+// GEMM epilogue contract shared by the tcgen05 (bf16) and SIMT (fp32) GEMMs.
+#pragma once
+#include "common.cuh"
+
+namespace gpp {
+
+enum {
+  EPI_FWD = 0,    // out(dtype) = act(alpha*acc + bias) [+ residual];  optional pre-act store
+  EPI_DGRAD = 1,  // out(dtype) = alpha*acc * act'(saved)
+  EPI_F32 = 2,    // out(f32)   = alpha*acc + beta*out
+  EPI_BF16 = 3    // out(dtype) = alpha*acc + beta*out
+};
+
+struct EpiParams {
+  void* out;
+  int64_t ldo;
+  const float* bias;  // EPI_FWD: [N] or null
+  const void* aux;    // EPI_FWD: residual (dtype); EPI_DGRAD: act'-saved (dtype)
+  int64_t ldaux;
+  void* pre;          // EPI_FWD: optional pre-activation store (dtype)
+  int64_t ldpre;
+  float alpha;
+  float beta;
+  int act;
+};
+
+// bf16 operands, tcgen05 + TMA (gemm_sm100.cu).
+int tc_gemm(int epi, const void* a, int64_t lda, int a_mn, const void* b, int64_t ldb, int b_mn,
+            const EpiParams& ep, int64_t M, int64_t N, int64_t K, cudaStream_t stream);
+// fp32 operands, SIMT FFMA (gemm_simt.cu) — exact-fp32 path for the toy config.
+int simt_gemm(int epi, const void* a, int64_t lda, int a_mn, const void* b, int64_t ldb,
+              int b_mn, const EpiParams& ep, int64_t M, int64_t N, int64_t K,
+              cudaStream_t stream);
+
+}  // namespace gpp

@@ -1,0 +1,413 @@
+// C-ABI entry points (include/gpp_b200.h) and the SIMT kernels around the GEMMs:
+// N=1 heads, fused losses, bias-grad column sums, the fused SGD step, casts and
+// strided row copies.  All memory-bound; vectorised where alignment allows.
+#include <atomic>
+#include <string>
+
+#include "gemm.cuh"
+
+namespace gpp {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T ld(const void* p, int64_t i) {
+  return static_cast<const T*>(p)[i];
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum; every thread receives the result.  blockDim.x multiple of 32, <= 1024.
+__device__ float block_sum(float v) {
+  __shared__ float red[32];
+  __shared__ float total;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    float s = lane < (blockDim.x >> 5) ? red[lane] : 0.f;
+    s = warp_sum(s);
+    if (lane == 0) total = s;
+  }
+  __syncthreads();
+  return total;
+}
+
+__device__ float block_max(float v) {
+  __shared__ float red[32];
+  __shared__ float total;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    float s = lane < (blockDim.x >> 5) ? red[lane] : -INFINITY;
+    s = warp_max(s);
+    if (lane == 0) total = s;
+  }
+  __syncthreads();
+  return total;
+}
+
+// ---------------- heads ----------------
+template <typename T>
+__global__ void rowdot_fwd_kernel(float* out, const T* x, int64_t ldx, const float* w, float b0,
+                                  int64_t M, int64_t K) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const T* xr = x + row * ldx;
+  float s = 0.f;
+  for (int64_t k = lane; k < K; k += 32) s = fmaf(to_f<T>(xr[k]), w[k], s);
+  s = warp_sum(s);
+  if (lane == 0) out[row] = s + b0;
+}
+
+template <typename T>
+__global__ void rowdot_dx_kernel(T* dx, int64_t lddx, const float* dout, const float* w,
+                                 const T* saved, int64_t ldsaved, int act, int64_t M, int64_t K) {
+  const int64_t n = M * K;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = i / K, k = i % K;
+    float v = dout[m] * w[k];
+    if (act != GPP_ACT_NONE) v *= act_bwd(to_f<T>(saved[m * ldsaved + k]), act);
+    dx[m * lddx + k] = from_f<T>(v);
+  }
+}
+
+// out[n] (+)= sum_m wts[m] * x[m, n]   (wts == nullptr -> 1).  Deterministic:
+// block = 8 row-groups x 32 columns, fixed-order smem reduction.
+template <typename T>
+__global__ void colsum_kernel(float* out, const T* x, int64_t ldx, const float* wts, int64_t M,
+                              int64_t N, int accumulate) {
+  __shared__ float part[8][33];
+  const int c = threadIdx.x & 31, r = threadIdx.x >> 5;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + c;
+  float s = 0.f;
+  if (col < N) {
+    for (int64_t m = r; m < M; m += 8) {
+      const float v = to_f<T>(x[m * ldx + col]);
+      s = wts ? fmaf(wts[m], v, s) : s + v;
+    }
+  }
+  part[r][c] = s;
+  __syncthreads();
+  if (r == 0 && col < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += part[i][c];
+    out[col] = accumulate ? out[col] + t : t;
+  }
+}
+
+// ---------------- losses (single block, deterministic reductions) ----------------
+__global__ void mse_kernel(float* loss_acc, float* dpred, const float* pred, const float* y,
+                           int64_t M, float scale) {
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    const float d = pred[i] - y[i];
+    s = fmaf(d, d, s);
+    dpred[i] = 2.f * scale * d;
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) loss_acc[0] += scale * s;
+}
+
+__global__ void bce_kernel(float* loss_acc, float* dz, const float* z, const float* y, int64_t M,
+                           float scale) {
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    const float zi = z[i], yi = y[i];
+    s += fmaxf(zi, 0.f) - zi * yi + log1pf(__expf(-fabsf(zi)));
+    dz[i] = scale * (1.f / (1.f + __expf(-zi)) - yi);
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) loss_acc[0] += scale * s;
+}
+
+// One block per row: softmax cross-entropy; writes dlogits, adds the row loss.
+template <typename T>
+__global__ void ce_kernel(float* loss_acc, T* dl, int64_t lddl, const T* logits, int64_t ldl,
+                          const int64_t* labels, int64_t C, float scale) {
+  const int64_t row = blockIdx.x;
+  const T* lr = logits + row * ldl;
+  float mx = -INFINITY;
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) mx = fmaxf(mx, to_f<T>(lr[c]));
+  mx = block_max(mx);
+  float se = 0.f;
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) se += __expf(to_f<T>(lr[c]) - mx);
+  se = block_sum(se);
+  const float lse = mx + logf(se);
+  const int64_t lab = labels[row];
+  T* dr = dl + row * lddl;
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+    const float p = __expf(to_f<T>(lr[c]) - lse);
+    dr[c] = from_f<T>(scale * (p - (c == lab ? 1.f : 0.f)));
+  }
+  if (threadIdx.x == 0) atomicAdd(loss_acc, scale * (lse - to_f<T>(lr[lab])));
+}
+
+__global__ void sum_into_kernel(float* acc, const float* v, int64_t n) {
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) acc[0] += s;
+}
+
+// ---------------- optimizer ----------------
+__global__ void sgd_kernel(float* __restrict__ master, bf16* __restrict__ shadow,
+                           const float* __restrict__ grad, int64_t n, float lr) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n4 = n / 4;
+  float4* m4 = reinterpret_cast<float4*>(master);
+  const float4* g4 = reinterpret_cast<const float4*>(grad);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += stride) {
+    float4 m = m4[i];
+    const float4 g = g4[i];
+    m.x -= lr * g.x; m.y -= lr * g.y; m.z -= lr * g.z; m.w -= lr * g.w;
+    m4[i] = m;
+    if (shadow) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(m.x, m.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(m.z, m.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(shadow)[i] = pk;
+    }
+  }
+  for (int64_t i = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const float m = master[i] - lr * grad[i];
+    master[i] = m;
+    if (shadow) shadow[i] = __float2bfloat16_rn(m);
+  }
+}
+
+template <typename D, typename S>
+__global__ void cast_kernel(D* dst, const S* src, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = from_f<D>(to_f<S>(src[i]));
+}
+
+int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace
+}  // namespace gpp
+
+using namespace gpp;
+
+extern "C" {
+
+int gpp_version(void) { return 1; }
+const char* gpp_last_error(void) { return g_last_error.c_str(); }
+uint64_t gpp_launch_count(void) { return g_launches.load(); }
+
+static int gemm_any(int epi, const void* a, int64_t lda, int a_mn, const void* b, int64_t ldb,
+                    int b_mn, const EpiParams& ep, int64_t M, int64_t N, int64_t K, int dtype,
+                    void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == GPP_BF16) return tc_gemm(epi, a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, s);
+  if (dtype == GPP_F32) return simt_gemm(epi, a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, s);
+  set_error("unknown dtype");
+  return GPP_ERR_ARG;
+}
+
+int gpp_linear_fwd(void* y, int64_t ldy, const void* x, int64_t ldx, const void* w, int64_t ldw,
+                   const float* bias, const void* residual, int64_t ldres, void* pre_out,
+                   int64_t ldpre, int64_t M, int64_t N, int64_t K, int act, int dtype,
+                   void* stream) {
+  GPP_ARG_CHECK(y && x && w, "null pointer");
+  EpiParams ep{y, ldy, bias, residual, ldres, pre_out, ldpre, 1.f, 0.f, act};
+  return gemm_any(EPI_FWD, x, ldx, 0, w, ldw, 0, ep, M, N, K, dtype, stream);
+}
+
+int gpp_linear_dgrad(void* dx, int64_t lddx, const void* dy, int64_t lddy, const void* w,
+                     int64_t ldw, const void* saved, int64_t ldsaved, int64_t M, int64_t N,
+                     int64_t K, int act, int dtype, void* stream) {
+  GPP_ARG_CHECK(dx && dy && w, "null pointer");
+  GPP_ARG_CHECK(act == GPP_ACT_NONE || saved, "act' needs the saved tensor");
+  EpiParams ep{dx, lddx, nullptr, saved, ldsaved, nullptr, 0, 1.f, 0.f, act};
+  // dx[M,K] = dy[M,N] . w[N,K]: GEMM (M, K, N); B(n=k_in, k=n_out) = w[n_out][k_in] is MN-major.
+  return gemm_any(EPI_DGRAD, dy, lddy, 0, w, ldw, 1, ep, M, K, N, dtype, stream);
+}
+
+int gpp_linear_wgrad(float* dw, int64_t lddw, float* dbias, const void* dy, int64_t lddy,
+                     const void* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
+                     int accumulate, int dtype, void* stream) {
+  GPP_ARG_CHECK(dw && dy && x, "null pointer");
+  EpiParams ep{dw, lddw, nullptr, nullptr, 0, nullptr, 0, 1.f, accumulate ? 1.f : 0.f, 0};
+  // dw[N,K] = sum_m dy[m,n] x[m,k]: GEMM (N, K, M) with both operands MN-major.
+  int rc = gemm_any(EPI_F32, dy, lddy, 1, x, ldx, 1, ep, N, K, M, dtype, stream);
+  if (rc || !dbias) return rc;
+  return gpp_colsum(dbias, dy, lddy, M, N, accumulate, dtype, stream);
+}
+
+int gpp_gemm(void* c, int64_t ldc, const void* a, int64_t lda, int a_mn, const void* b,
+             int64_t ldb, int b_mn, int64_t M, int64_t N, int64_t K, float alpha, float beta,
+             int out_f32, int dtype, void* stream) {
+  GPP_ARG_CHECK(c && a && b, "null pointer");
+  EpiParams ep{c, ldc, nullptr, nullptr, 0, nullptr, 0, alpha, beta, 0};
+  const int epi = (dtype == GPP_F32 || out_f32) ? EPI_F32 : EPI_BF16;
+  return gemm_any(epi, a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, dtype, stream);
+}
+
+int gpp_rowdot_fwd(float* out, const void* x, int64_t ldx, const float* w, float bias0, int64_t M,
+                   int64_t K, int dtype, void* stream) {
+  GPP_ARG_CHECK(out && x && w && M > 0 && K > 0, "bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int blocks = static_cast<int>((M + 7) / 8);
+  if (dtype == GPP_BF16)
+    rowdot_fwd_kernel<bf16><<<blocks, 256, 0, s>>>(out, static_cast<const bf16*>(x), ldx, w, bias0, M, K);
+  else
+    rowdot_fwd_kernel<float><<<blocks, 256, 0, s>>>(out, static_cast<const float*>(x), ldx, w, bias0, M, K);
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_rowdot_bwd(void* dx, int64_t lddx, float* dw, float* dbias, const float* dout,
+                   const void* x, int64_t ldx, const float* w, const void* saved,
+                   int64_t ldsaved, int act, int64_t M, int64_t K, int accumulate, int dtype,
+                   void* stream) {
+  GPP_ARG_CHECK(dout && x && w && M > 0 && K > 0, "bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dx) {
+    const int g = grid_for(M * K, 256);
+    if (dtype == GPP_BF16)
+      rowdot_dx_kernel<bf16><<<g, 256, 0, s>>>(static_cast<bf16*>(dx), lddx, dout, w,
+                                               static_cast<const bf16*>(saved), ldsaved, act, M, K);
+    else
+      rowdot_dx_kernel<float><<<g, 256, 0, s>>>(static_cast<float*>(dx), lddx, dout, w,
+                                                static_cast<const float*>(saved), ldsaved, act, M, K);
+    GPP_LAUNCH_CHECK();
+  }
+  if (dw) {
+    const unsigned g = static_cast<unsigned>((K + 31) / 32);
+    if (dtype == GPP_BF16)
+      colsum_kernel<bf16><<<g, 256, 0, s>>>(dw, static_cast<const bf16*>(x), ldx, dout, M, K, accumulate);
+    else
+      colsum_kernel<float><<<g, 256, 0, s>>>(dw, static_cast<const float*>(x), ldx, dout, M, K, accumulate);
+    GPP_LAUNCH_CHECK();
+  }
+  if (dbias) {
+    colsum_kernel<float><<<1, 256, 0, s>>>(dbias, dout, 1, nullptr, M, 1, accumulate);
+    GPP_LAUNCH_CHECK();
+  }
+  return GPP_OK;
+}
+
+int gpp_mse_loss(float* loss_acc, float* dpred, const float* pred, const float* y, int64_t M,
+                 float scale, void* stream) {
+  GPP_ARG_CHECK(loss_acc && dpred && pred && y && M > 0, "bad argument");
+  mse_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(loss_acc, dpred, pred, y, M, scale);
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_bce_loss(float* loss_acc, float* dlogit, const float* logit, const float* y, int64_t M,
+                 float scale, void* stream) {
+  GPP_ARG_CHECK(loss_acc && dlogit && logit && y && M > 0, "bad argument");
+  bce_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(loss_acc, dlogit, logit, y, M, scale);
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_ce_loss(float* loss_acc, void* dlogits, int64_t lddl, const void* logits, int64_t ldl,
+                const int64_t* labels, int64_t M, int64_t C, float scale, int dtype,
+                void* stream) {
+  GPP_ARG_CHECK(loss_acc && dlogits && logits && labels && M > 0 && C > 0, "bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == GPP_BF16)
+    ce_kernel<bf16><<<static_cast<unsigned>(M), 256, 0, s>>>(loss_acc, static_cast<bf16*>(dlogits), lddl,
+                                                             static_cast<const bf16*>(logits), ldl, labels, C, scale);
+  else
+    ce_kernel<float><<<static_cast<unsigned>(M), 256, 0, s>>>(loss_acc, static_cast<float*>(dlogits), lddl,
+                                                              static_cast<const float*>(logits), ldl, labels, C, scale);
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_colsum(float* out, const void* x, int64_t ldx, int64_t M, int64_t N, int accumulate,
+               int dtype, void* stream) {
+  GPP_ARG_CHECK(out && x && M > 0 && N > 0, "bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned g = static_cast<unsigned>((N + 31) / 32);
+  if (dtype == GPP_BF16)
+    colsum_kernel<bf16><<<g, 256, 0, s>>>(out, static_cast<const bf16*>(x), ldx, nullptr, M, N, accumulate);
+  else
+    colsum_kernel<float><<<g, 256, 0, s>>>(out, static_cast<const float*>(x), ldx, nullptr, M, N, accumulate);
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_sgd_step(float* master, void* shadow_bf16, const float* grad, int64_t n, float lr,
+                 void* stream) {
+  GPP_ARG_CHECK(master && grad && n > 0, "bad argument");
+  GPP_ARG_CHECK((reinterpret_cast<uintptr_t>(master) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(grad) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(shadow_bf16) & 7) == 0,
+                "sgd buffers must be 16-byte aligned");
+  sgd_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      master, static_cast<bf16*>(shadow_bf16), grad, n, lr);
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_copy_rows(void* dst, int64_t lddst, const void* src, int64_t ldsrc, int64_t rows,
+                  int64_t cols, int elem_bytes, void* stream) {
+  GPP_ARG_CHECK(dst && src && rows >= 0 && cols >= 0, "bad argument");
+  if (rows == 0 || cols == 0) return GPP_OK;
+  cudaError_t e = cudaMemcpy2DAsync(dst, lddst * elem_bytes, src, ldsrc * elem_bytes,
+                                    cols * elem_bytes, rows, cudaMemcpyDeviceToDevice,
+                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    set_error(std::string("gpp_copy_rows: ") + cudaGetErrorString(e));
+    return GPP_ERR_CUDA;
+  }
+  return GPP_OK;
+}
+
+int gpp_cast(void* dst, int dst_dtype, const void* src, int src_dtype, int64_t n, void* stream) {
+  GPP_ARG_CHECK(dst && src && n >= 0, "bad argument");
+  if (n == 0) return GPP_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int g = grid_for(n, 256);
+  if (dst_dtype == GPP_F32 && src_dtype == GPP_BF16)
+    cast_kernel<float, bf16><<<g, 256, 0, s>>>(static_cast<float*>(dst), static_cast<const bf16*>(src), n);
+  else if (dst_dtype == GPP_BF16 && src_dtype == GPP_F32)
+    cast_kernel<bf16, float><<<g, 256, 0, s>>>(static_cast<bf16*>(dst), static_cast<const float*>(src), n);
+  else {
+    set_error("gpp_cast: unsupported dtype pair");
+    return GPP_ERR_ARG;
+  }
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+}  // extern "C"

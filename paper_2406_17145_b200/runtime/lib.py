@@ -1,0 +1,196 @@
+"""ctypes binding of the C-ABI library ``libgpp_b200.so`` (include/gpp_b200.h).
+
+PyTorch supplies device memory and streams only; every compute call below goes
+through the sm_100a library.  There is no CPU or eager-PyTorch fallback: if the
+library is missing or a call fails, a ``RuntimeError`` is raised.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import torch
+
+_PKG = Path(__file__).resolve().parent.parent
+LIB_PATH = _PKG / "libgpp_b200.so"
+
+F32, BF16 = 0, 1
+ACT = {"none": 0, "relu": 1, "gelu": 2}
+
+_lib = None
+
+_vp, _i64, _i32, _f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
+
+_SIGS = {
+    "gpp_version": ([], _i32),
+    "gpp_last_error": ([], ctypes.c_char_p),
+    "gpp_launch_count": ([], ctypes.c_uint64),
+    "gpp_linear_fwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
+    "gpp_linear_dgrad": ([_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
+    "gpp_linear_wgrad": ([_vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
+    "gpp_gemm": ([_vp, _i64, _vp, _i64, _i32, _vp, _i64, _i32, _i64, _i64, _i64, _f32, _f32, _i32, _i32, _vp], _i32),
+    "gpp_rowdot_fwd": ([_vp, _vp, _i64, _vp, _f32, _i64, _i64, _i32, _vp], _i32),
+    "gpp_rowdot_bwd": ([_vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _i64, _i64, _i32, _i32, _vp], _i32),
+    "gpp_mse_loss": ([_vp, _vp, _vp, _vp, _i64, _f32, _vp], _i32),
+    "gpp_bce_loss": ([_vp, _vp, _vp, _vp, _i64, _f32, _vp], _i32),
+    "gpp_ce_loss": ([_vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _f32, _i32, _vp], _i32),
+    "gpp_colsum": ([_vp, _vp, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
+    "gpp_sgd_step": ([_vp, _vp, _vp, _i64, _f32, _vp], _i32),
+    "gpp_copy_rows": ([_vp, _i64, _vp, _i64, _i64, _i64, _i32, _vp], _i32),
+    "gpp_cast": ([_vp, _i32, _vp, _i32, _i64, _vp], _i32),
+    "gpp_layernorm_fwd": ([_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _vp], _i32),
+    "gpp_layernorm_bwd": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp], _i32),
+    "gpp_attention_fwd": ([_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
+    "gpp_attention_bwd": ([_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
+    "gpp_embbag_fwd": ([_vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
+    "gpp_embbag_bwd_sgd": ([_vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
+    "gpp_interaction_fwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp], _i32),
+    "gpp_interaction_bwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp], _i32),
+}
+
+
+def declared_symbols() -> list[str]:
+    """Every entry point the binding expects the C-ABI library to export."""
+    return sorted(_SIGS)
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load (once) and return the ctypes handle; raise loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"libgpp_b200.so not found at {p}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
+        )
+    lib = ctypes.CDLL(str(p))
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name, None)
+        if fn is None:
+            continue  # optional entry points are checked by tests against the header
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, name: str) -> None:
+    if rc != 0:
+        msg = _lib.gpp_last_error().decode(errors="replace") if _lib is not None else "?"
+        raise RuntimeError(f"{name} failed (status {rc}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    fn = getattr(lib, name, None)
+    if fn is None:
+        raise RuntimeError(f"{name} is not exported by {LIB_PATH}")
+    _check(fn(*args), name)
+
+
+def launch_count() -> int:
+    return int(load().gpp_launch_count())
+
+
+# ---------------------------------------------------------------------------
+# Tensor-level helpers (device tensors; row-major 2-D with unit inner stride).
+# ---------------------------------------------------------------------------
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _ld(t: torch.Tensor | None) -> int:
+    if t is None:
+        return 0
+    if t.dim() == 1:
+        return t.shape[0]
+    assert t.stride(-1) == 1, "inner dimension must be contiguous"
+    return t.stride(0)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def linear_fwd(y, x, w, bias=None, act="none", residual=None, pre=None, stream=None):
+    M, K = x.shape
+    N = w.shape[0]
+    call("gpp_linear_fwd", _ptr(y), _ld(y), _ptr(x), _ld(x), _ptr(w), _ld(w), _ptr(bias),
+         _ptr(residual), _ld(residual), _ptr(pre), _ld(pre), M, N, K, ACT[act], _dt(x), _stream(stream))
+
+
+def linear_dgrad(dx, dy, w, saved=None, act="none", stream=None):
+    M, N = dy.shape
+    K = w.shape[1]
+    call("gpp_linear_dgrad", _ptr(dx), _ld(dx), _ptr(dy), _ld(dy), _ptr(w), _ld(w), _ptr(saved),
+         _ld(saved), M, N, K, ACT[act], _dt(dy), _stream(stream))
+
+
+def linear_wgrad(dw, dbias, dy, x, accumulate=False, stream=None):
+    M, N = dy.shape
+    K = x.shape[1]
+    call("gpp_linear_wgrad", _ptr(dw), _ld(dw), _ptr(dbias), _ptr(dy), _ld(dy), _ptr(x), _ld(x),
+         M, N, K, int(bool(accumulate)), _dt(dy), _stream(stream))
+
+
+def gemm(c, a, b, a_mn=False, b_mn=False, alpha=1.0, beta=0.0, stream=None):
+    """c[M,N] = alpha * A·Bᵀ + beta*c with A(m,k)/B(n,k) in K- or MN-major storage."""
+    M = a.shape[1] if a_mn else a.shape[0]
+    K = a.shape[0] if a_mn else a.shape[1]
+    N = b.shape[1] if b_mn else b.shape[0]
+    call("gpp_gemm", _ptr(c), _ld(c), _ptr(a), _ld(a), int(a_mn), _ptr(b), _ld(b), int(b_mn),
+         M, N, K, float(alpha), float(beta), int(c.dtype == torch.float32), _dt(a), _stream(stream))
+
+
+def rowdot_fwd(out, x, w, bias0: float, stream=None):
+    M, K = x.shape
+    call("gpp_rowdot_fwd", _ptr(out), _ptr(x), _ld(x), _ptr(w), float(bias0), M, K, _dt(x), _stream(stream))
+
+
+def rowdot_bwd(dx, dw, dbias, dout, x, w, saved=None, act="none", accumulate=False, stream=None):
+    M, K = x.shape
+    call("gpp_rowdot_bwd", _ptr(dx), _ld(dx), _ptr(dw), _ptr(dbias), _ptr(dout), _ptr(x), _ld(x),
+         _ptr(w), _ptr(saved), _ld(saved), ACT[act], M, K, int(bool(accumulate)), _dt(x), _stream(stream))
+
+
+def mse_loss(loss_acc, dpred, pred, y, scale: float, stream=None):
+    call("gpp_mse_loss", _ptr(loss_acc), _ptr(dpred), _ptr(pred), _ptr(y), pred.numel(), float(scale), _stream(stream))
+
+
+def bce_loss(loss_acc, dlogit, logit, y, scale: float, stream=None):
+    call("gpp_bce_loss", _ptr(loss_acc), _ptr(dlogit), _ptr(logit), _ptr(y), logit.numel(), float(scale), _stream(stream))
+
+
+def ce_loss(loss_acc, dlogits, logits, labels, scale: float, stream=None):
+    M, C = logits.shape
+    call("gpp_ce_loss", _ptr(loss_acc), _ptr(dlogits), _ld(dlogits), _ptr(logits), _ld(logits),
+         _ptr(labels), M, C, float(scale), _dt(logits), _stream(stream))
+
+
+def colsum(out, x, accumulate=False, stream=None):
+    M, N = x.shape
+    call("gpp_colsum", _ptr(out), _ptr(x), _ld(x), M, N, int(bool(accumulate)), _dt(x), _stream(stream))
+
+
+def sgd_step(master, shadow, grad, lr: float, stream=None):
+    call("gpp_sgd_step", _ptr(master), _ptr(shadow), _ptr(grad), master.numel(), float(lr), _stream(stream))
+
+
+def copy_rows(dst, src, stream=None):
+    rows, cols = src.shape
+    call("gpp_copy_rows", _ptr(dst), _ld(dst), _ptr(src), _ld(src), rows, cols, src.element_size(), _stream(stream))

@@ -1,0 +1,181 @@
+"""Kernel-level numerics of libgpp_b200.so against a plain PyTorch fp32 reference.
+
+bf16 kernels: inputs are bf16, the reference is fp32 math on the same bf16 values,
+so only accumulation order / final rounding differ.  fp32 kernels: rtol 1e-5.
+"""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(128, 256, 64), (256, 512, 128), (1000, 520, 200), (384, 128, 4096), (1024, 4096, 1024)]
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).abs().max() / (b.float().abs().max() + 1e-6)).item()
+
+
+def _op(x_rows_k, mn):
+    """Return storage for an operand with logical (rows, k): MN-major stores its transpose."""
+    return x_rows_k.t().contiguous() if mn else x_rows_k.contiguous()
+
+
+@pytest.mark.parametrize("a_mn", [0, 1])
+@pytest.mark.parametrize("b_mn", [0, 1])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_bf16_layouts(cuda_lib, a_mn, b_mn, shape):
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K + a_mn * 2 + b_mn)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    C = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    cuda_lib.gemm(C, _op(A, a_mn), _op(B, b_mn), a_mn=a_mn, b_mn=b_mn)
+    ref = A.float() @ B.float().t()
+    torch.cuda.synchronize()
+    assert _rel(C, ref) < 1e-4
+
+
+@pytest.mark.parametrize("a_mn", [0, 1])
+@pytest.mark.parametrize("b_mn", [0, 1])
+def test_gemm_f32_layouts(cuda_lib, a_mn, b_mn):
+    M, N, K = 200, 136, 72
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(M, K, device="cuda", generator=g)
+    B = torch.randn(N, K, device="cuda", generator=g)
+    C = torch.full((M, N), 2.0, device="cuda")
+    cuda_lib.gemm(C, _op(A, a_mn), _op(B, b_mn), a_mn=a_mn, b_mn=b_mn, alpha=0.5, beta=1.0)
+    ref = 0.5 * (A.double() @ B.double().t()) + 2.0
+    torch.cuda.synchronize()
+    assert _rel(C, ref) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("act", ["none", "relu", "gelu"])
+def test_linear_fwd_bwd(cuda_lib, dtype, act):
+    M, N, K = 512, 768, 384
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(M, K, device="cuda", generator=g).to(dtype)
+    w = (torch.randn(N, K, device="cuda", generator=g) / K**0.5).to(dtype)
+    b = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g).to(dtype)
+    y = torch.empty(M, N, device="cuda", dtype=dtype)
+    pre = torch.empty(M, N, device="cuda", dtype=dtype)
+    cuda_lib.linear_fwd(y, x, w, bias=b, act=act, residual=res, pre=pre)
+    z = x.float() @ w.float().t() + b
+    fa = {"none": lambda t: t, "relu": torch.relu, "gelu": torch.nn.functional.gelu}[act]
+    ref = fa(z) + res.float()
+    tol = 2e-2 if dtype == torch.bfloat16 else 1e-5
+    torch.cuda.synchronize()
+    assert _rel(y, ref) < tol
+    assert _rel(pre, z) < tol
+
+    # dgrad with the act' of the predecessor: saved = output (relu) or pre-activation (gelu)
+    dy = torch.randn(M, N, device="cuda", generator=g).to(dtype)
+    saved = torch.randn(M, K, device="cuda", generator=g).to(dtype)
+    dx = torch.empty(M, K, device="cuda", dtype=dtype)
+    cuda_lib.linear_dgrad(dx, dy, w, saved=saved, act=act)
+    dxr = dy.float() @ w.float()
+    s = saved.float()
+    if act == "relu":
+        dxr = dxr * (s > 0)
+    elif act == "gelu":
+        s = s.clone().requires_grad_(True)
+        torch.nn.functional.gelu(s).backward(torch.ones_like(s))
+        dxr = dxr * s.grad
+    torch.cuda.synchronize()
+    assert _rel(dx, dxr) < tol
+
+    dw = torch.full((N, K), 1.0, device="cuda")
+    db = torch.full((N,), 1.0, device="cuda")
+    cuda_lib.linear_wgrad(dw, db, dy, x, accumulate=True)
+    torch.cuda.synchronize()
+    assert _rel(dw, dy.float().t() @ x.float() + 1.0) < (1e-4 if dtype == torch.bfloat16 else 1e-5)
+    assert _rel(db, dy.float().sum(0) + 1.0) < 1e-4
+
+
+def test_big_tile_shapes(cuda_lib):
+    # CANDLE tower layer at b=1024: fw / dgrad / wgrad
+    M, N, K = 1024, 4096, 4096
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(N, K, device="cuda", generator=g) / 64).bfloat16()
+    y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    cuda_lib.linear_fwd(y, x, w, act="relu")
+    torch.cuda.synchronize()
+    assert _rel(y, torch.relu(x.float() @ w.float().t())) < 1e-2
+    dw = torch.empty(N, K, device="cuda")
+    cuda_lib.linear_wgrad(dw, None, y, x)
+    torch.cuda.synchronize()
+    assert _rel(dw, y.float().t() @ x.float()) < 1e-4
+
+
+def test_heads_and_losses(cuda_lib):
+    M, K = 1000, 300
+    g = torch.Generator(device="cuda").manual_seed(9)
+    for dtype in (torch.float32, torch.bfloat16):
+        x = torch.randn(M, K, device="cuda", generator=g).to(dtype)
+        w = torch.randn(K, device="cuda", generator=g)
+        out = torch.empty(M, device="cuda")
+        cuda_lib.rowdot_fwd(out, x, w, 0.25)
+        torch.cuda.synchronize()
+        assert _rel(out, x.float() @ w + 0.25) < 1e-4
+        y = torch.randn(M, device="cuda", generator=g)
+        loss = torch.zeros(1, device="cuda")
+        dpred = torch.empty(M, device="cuda")
+        cuda_lib.mse_loss(loss, dpred, out, y, 1.0 / M)
+        torch.cuda.synchronize()
+        ref = ((out - y) ** 2).mean()
+        assert abs(loss.item() - ref.item()) / ref.item() < 1e-5
+        assert _rel(dpred, 2 * (out - y) / M) < 1e-5
+        dx = torch.empty(M, K, device="cuda", dtype=dtype)
+        dw = torch.empty(K, device="cuda")
+        db = torch.empty(1, device="cuda")
+        cuda_lib.rowdot_bwd(dx, dw, db, dpred, x, w, saved=x, act="relu")
+        torch.cuda.synchronize()
+        assert _rel(dx, dpred[:, None] * w[None, :] * (x.float() > 0)) < 1e-2
+        assert _rel(dw, dpred @ x.float()) < 1e-4
+        assert abs(db.item() - dpred.sum().item()) < 1e-5
+    # CE
+    C = 1000
+    logits = torch.randn(64, C, device="cuda", generator=g)
+    labels = torch.randint(0, C, (64,), device="cuda", generator=g)
+    dl = torch.empty_like(logits)
+    loss = torch.zeros(1, device="cuda")
+    cuda_lib.ce_loss(loss, dl, logits, labels, 1.0 / 64)
+    lt = logits.clone().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(lt, labels)
+    ref.backward()
+    torch.cuda.synchronize()
+    assert abs(loss.item() - ref.item()) < 1e-4
+    assert _rel(dl, lt.grad) < 1e-4
+    # BCE
+    z = torch.randn(500, device="cuda", generator=g)
+    yb = (torch.rand(500, device="cuda", generator=g) > 0.5).float()
+    dz = torch.empty_like(z)
+    loss.zero_()
+    cuda_lib.bce_loss(loss, dz, z, yb, 1.0 / 500)
+    zt = z.clone().requires_grad_(True)
+    ref = torch.nn.functional.binary_cross_entropy_with_logits(zt, yb)
+    ref.backward()
+    torch.cuda.synchronize()
+    assert abs(loss.item() - ref.item()) < 1e-5
+    assert _rel(dz, zt.grad) < 1e-5
+
+
+def test_sgd_and_colsum(cuda_lib):
+    g = torch.Generator(device="cuda").manual_seed(1)
+    n = 1000003
+    m = torch.randn(n, device="cuda", generator=g)
+    gr = torch.randn(n, device="cuda", generator=g)
+    sh = torch.empty(n, device="cuda", dtype=torch.bfloat16)
+    ref = m - 0.1 * gr
+    cuda_lib.sgd_step(m, sh, gr, 0.1)
+    torch.cuda.synchronize()
+    assert torch.allclose(m, ref, rtol=1e-6, atol=1e-7)  # FMA vs two roundings
+    assert torch.equal(sh, m.bfloat16())
+    x = torch.randn(777, 333, device="cuda", generator=g)
+    out = torch.empty(333, device="cuda")
+    cuda_lib.colsum(out, x)
+    torch.cuda.synchronize()
+    assert _rel(out, x.sum(0)) < 1e-5
