@@ -1,0 +1,210 @@
+"""Workload presets: computation graphs (for the partitioner) + layer specs (for the executor).
+
+Appendix B model shapes as restated by BASELINE.json
+``configs`` and SURVEY.md §8(d); the paper gives shapes, not millisecond
+profiles, so the cost curves here are analytic B200 estimates (FLOPs at a
+fixed fraction of the measured bf16 peak plus a per-launch overhead, bytes at
+measured HBM bandwidth).  ``runtime.profiler`` replaces them with measured
+table curves.  Graph-only presets (``fig2``, ``case_study``, ``chain``) carry
+unit costs for the SPEC acceptance checks.
+
+Op ids are assigned branch by branch, so ``linearize`` (smallest ready id
+first) yields the branch-by-branch SPP order.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .model import ComputationGraph, CostCurve, DeviceCluster, Operator
+
+__all__ = ["LayerSpec", "Workload", "b200_cluster", "PRESETS", "make"]
+
+# B200 constants (MEASURED_PEAKS.json).
+BF16_TFLOPS_SUSTAINED = 1397.3
+HBM_GBS = 6539.5
+GEMM_EFF = 0.6                       # assumed achieved fraction for the analytic curves
+FLOP_PER_MS = BF16_TFLOPS_SUSTAINED * 1e9 * GEMM_EFF
+FP32_FLOP_PER_MS = 60e9              # SIMT FFMA, ~60 TFLOP/s
+BYTES_PER_MS = HBM_GBS * 1e6
+LAUNCH_MS = 0.004
+
+
+@dataclass(frozen=True)
+class LayerSpec:
+    """What the executor runs for one operator.
+
+    kind: "dense" (Linear + act), "concat", "mse_head", "bce_head", "ce_head",
+    "mmt_layer", "embbag", "interaction".
+    """
+
+    kind: str
+    in_dim: int = 0
+    out_dim: int = 0
+    act: str = "none"
+    data_key: str | None = None      # source ops read this batch tensor
+    label_key: str | None = None     # loss heads read this batch tensor
+    extra: tuple = ()                # kind-specific (e.g. mmt: (seq, heads, ffn, pool))
+
+
+@dataclass
+class Workload:
+    name: str
+    graph: ComputationGraph
+    layers: dict[int, LayerSpec]
+    data: dict[str, tuple[tuple[int, ...], str]]  # key -> (per-sample shape, kind: normal|label|binary|index)
+    mini_batch: int
+    dtype: str = "bf16"
+    flops_per_sample: float = 0.0    # train (fw+bw) algorithmic FLOPs per sample
+    bytes_per_sample: float = 0.0    # HBM-bound algorithmic bytes per sample (embeddings)
+    notes: str = ""
+    meta: dict = field(default_factory=dict)
+
+
+def b200_cluster(n: int, mem_bytes: float = 180e9) -> DeviceCluster:
+    """NVLink 5 / NVSwitch box: 900 GB/s per direction = 9e8 bytes/ms, ~10 us latency."""
+    return DeviceCluster(num_devices=n, mem_per_device=mem_bytes, intra_bw=9e8, inter_bw=9e8, link_latency=0.01)
+
+
+def _gemm_curve(flops_per_sample: float, launches: int, fp32: bool = False) -> CostCurve:
+    rate = FP32_FLOP_PER_MS if fp32 else FLOP_PER_MS
+    return CostCurve.affine(LAUNCH_MS * launches, flops_per_sample / rate)
+
+
+def _dense(oid, name, din, dout, act, bytes_el, data_key=None, fp32=False):
+    f = 2.0 * din * dout
+    op = Operator(
+        id=oid, name=name, param_bytes=4.0 * (din * dout + dout),  # fp32 master weights
+        act_bytes_per_sample=bytes_el * (din + dout), out_bytes_per_sample=bytes_el * dout,
+        fwd_cost=_gemm_curve(f, 1, fp32), bwd_cost=_gemm_curve(2 * f, 3, fp32),
+    )
+    return op, LayerSpec("dense", din, dout, act, data_key=data_key)
+
+
+def _concat(oid, name, dout, bytes_el):
+    op = Operator(id=oid, name=name, act_bytes_per_sample=0.0, out_bytes_per_sample=bytes_el * dout,
+                  fwd_cost=CostCurve.affine(LAUNCH_MS, bytes_el * dout * 2 / BYTES_PER_MS),
+                  bwd_cost=CostCurve.affine(0.0, 0.0))
+    return op, LayerSpec("concat", dout, dout)
+
+
+def _head(oid, name, kind, din, nout, bytes_el, label_key, fp32=False):
+    f = 2.0 * din * nout
+    op = Operator(id=oid, name=name, param_bytes=4.0 * (din * nout + nout),
+                  act_bytes_per_sample=bytes_el * din, out_bytes_per_sample=4.0,
+                  fwd_cost=_gemm_curve(f, 2, fp32), bwd_cost=_gemm_curve(2 * f, 3, fp32))
+    return op, LayerSpec(kind, din, nout, label_key=label_key)
+
+
+def multi_tower(name: str, towers: int, layers: int, width: int, in_dim: int, tail_hidden: int,
+                B: int, dtype: str = "bf16") -> Workload:
+    """CANDLE-Uno-style towers -> concat -> [tail Linear+ReLU] -> MSE head."""
+    fp32 = dtype == "fp32"
+    el = 4 if fp32 else 2
+    ops, specs, edges, data = [], {}, [], {}
+    oid = 0
+    ends = []
+    for t in range(towers):
+        prev = None
+        for l in range(layers):
+            din = in_dim if l == 0 else width
+            op, spec = _dense(oid, f"t{t}_ff{l}", din, width, "relu", el, data_key=f"x{t}" if l == 0 else None, fp32=fp32)
+            ops.append(op)
+            specs[oid] = spec
+            if prev is not None:
+                edges.append((prev, oid))
+            prev = oid
+            oid += 1
+        ends.append(prev)
+        data[f"x{t}"] = ((in_dim,), "normal")
+    cat = oid
+    op, spec = _concat(cat, "concat", towers * width, el)
+    ops.append(op)
+    specs[cat] = spec
+    edges += [(e, cat) for e in ends]
+    oid += 1
+    prev, dprev = cat, towers * width
+    if tail_hidden:
+        op, spec = _dense(oid, "tail_ff", dprev, tail_hidden, "relu", el, fp32=fp32)
+        ops.append(op)
+        specs[oid] = spec
+        edges.append((prev, oid))
+        prev, dprev = oid, tail_hidden
+        oid += 1
+    op, spec = _head(oid, "head_mse", "mse_head", dprev, 1, el, "y", fp32=fp32)
+    ops.append(op)
+    specs[oid] = spec
+    edges.append((prev, oid))
+    data["y"] = ((), "normal")
+    flops = 0.0
+    for s in specs.values():
+        if s.kind in ("dense", "mse_head"):
+            flops += 6.0 * s.in_dim * max(1, s.out_dim)
+    return Workload(name, ComputationGraph(ops, edges), specs, data, B, dtype, flops_per_sample=flops)
+
+
+def toy(B: int = 64) -> Workload:
+    """BASELINE configs[0]: 2 branches x 4 x [Linear(256,256)+ReLU] -> concat 512 ->
+    Linear(512,256)+ReLU -> Linear(256,1), MSE; fp32; B=64 (b=16: 4 micro-batches)."""
+    return multi_tower("toy", towers=2, layers=4, width=256, in_dim=256, tail_hidden=256, B=B, dtype="fp32")
+
+
+def candle(B: int = 1024, towers: int = 7) -> Workload:
+    """BASELINE configs[1]: CANDLE-Uno, 7 towers x 4 x FF(4096)+ReLU,
+    light tail Linear(28672,1024)+ReLU -> Linear(1024,1) MSE."""
+    return multi_tower("candle", towers=towers, layers=4, width=4096, in_dim=4096, tail_hidden=1024, B=B)
+
+
+# ---------------------------------------------------------------------------
+# Graph-only presets for the SPEC acceptance checks (unit costs).
+# ---------------------------------------------------------------------------
+
+
+def _unit(oid, name, act=1.0, out=1.0, params=1e3, fw=1.0, bw=1.0):
+    return Operator(oid, name, params, act, out, CostCurve.affine(0.0, fw), CostCurve.affine(0.0, bw))
+
+
+def fig2() -> ComputationGraph:
+    """PAPER.md Fig. 2: three 2-op branches merging into a 2-op tail (unit costs)."""
+    ops = [_unit(i, f"o{i + 1}") for i in range(8)]
+    edges = [(0, 1), (2, 3), (4, 5), (1, 6), (3, 6), (5, 6), (6, 7)]
+    return ComputationGraph(ops, edges)
+
+
+def chain(n: int, costs: list[float] | None = None) -> ComputationGraph:
+    costs = costs or [1.0] * n
+    ops = [_unit(i, f"c{i}", fw=costs[i], bw=2 * costs[i]) for i in range(n)]
+    return ComputationGraph(ops, [(i, i + 1) for i in range(n - 1)])
+
+
+def case_study(blocks: int = 4, branches: int = 2) -> ComputationGraph:
+    """§7.5: branches x [attention + 2 linear] blocks, merged by a concat.
+
+    One block = one operator (layer granularity).  Table costs
+    make b=4 twice as efficient per sample as b=1 and ~10% better than b=2,
+    and activations are large so the memory cap decides b.
+    """
+    ops, edges = [], []
+    oid = 0
+    ends = []
+    curve_f = CostCurve.table({1: 1.0, 2: 1.2, 4: 2.2, 8: 4.4})
+    curve_b = CostCurve.table({1: 2.0, 2: 2.4, 4: 4.4, 8: 8.8})
+    for br in range(branches):
+        prev = None
+        for k in range(blocks):
+            ops.append(Operator(oid, f"b{br}_blk{k}", 1e6, 1e6, 1e6, curve_f, curve_b))
+            if prev is not None:
+                edges.append((prev, oid))
+            prev = oid
+            oid += 1
+        ends.append(prev)
+    return ComputationGraph(ops, edges)
+
+
+PRESETS = {"toy": toy, "candle": candle}
+
+
+def make(name: str, **kw) -> Workload:
+    if name not in PRESETS:
+        raise ValueError(f"unknown preset {name!r}; known: {sorted(PRESETS)}")
+    return PRESETS[name](**kw)
