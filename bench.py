@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark: GPP training throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--workload candle|toy] [--mode gpp|spp]
+
+One process per GPU (torchrun for N > 1).  A "step" is one synchronous training
+iteration of the workload's configured StageGraph: every stage's kFkB task
+list, the P2P activation/gradient transfers, the DP all-reduce and the SGD
+update.  Workload at N GPUs: CANDLE-Uno (BASELINE configs[1]) with mini-batch
+1024*N (PAPER.md:1100 scales B with the device count; 4096 at 4 GPUs), random
+init, synthetic N(0,1) features.
+
+value : samples/s with the inputs already resident in HBM (CUDA events, max
+        over ranks; per-iteration working set = 0.94 GB bf16 weights + 1.9 GB
+        fp32 master/grad >> 126 MB L2, so every timed step starts L2-cold).
+e2e   : same metric through the public API with pinned HOST buffers: every
+        step's H2D input copy (double-buffered on a copy stream) and the D2H
+        loss read are inside the timed region.
+--impl reference : the CPU path (oracle/reference_model.py: the monolithic
+        torch-CPU training step) on a bounded sample, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self) -> dict:
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def _workload(name: str, world: int, per_gpu: int | None):
+    from paper_2406_17145_b200 import workloads as W
+
+    if name == "candle":
+        return W.candle(B=(per_gpu or 1024) * world)
+    if name == "toy":
+        return W.toy(B=(per_gpu or 64) * world)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def cpu_reference_run(wl_name: str, sample_B: int, steps: int):
+    """Time the reference's CPU path (monolithic torch-CPU step) on a bounded sample."""
+    from oracle.reference_model import ReferenceModel
+    from paper_2406_17145_b200.runtime.data import make_batch
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    wl = _workload(wl_name, 1, sample_B)
+    ref = ReferenceModel(wl)
+    batch = make_batch(wl, 0)
+    ref.step(batch, 1e-3)  # warm-up (allocations, thread pools)
+    t0 = time.perf_counter()
+    for s in range(steps):
+        ref.step(make_batch(wl, s + 1), 1e-3)
+    dt = time.perf_counter() - t0
+    return sample_B * steps / dt, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    sample = {"candle": 32, "toy": 64}[args.workload]
+    val, dt = cpu_reference_run(args.workload, sample, max(1, min(args.steps, 3)))
+    cores = torch.get_num_threads()
+    line = {
+        "metric": "train samples/sec", "value": round(val, 3), "unit": "samples/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": max(1, min(args.steps, 3)), "warmup": 1,
+        "ms_per_step": round(1e3 * dt / max(1, min(args.steps, 3)), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16-emulated fp32 (CPU)", "data": "synthetic",
+        "config": {"workload": f"{args.workload} (CPU sample B={sample} per step)", "device": "host CPU"},
+        "cpu_baseline": {"value": round(val, 3), "unit": "samples/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.workload} mini-batch of {sample} samples, monolithic torch-CPU step"},
+        "e2e": {"value": round(val, 3), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="candle", choices=["candle", "toy"])
+    ap.add_argument("--mode", default="gpp", choices=["gpp", "spp"])
+    ap.add_argument("--per-gpu-batch", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    from paper_2406_17145_b200.runtime.api import dist_env
+
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2406_17145_b200 import model as M
+    from paper_2406_17145_b200.runtime import lib
+    from paper_2406_17145_b200.runtime.api import plan
+    from paper_2406_17145_b200.runtime.data import make_batch, to_device_rows
+    from paper_2406_17145_b200.runtime.executor import Executor
+    from paper_2406_17145_b200.runtime.profiler import TimedBackend
+    from paper_2406_17145_b200.sim import simulate
+    from paper_2406_17145_b200.workloads import b200_cluster
+
+    wl = _workload(args.workload, world, args.per_gpu_batch)
+    t_plan = time.perf_counter()
+    strategy = plan(wl, world, args.mode)
+    t_plan = time.perf_counter() - t_plan
+    sg = strategy.stage_graph
+    dev = torch.device("cuda", local)
+    be = TimedBackend(dev)
+    be.enabled = False
+    ex = Executor(wl, sg, rank, world, be, lr=1e-4)
+    keys = set(ex.data_keys()) if ex.stage else set()
+
+    # ---------------- value: inputs resident in HBM ----------------
+    full = make_batch(wl, 0, keys=keys)
+    dev_batch = to_device_rows(ex, full, ex.dtype, dev) if ex.stage else {}
+    for _ in range(args.warmup):
+        ex.run_iteration(dev_batch)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        ex.run_iteration(dev_batch)
+    e1.record()
+    torch.cuda.synchronize()
+    launches = lib.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        lt = torch.tensor([float(launches)], device=dev)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+    value = wl.mini_batch * args.steps / (ms / 1e3)
+
+    # ---------------- e2e: host buffers through the public API ----------------
+    host = []
+    h2d_bytes = 0
+    for s in range(2):
+        fb = make_batch(wl, s + 1, keys=keys)
+        hb = {}
+        for k in ex.data_keys() if ex.stage else []:
+            t = ex.local_rows(fb[k])
+            if t.is_floating_point():
+                t = t.to(ex.dtype) if t.dim() > 1 else t.float()
+            hb[k] = t.pin_memory()
+        host.append(hb)
+    h2d_bytes = sum(t.numel() * t.element_size() for t in host[0].values())
+    dbufs = [{k: torch.empty_like(v, device=dev) for k, v in hb.items()} for hb in host]
+    loss_host = torch.zeros(args.steps, dtype=torch.float32).pin_memory()
+    copy_stream = torch.cuda.Stream(dev)
+    ready = [torch.cuda.Event(), torch.cuda.Event()]
+    consumed = [torch.cuda.Event(), torch.cuda.Event()]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+
+    def h2d(i):
+        with torch.cuda.stream(copy_stream):
+            copy_stream.wait_event(consumed[i % 2])
+            for k, v in host[i % 2].items():
+                dbufs[i % 2][k].copy_(v, non_blocking=True)
+            ready[i % 2].record(copy_stream)
+
+    for i in range(2):
+        consumed[i].record()
+    h2d(0)
+    for i in range(args.steps):
+        if i + 1 < args.steps:
+            h2d(i + 1)
+        torch.cuda.current_stream().wait_event(ready[i % 2])
+        loss = ex.run_iteration(dbufs[i % 2])
+        consumed[i % 2].record()
+        if loss is not None:
+            loss_host[i:i + 1].copy_(loss, non_blocking=True)
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = wl.mini_batch * args.steps / (e2e_ms / 1e3)
+
+    # ---------------- roofline: live GEMM timing (events around each launch) ----------------
+    be.enabled = True
+    be.reset()
+    prof_iters = 2
+    for _ in range(prof_iters):
+        ex.run_iteration(dev_batch)
+    torch.cuda.synchronize()
+    summ = be.summary() if ex.stage else {"flops": 0.0, "ms": 0.0, "tflops": 0.0, "launches": 0}
+    be.enabled = False
+    peaks, peak_src = _peaks()
+    gemm_share = (summ["ms"] / prof_iters) / (ms / args.steps) if ms > 0 else 0.0
+
+    # ---------------- simulated twin + bubble estimate ----------------
+    cluster = b200_cluster(world)
+    sim = simulate(sg, cluster, wl.graph)
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            sample = {"candle": 32, "toy": 64}[args.workload]
+            cv, cdt = cpu_reference_run(args.workload, sample, 2)
+            cpu = {"value": round(cv, 3), "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "port",
+                   "sample": f"{args.workload}, 2 steps x B={sample}, monolithic torch-CPU training step "
+                             f"(oracle/reference_model.py), {cdt:.1f}s"}
+        achieved = summ["tflops"]
+        peak = peaks["bf16_tflops_sustained"]
+        line = {
+            "metric": "train samples/sec", "value": round(value, 3), "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16" if wl.dtype != "fp32" else "fp32", "data": "synthetic",
+            "config": {
+                "workload": f"{wl.name}: 7 towers x 4 x Linear(4096,4096)+ReLU -> concat -> Linear(28672,1024)+ReLU -> Linear(1024,1) MSE"
+                if wl.name == "candle" else wl.name,
+                "global_batch": wl.mini_batch, "mode": args.mode,
+                "parallelism": f"{args.mode} stages={len(sg.stages)} depth={sim.depth}",
+                "stages": [{"ops": len(s.op_ids), "b": s.micro_batch, "d": s.dp_degree,
+                            "inflight": s.sched_cfg.inflight_samples} for s in sg.stages],
+                "l2": "per-step working set (weights+master+grads ~2.9 GB) >> 126 MB L2",
+                "optimizer": "SGD fp32 master + bf16 shadow", "plan_s": round(t_plan, 3),
+            },
+            "e2e": {"value": round(e2e, 3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d_bytes),
+                    "d2h_bytes_per_step": 4},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05 bf16 GEMM, all dense fw/dgrad/wgrad)",
+                         "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+                         "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
+                         "peak_source": f"{peak_src} bf16_tflops_sustained",
+                         "share_of_step": round(gemm_share, 4),
+                         "by_kind": summ.get("by_kind", {})},
+            "clocks": clk,
+            "sim": {"iteration_ms_model": round(sim.iteration_ms, 4), "bubble_fraction_model": round(sim.bubble_fraction, 4)},
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+        if os.environ.get("GPP_BENCH_DETAIL"):
+            print(json.dumps({"gemm_by_shape": summ.get("by_shape", {})}), file=sys.stderr)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

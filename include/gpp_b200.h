@@ -94,9 +94,9 @@ int gpp_gemm(void* c, int64_t ldc, const void* a, int64_t lda, int a_mn, const v
 
 /* ---- heads and losses (Appendix B tails; SURVEY.md §2.3 note B) --------- */
 
-/* out[m] = dot(x[m,:K], w[:K]) + bias0   (fp32 out; x in dtype). */
-int gpp_rowdot_fwd(float* out, const void* x, int64_t ldx, const float* w, float bias0, int64_t M,
-                   int64_t K, int dtype, void* stream);
+/* out[m] = dot(x[m,:K], w[:K]) + bias[0]   (fp32 out; x in dtype; bias may be NULL). */
+int gpp_rowdot_fwd(float* out, const void* x, int64_t ldx, const float* w, const float* bias,
+                   int64_t M, int64_t K, int dtype, void* stream);
 /* dx[m,k] = dout[m] * w[k] * act'(saved[m,k]);  dw[k] (+)= sum_m dout[m] x[m,k];
  * dbias[0] (+)= sum_m dout[m]. */
 int gpp_rowdot_bwd(void* dx, int64_t lddx, float* dw, float* dbias, const float* dout,

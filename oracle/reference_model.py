@@ -1,0 +1,83 @@
+"""TEST INFRASTRUCTURE ONLY.  Monolithic torch-CPU model of a workload.
+
+The numerics oracle for the pipelined executor (BASELINE.json north_star:
+"per-step loss and parameter gradients must match within rtol 2e-2 in bf16
+(1e-4 in fp32)").  No pipeline, no micro-batches, no stages: the whole
+mini-batch through the computation graph in op order, autograd for the
+gradients.  For bf16 workloads it rounds exactly where the device path stores
+bf16 (weights used by GEMMs, every layer output); gradients flow straight-
+through the roundings, and all math is fp32.
+
+Also the CPU baseline of bench.py (``--impl reference`` / ``cpu_baseline``):
+the training step the reference would run on host cores.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from paper_2406_17145_b200.runtime.executor import init_params
+
+
+def _round(t, bf16: bool):
+    if not bf16:
+        return t
+    return t + (t.to(torch.bfloat16).float() - t).detach()
+
+
+class ReferenceModel:
+    def __init__(self, wl, seed: int = 0):
+        self.wl = wl
+        self.bf16 = wl.dtype != "fp32"
+        self.params: dict[tuple[int, str], torch.Tensor] = {}
+        for o in wl.graph.topo_order:
+            for name, t in init_params(wl.layers[o], o, seed):
+                self.params[(o, name)] = t.clone().requires_grad_(True)
+
+    def loss(self, batch: dict[str, torch.Tensor]) -> torch.Tensor:
+        wl, g, P = self.wl, self.wl.graph, self.params
+        B = wl.mini_batch
+        out: dict[int, torch.Tensor] = {}
+        total = None
+        for o in g.topo_order:
+            spec = wl.layers[o]
+            if spec.data_key is not None:
+                x = _round(batch[spec.data_key].float(), self.bf16)
+            else:
+                preds = g.predecessors(o)
+                x = out[preds[0]] if len(preds) == 1 else None
+            if spec.kind == "dense":
+                w = _round(P[(o, "w")], self.bf16)
+                z = x @ w.t() + P[(o, "b")]
+                y = torch.relu(z) if spec.act == "relu" else (torch.nn.functional.gelu(z) if spec.act == "gelu" else z)
+                out[o] = _round(y, self.bf16)
+            elif spec.kind == "concat":
+                out[o] = torch.cat([out[u] for u in g.predecessors(o)], dim=1)
+            elif spec.kind == "mse_head":
+                pred = x @ P[(o, "w")] + P[(o, "b")][0]
+                l = ((pred - batch[spec.label_key].float()) ** 2).sum() / B
+                total = l if total is None else total + l
+            elif spec.kind == "bce_head":
+                z = x @ P[(o, "w")] + P[(o, "b")][0]
+                l = torch.nn.functional.binary_cross_entropy_with_logits(z, batch[spec.label_key].float(), reduction="sum") / B
+                total = l if total is None else total + l
+            elif spec.kind == "ce_head":
+                w = _round(P[(o, "w")], self.bf16)
+                logits = _round(x @ w.t() + P[(o, "b")], self.bf16)
+                l = torch.nn.functional.cross_entropy(logits, batch[spec.label_key], reduction="sum") / B
+                total = l if total is None else total + l
+            else:
+                raise NotImplementedError(spec.kind)
+        return total
+
+    def step(self, batch, lr: float):
+        """loss, grads (dict) and the SGD update applied in place."""
+        for p in self.params.values():
+            p.grad = None
+        loss = self.loss(batch)
+        loss.backward()
+        grads = {k: p.grad.detach().clone() for k, p in self.params.items()}
+        with torch.no_grad():
+            for p in self.params.values():
+                p.sub_(lr * p.grad)
+        return loss.detach(), grads

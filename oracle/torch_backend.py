@@ -1,0 +1,112 @@
+"""TEST INFRASTRUCTURE ONLY.  torch-CPU restatement of the executor kernel interface.
+
+Same method signatures and numeric contract as ``runtime.backend.CudaBackend``
+(include/gpp_b200.h): fp32 math, results rounded to the destination dtype.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+
+def _act(z, act):
+    if act == "relu":
+        return torch.relu(z)
+    if act == "gelu":
+        return torch.nn.functional.gelu(z)
+    return z
+
+
+def _dact(saved, act):
+    s = saved.float()
+    if act == "relu":
+        return (s > 0).float()
+    if act == "gelu":
+        cdf = 0.5 * (1.0 + torch.erf(s / math.sqrt(2.0)))
+        pdf = torch.exp(-0.5 * s * s) / math.sqrt(2.0 * math.pi)
+        return cdf + s * pdf
+    return torch.ones_like(s)
+
+
+class TorchBackend:
+    name = "torch-cpu"
+
+    def __init__(self, device="cpu"):
+        self.device = torch.device(device)
+
+    def linear_fwd(self, y, x, w, bias, act, residual=None, pre=None):
+        z = x.float() @ w.float().t()
+        if bias is not None:
+            z = z + bias
+        if pre is not None:
+            pre.copy_(z)
+        out = _act(z, act)
+        if residual is not None:
+            out = out + residual.float()
+        y.copy_(out)
+
+    def linear_dgrad(self, dx, dy, w, saved, act):
+        v = dy.float() @ w.float()
+        if act != "none":
+            v = v * _dact(saved, act)
+        dx.copy_(v)
+
+    def linear_wgrad(self, dw, db, dy, x, accumulate):
+        v = dy.float().t() @ x.float()
+        if accumulate:
+            dw.add_(v)
+        else:
+            dw.copy_(v)
+        if db is not None:
+            s = dy.float().sum(0)
+            if accumulate:
+                db.add_(s)
+            else:
+                db.copy_(s)
+
+    def rowdot_fwd(self, out, x, w, bias):
+        v = x.float() @ w
+        if bias is not None:
+            v = v + bias[0]
+        out.copy_(v)
+
+    def rowdot_bwd(self, dx, dw, db, dout, x, w, saved, act, accumulate):
+        if dx is not None:
+            v = dout[:, None] * w[None, :]
+            if act != "none":
+                v = v * _dact(saved, act)
+            dx.copy_(v)
+        if dw is not None:
+            v = dout @ x.float()
+            dw.add_(v) if accumulate else dw.copy_(v)
+        if db is not None:
+            v = dout.sum().reshape(1)
+            db.add_(v) if accumulate else db.copy_(v)
+
+    def mse_loss(self, loss_acc, dpred, pred, y, scale):
+        d = pred - y
+        loss_acc.add_(scale * (d * d).sum())
+        dpred.copy_(2.0 * scale * d)
+
+    def bce_loss(self, loss_acc, dz, z, y, scale):
+        l = torch.clamp(z, min=0) - z * y + torch.log1p(torch.exp(-z.abs()))
+        loss_acc.add_(scale * l.sum())
+        dz.copy_(scale * (torch.sigmoid(z) - y))
+
+    def ce_loss(self, loss_acc, dlogits, logits, labels, scale):
+        lf = logits.float()
+        lse = torch.logsumexp(lf, dim=1)
+        loss_acc.add_(scale * (lse - lf.gather(1, labels[:, None]).squeeze(1)).sum())
+        p = torch.softmax(lf, dim=1)
+        p[torch.arange(lf.shape[0]), labels] -= 1.0
+        dlogits.copy_(scale * p)
+
+    def copy_rows(self, dst, src):
+        dst.copy_(src)
+
+    def sgd_step(self, master, shadow, grad, lr):
+        master.sub_(lr * grad)
+        if shadow is not None:
+            shadow.copy_(master)

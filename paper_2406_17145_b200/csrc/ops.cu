@@ -70,8 +70,8 @@ __device__ float block_max(float v) {
 
 // ---------------- heads ----------------
 template <typename T>
-__global__ void rowdot_fwd_kernel(float* out, const T* x, int64_t ldx, const float* w, float b0,
-                                  int64_t M, int64_t K) {
+__global__ void rowdot_fwd_kernel(float* out, const T* x, int64_t ldx, const float* w,
+                                  const float* bias, int64_t M, int64_t K) {
   const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -79,7 +79,7 @@ __global__ void rowdot_fwd_kernel(float* out, const T* x, int64_t ldx, const flo
   float s = 0.f;
   for (int64_t k = lane; k < K; k += 32) s = fmaf(to_f<T>(xr[k]), w[k], s);
   s = warp_sum(s);
-  if (lane == 0) out[row] = s + b0;
+  if (lane == 0) out[row] = s + (bias ? bias[0] : 0.f);
 }
 
 template <typename T>
@@ -278,15 +278,15 @@ int gpp_gemm(void* c, int64_t ldc, const void* a, int64_t lda, int a_mn, const v
   return gemm_any(epi, a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, dtype, stream);
 }
 
-int gpp_rowdot_fwd(float* out, const void* x, int64_t ldx, const float* w, float bias0, int64_t M,
-                   int64_t K, int dtype, void* stream) {
+int gpp_rowdot_fwd(float* out, const void* x, int64_t ldx, const float* w, const float* bias,
+                   int64_t M, int64_t K, int dtype, void* stream) {
   GPP_ARG_CHECK(out && x && w && M > 0 && K > 0, "bad argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int blocks = static_cast<int>((M + 7) / 8);
   if (dtype == GPP_BF16)
-    rowdot_fwd_kernel<bf16><<<blocks, 256, 0, s>>>(out, static_cast<const bf16*>(x), ldx, w, bias0, M, K);
+    rowdot_fwd_kernel<bf16><<<blocks, 256, 0, s>>>(out, static_cast<const bf16*>(x), ldx, w, bias, M, K);
   else
-    rowdot_fwd_kernel<float><<<blocks, 256, 0, s>>>(out, static_cast<const float*>(x), ldx, w, bias0, M, K);
+    rowdot_fwd_kernel<float><<<blocks, 256, 0, s>>>(out, static_cast<const float*>(x), ldx, w, bias, M, K);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }

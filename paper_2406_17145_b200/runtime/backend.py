@@ -1,0 +1,60 @@
+"""Kernel backend of the stage executor: every compute op goes to libgpp_b200.so.
+
+The executor (``runtime.executor``) is written against this small tensor-level
+interface.  ``CudaBackend`` is the only product implementation; the torch-CPU
+restatement with identical signatures lives in ``oracle/torch_backend.py`` and
+is used by tests only (multi-rank gloo tests of the executor's host logic).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import lib
+
+
+class CudaBackend:
+    name = "cuda"
+
+    def __init__(self, device: torch.device | int | str):
+        if not torch.cuda.is_available():
+            raise RuntimeError("CudaBackend needs a CUDA device (there is no CPU fallback)")
+        self.device = torch.device(device) if not isinstance(device, int) else torch.device("cuda", device)
+        lib.load()
+
+    # stream plumbing -------------------------------------------------------
+    def current_stream(self):
+        return torch.cuda.current_stream(self.device)
+
+    # dense operator --------------------------------------------------------
+    def linear_fwd(self, y, x, w, bias, act, residual=None, pre=None):
+        lib.linear_fwd(y, x, w, bias=bias, act=act, residual=residual, pre=pre)
+
+    def linear_dgrad(self, dx, dy, w, saved, act):
+        lib.linear_dgrad(dx, dy, w, saved=saved, act=act)
+
+    def linear_wgrad(self, dw, db, dy, x, accumulate):
+        lib.linear_wgrad(dw, db, dy, x, accumulate=accumulate)
+
+    # heads / losses --------------------------------------------------------
+    def rowdot_fwd(self, out, x, w, bias):
+        lib.rowdot_fwd(out, x, w, bias)
+
+    def rowdot_bwd(self, dx, dw, db, dout, x, w, saved, act, accumulate):
+        lib.rowdot_bwd(dx, dw, db, dout, x, w, saved=saved, act=act, accumulate=accumulate)
+
+    def mse_loss(self, loss_acc, dpred, pred, y, scale):
+        lib.mse_loss(loss_acc, dpred, pred, y, scale)
+
+    def bce_loss(self, loss_acc, dz, z, y, scale):
+        lib.bce_loss(loss_acc, dz, z, y, scale)
+
+    def ce_loss(self, loss_acc, dlogits, logits, labels, scale):
+        lib.ce_loss(loss_acc, dlogits, logits, labels, scale)
+
+    # data movement / optimizer --------------------------------------------
+    def copy_rows(self, dst, src):
+        lib.copy_rows(dst, src)
+
+    def sgd_step(self, master, shadow, grad, lr):
+        lib.sgd_step(master, shadow, grad, lr)

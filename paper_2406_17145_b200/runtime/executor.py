@@ -1,0 +1,433 @@
+"""GPP stage executor: runs a configured StageGraph for real, one process per GPU.
+
+This is the hot path the reference delegates to FlexFlow (
+out of scope in SPEC.md:8).  Its contract is the simulator's semantics
+(``sim.simulate``):
+
+* rank r runs the stage S with r in S.devices; inside a DP stage of degree d,
+  DP index q owns rows [q*b/d, (q+1)*b/d) of every micro-batch (cost.py:61);
+* the stage executes its task list Pi strictly in order;
+* fw(y, j) consumes every predecessor's outputs covering samples
+  [j*b_y, (j+1)*b_y); bw(x, j) every successor's gradients covering x's range
+  — realised as *pieces*: intersections of producer (task, rank) row ranges
+  with consumer (task, rank) row ranges, each moved by one P2P message;
+* activations live in rings of l = peak-in-flight slots indexed j mod l
+  (kFkB never holds more than l micro-batches);
+* after the last task, DP stages all-reduce their flat gradient buffer once
+  (NCCL), then one fused SGD kernel updates master weights + bf16 shadows.
+
+Transport: ``torch.distributed`` P2P (NCCL over NVLink on B200) with one
+process group per ordered rank pair and direction, so forward and backward
+streams never serialise against each other; pieces on a pair are posted in
+global sample order on both sides, which is what makes NCCL's in-order
+matching correct.  Compute: every kernel goes through the ``backend`` (the
+sm_100a C-ABI library in production).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from ..model import Stage, StageGraph
+from ..workloads import LayerSpec, Workload
+
+__all__ = ["Piece", "build_pieces", "Executor", "init_params"]
+
+_ALIGN = 64  # elements; keeps every parameter view 128-byte aligned (TMA needs 16 B)
+
+
+@dataclass(frozen=True)
+class Piece:
+    tensor: int          # producer op id
+    producer: int        # rank
+    consumer: int        # rank
+    p_task: int
+    c_task: int
+    p_row0: int          # row offset inside the producer's rank-local micro-batch block
+    c_row0: int          # row offset inside the consumer's rank-local micro-batch block
+    rows: int
+    start: int           # global sample index of the first row (ordering key)
+
+
+def _rank_rows(st: Stage, rank: int) -> tuple[int, int]:
+    devs = sorted(st.devices)
+    q = devs.index(rank)
+    m = st.micro_batch // len(devs)
+    return q * m, m
+
+
+def build_pieces(prod: Stage, cons: Stage, tensors: list[int], B: int) -> list[Piece]:
+    """All (producer task, rank) x (consumer task, rank) row-range intersections."""
+    out: list[Piece] = []
+    bp, bc = prod.micro_batch, cons.micro_batch
+    for p in sorted(prod.devices):
+        p_off, mp = _rank_rows(prod, p)
+        for c in sorted(cons.devices):
+            c_off, mc = _rank_rows(cons, c)
+            for i in range(B // bp):
+                lo_p = i * bp + p_off
+                hi_p = lo_p + mp
+                for j in range(lo_p // bc, (hi_p - 1) // bc + 1):
+                    lo_c = j * bc + c_off
+                    hi_c = lo_c + mc
+                    s, e = max(lo_p, lo_c), min(hi_p, hi_c)
+                    if s >= e:
+                        continue
+                    for t in tensors:
+                        out.append(Piece(t, p, c, i, j, s - lo_p, s - lo_c, e - s, s))
+    return out
+
+
+def _order(pieces):
+    return sorted(pieces, key=lambda pc: (pc.start, pc.tensor))
+
+
+def init_params(spec: LayerSpec, op_id: int, seed: int) -> list[tuple[str, torch.Tensor]]:
+    """Deterministic fp32 parameters of one op (CPU generator per (seed, op))."""
+    g = torch.Generator().manual_seed(seed * 1_000_003 + op_id * 7919 + 17)
+    if spec.kind == "dense" or spec.kind == "ce_head":
+        w = torch.randn(spec.out_dim, spec.in_dim, generator=g) / spec.in_dim**0.5
+        b = torch.randn(spec.out_dim, generator=g) * 0.01
+        return [("w", w), ("b", b)]
+    if spec.kind in ("mse_head", "bce_head"):
+        w = torch.randn(spec.in_dim, generator=g) / spec.in_dim**0.5
+        b = torch.randn(1, generator=g) * 0.01
+        return [("w", w), ("b", b)]
+    return []
+
+
+def _width(spec: LayerSpec) -> int:
+    return spec.out_dim
+
+
+class Executor:
+    """One rank's share of a GPP strategy."""
+
+    def __init__(self, wl: Workload, sg: StageGraph, rank: int, world: int, backend,
+                 lr: float = 1e-3, seed: int = 0, use_dist: bool | None = None):
+        self.wl, self.sg, self.rank, self.world, self.be = wl, sg, rank, world, backend
+        self.lr = float(lr)
+        self.seed = seed
+        self.B = sg.mini_batch
+        self.dev = backend.device
+        self.dtype = torch.float32 if wl.dtype == "fp32" else torch.bfloat16
+        self.use_dist = (world > 1) if use_dist is None else use_dist
+        g = wl.graph
+        self.owner = {op: st.id for st in sg.stages for op in st.op_ids}
+        mine = [st for st in sg.stages if rank in st.devices]
+        self.stage: Stage | None = mine[0] if mine else None
+        self._make_groups()
+        if self.stage is None:
+            return
+        st = self.stage
+        self.d = st.dp_degree
+        self.row_off, self.m = _rank_rows(st, rank)
+        self.n = self.B // st.micro_batch
+        # ring depth = peak in-flight micro-batches along Pi
+        live = hi = 0
+        for t in st.schedule:
+            live += 1 if t.direction == "fw" else -1
+            hi = max(hi, live)
+        self.ell = max(1, hi)
+        self.ops = [o for o in g.topo_order if o in st.op_ids]
+        self.layers = {o: wl.layers[o] for o in self.ops}
+        for o in self.ops:
+            succ = g.successors(o)
+            if len(succ) > 1:
+                raise NotImplementedError(f"op {o} fans out to {len(succ)} consumers (unsupported)")
+        self._build_plan()
+        self._alloc_params()
+        self._alloc_buffers()
+
+    # ------------------------------------------------------------------ plan
+    def _make_groups(self):
+        """Process groups: one per ordered (src, dst) rank pair with traffic, one per DP stage.
+        Every rank creates every group in the same order (torch.distributed requirement)."""
+        self.p2p_groups: dict[tuple[int, int], object] = {}
+        self.dp_group = None
+        if not self.use_dist:
+            return
+        g = self.wl.graph
+        pairs = set()
+        for (a, b) in sorted(self.sg.edges):
+            sa, sb = self.sg.by_id[a], self.sg.by_id[b]
+            for p in sa.devices:
+                for c in sb.devices:
+                    pairs.add((p, c))
+                    pairs.add((c, p))
+        for (a, b) in sorted(pairs):
+            grp = dist.new_group(ranks=sorted({a, b}))
+            self.p2p_groups[(a, b)] = grp
+        for st in self.sg.stages:
+            if st.dp_degree > 1:
+                grp = dist.new_group(ranks=sorted(st.devices))
+                if self.rank in st.devices:
+                    self.dp_group = grp
+
+    def _build_plan(self):
+        g = self.wl.graph
+        st = self.stage
+        mine = set(self.ops)
+        # remote producers of local consumers / local producers with remote consumers
+        self.in_remote: dict[int, int] = {}     # producer op -> producer stage id
+        self.out_remote: dict[int, int] = {}    # local op -> consumer stage id
+        for o in self.ops:
+            for u in g.predecessors(o):
+                if u not in mine:
+                    self.in_remote[u] = self.owner[u]
+            for v in g.successors(o):
+                if v not in mine:
+                    self.out_remote[o] = self.owner[v]
+        self.recv_fw = {j: [] for j in range(self.n)}
+        self.send_fw = {j: [] for j in range(self.n)}
+        by_stage_in: dict[int, list[int]] = {}
+        for u, sid in self.in_remote.items():
+            by_stage_in.setdefault(sid, []).append(u)
+        for sid, tensors in by_stage_in.items():
+            for pc in build_pieces(self.sg.by_id[sid], st, sorted(tensors), self.B):
+                if pc.consumer == self.rank:
+                    self.recv_fw[pc.c_task].append(pc)
+        by_stage_out: dict[int, list[int]] = {}
+        for u, sid in self.out_remote.items():
+            by_stage_out.setdefault(sid, []).append(u)
+        for sid, tensors in by_stage_out.items():
+            for pc in build_pieces(st, self.sg.by_id[sid], sorted(tensors), self.B):
+                if pc.producer == self.rank:
+                    self.send_fw[pc.p_task].append(pc)
+        for j in range(self.n):
+            self.recv_fw[j] = _order(self.recv_fw[j])
+            self.send_fw[j] = _order(self.send_fw[j])
+        self.first_bw = next(t.index for t in st.schedule if t.direction == "bw")
+
+    def eff_act(self, u: int) -> str:
+        spec = self.wl.layers[u]
+        if spec.kind == "dense":
+            return spec.act
+        if spec.kind == "concat":
+            acts = {self.eff_act(p) for p in self.wl.graph.predecessors(u)}
+            if len(acts) != 1:
+                raise NotImplementedError("concat of inputs with different activations")
+            return acts.pop()
+        return "none"
+
+    # ---------------------------------------------------------------- memory
+    def _alloc_params(self):
+        specs = []
+        total = 0
+        for o in self.ops:
+            for name, t in init_params(self.layers[o], o, self.seed):
+                specs.append((o, name, t))
+                total += -(-t.numel() // _ALIGN) * _ALIGN
+        total = max(total, _ALIGN)
+        self.master = torch.zeros(total, dtype=torch.float32, device=self.dev)
+        self.grad = torch.zeros(total, dtype=torch.float32, device=self.dev)
+        self.shadow = torch.zeros(total, dtype=torch.bfloat16, device=self.dev) if self.dtype == torch.bfloat16 else None
+        self.P: dict[tuple[int, str], torch.Tensor] = {}     # fp32 master views
+        self.G: dict[tuple[int, str], torch.Tensor] = {}     # fp32 grad views
+        self.W: dict[tuple[int, str], torch.Tensor] = {}     # compute-dtype weight views
+        off = 0
+        for o, name, t in specs:
+            n = t.numel()
+            self.master[off:off + n].copy_(t.reshape(-1))
+            self.P[(o, name)] = self.master[off:off + n].view(t.shape)
+            self.G[(o, name)] = self.grad[off:off + n].view(t.shape)
+            if self.shadow is not None:
+                self.W[(o, name)] = self.shadow[off:off + n].view(t.shape)
+            else:
+                self.W[(o, name)] = self.P[(o, name)]
+            off += -(-n // _ALIGN) * _ALIGN
+        if self.shadow is not None:
+            self.shadow.copy_(self.master.to(torch.bfloat16))
+        self.param_count = sum(t.numel() for _, _, t in specs)
+
+    def _ring(self, shape, dtype=None):
+        return [torch.zeros(shape, dtype=dtype or self.dtype, device=self.dev) for _ in range(self.ell)]
+
+    def _alloc_buffers(self):
+        m, g = self.m, self.wl.graph
+        self.out, self.recv, self.gbuf, self.grecv, self.gsend = {}, {}, {}, {}, {}
+        self.pred, self.dpred = {}, {}
+        for o in self.ops:
+            spec = self.layers[o]
+            if spec.kind in ("dense", "concat"):
+                self.out[o] = self._ring((m, _width(spec)))
+                if o in self.out_remote:
+                    self.grecv[o] = self._ring((m, _width(spec)))
+                elif g.successors(o):
+                    self.gbuf[o] = self._ring((m, _width(spec)))
+            elif spec.kind in ("mse_head", "bce_head"):
+                self.pred[o] = self._ring((m,), torch.float32)
+                self.dpred[o] = self._ring((m,), torch.float32)
+            elif spec.kind == "ce_head":
+                self.pred[o] = self._ring((m, spec.out_dim))
+                self.dpred[o] = self._ring((m, spec.out_dim))
+            else:
+                raise NotImplementedError(f"layer kind {spec.kind}")
+        for u in self.in_remote:
+            w = _width(self.wl.layers[u])
+            self.recv[u] = self._ring((m, w))
+            self.gsend[u] = self._ring((m, w))
+        self.loss_acc = torch.zeros(1, dtype=torch.float32, device=self.dev)
+        self._send_works: dict[tuple, list] = {}
+
+    # ------------------------------------------------------------ data access
+    def local_rows(self, key_tensor_full: torch.Tensor) -> torch.Tensor:
+        """This rank's rows of a full [B, ...] batch tensor, in (task, row) order."""
+        b = self.stage.micro_batch
+        idx = torch.cat([torch.arange(j * b + self.row_off, j * b + self.row_off + self.m) for j in range(self.n)])
+        return key_tensor_full.index_select(0, idx)
+
+    def data_keys(self) -> list[str]:
+        keys = []
+        for o in self.ops:
+            s = self.layers[o]
+            for k in (s.data_key, s.label_key):
+                if k is not None:
+                    keys.append(k)
+        return keys
+
+    def _x_of(self, u: int, slot: int) -> torch.Tensor:
+        return self.out[u][slot] if u in self.out else self.recv[u][slot]
+
+    def _input(self, o: int, j: int, slot: int, batch) -> torch.Tensor:
+        spec = self.layers[o]
+        if spec.data_key is not None:
+            return batch[spec.data_key][j * self.m:(j + 1) * self.m]
+        preds = self.wl.graph.predecessors(o)
+        if len(preds) != 1:
+            raise NotImplementedError(f"op {o} ({spec.kind}) needs exactly one input")
+        return self._x_of(preds[0], slot)
+
+    def _dx_target(self, u: int, slot: int) -> torch.Tensor:
+        return self.gbuf[u][slot] if u in self.gbuf else self.gsend[u][slot]
+
+    def _dz_of(self, o: int, slot: int) -> torch.Tensor:
+        return self.grecv[o][slot] if o in self.grecv else self.gbuf[o][slot]
+
+    # ------------------------------------------------------------- transport
+    def _grp(self, a: int, b: int):
+        return self.p2p_groups[(a, b)]
+
+    def _wait_sends(self, key):
+        for w in self._send_works.pop(key, []):
+            w.wait()
+
+    # ---------------------------------------------------------------- tasks
+    def _fw(self, j: int, batch):
+        be, slot = self.be, j % self.ell
+        works = []
+        for pc in self.recv_fw[j]:
+            buf = self.recv[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows]
+            works.append(dist.irecv(buf, src=pc.producer, group=self._grp(pc.producer, self.rank)))
+        for w in works:
+            w.wait()
+        self._wait_sends(("fw", slot))
+        scale = 1.0 / self.B
+        for o in self.ops:
+            spec = self.layers[o]
+            if spec.kind == "dense":
+                x = self._input(o, j, slot, batch)
+                be.linear_fwd(self.out[o][slot], x, self.W[(o, "w")], self.P[(o, "b")], spec.act)
+            elif spec.kind == "concat":
+                off = 0
+                for u in self.wl.graph.predecessors(o):
+                    w_u = _width(self.wl.layers[u])
+                    be.copy_rows(self.out[o][slot][:, off:off + w_u], self._x_of(u, slot))
+                    off += w_u
+            elif spec.kind in ("mse_head", "bce_head"):
+                x = self._input(o, j, slot, batch)
+                be.rowdot_fwd(self.pred[o][slot], x, self.P[(o, "w")], self.P[(o, "b")])
+                y = batch[spec.label_key][j * self.m:(j + 1) * self.m]
+                loss = be.mse_loss if spec.kind == "mse_head" else be.bce_loss
+                loss(self.loss_acc, self.dpred[o][slot], self.pred[o][slot], y, scale)
+            elif spec.kind == "ce_head":
+                x = self._input(o, j, slot, batch)
+                be.linear_fwd(self.pred[o][slot], x, self.W[(o, "w")], self.P[(o, "b")], "none")
+                lab = batch[spec.label_key][j * self.m:(j + 1) * self.m]
+                be.ce_loss(self.loss_acc, self.dpred[o][slot], self.pred[o][slot], lab, scale)
+        sends = []
+        for pc in self.send_fw[j]:
+            buf = self.out[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows]
+            sends.append(dist.isend(buf, dst=pc.consumer, group=self._grp(self.rank, pc.consumer)))
+        if sends:
+            self._send_works[("fw", slot)] = sends
+
+    def _bw(self, j: int, batch, accumulate: bool):
+        be, slot = self.be, j % self.ell
+        works = []
+        for pc in self.send_fw[j]:  # grads come back along the forward pieces of task j
+            buf = self.grecv[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows]
+            works.append(dist.irecv(buf, src=pc.consumer, group=self._grp(pc.consumer, self.rank)))
+        for w in works:
+            w.wait()
+        self._wait_sends(("bw", slot))
+        g = self.wl.graph
+        for o in reversed(self.ops):
+            spec = self.layers[o]
+            preds = g.predecessors(o)
+            needs_dx = spec.data_key is None and len(preds) == 1
+            if spec.kind == "dense":
+                x = self._input(o, j, slot, batch)
+                dz = self._dz_of(o, slot)
+                be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
+                if needs_dx:
+                    u = preds[0]
+                    be.linear_dgrad(self._dx_target(u, slot), dz, self.W[(o, "w")], x, self.eff_act(u))
+            elif spec.kind == "concat":
+                dz = self._dz_of(o, slot)
+                off = 0
+                for u in preds:
+                    w_u = _width(self.wl.layers[u])
+                    be.copy_rows(self._dx_target(u, slot), dz[:, off:off + w_u])
+                    off += w_u
+            elif spec.kind in ("mse_head", "bce_head"):
+                x = self._input(o, j, slot, batch)
+                u = preds[0] if needs_dx else None
+                dx = self._dx_target(u, slot) if needs_dx else None
+                be.rowdot_bwd(dx, self.G[(o, "w")], self.G[(o, "b")], self.dpred[o][slot], x,
+                              self.P[(o, "w")], x, self.eff_act(u) if needs_dx else "none", accumulate)
+            elif spec.kind == "ce_head":
+                x = self._input(o, j, slot, batch)
+                dl = self.dpred[o][slot]
+                be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dl, x, accumulate)
+                if needs_dx:
+                    u = preds[0]
+                    be.linear_dgrad(self._dx_target(u, slot), dl, self.W[(o, "w")], x, self.eff_act(u))
+        sends = []
+        for pc in self.recv_fw[j]:  # our input gradients go back along task j's forward pieces
+            buf = self.gsend[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows]
+            sends.append(dist.isend(buf, dst=pc.producer, group=self._grp(self.rank, pc.producer)))
+        if sends:
+            self._send_works[("bw", slot)] = sends
+
+    # ------------------------------------------------------------ iteration
+    def run_iteration(self, batch: dict[str, torch.Tensor], step_optimizer: bool = True):
+        """One synchronous training iteration (all tasks of Pi, DP all-reduce, SGD).
+
+        ``batch`` maps data keys to this rank's rows ([B/d, ...] on the device).
+        Returns the device loss accumulator (head stages) or None.
+        """
+        if self.stage is None:
+            return None
+        self.loss_acc.zero_()
+        seen_bw = False
+        for t in self.stage.schedule:
+            if t.direction == "fw":
+                self._fw(t.index, batch)
+            else:
+                self._bw(t.index, batch, accumulate=seen_bw)
+                seen_bw = True
+        for key in list(self._send_works):
+            self._wait_sends(key)
+        if self.d > 1:
+            dist.all_reduce(self.grad, group=self.dp_group)
+        if step_optimizer:
+            self.be.sgd_step(self.master, self.shadow, self.grad, self.lr)
+        return self.loss_acc
+
+    @property
+    def is_head(self) -> bool:
+        return self.stage is not None and any(self.layers[o].kind.endswith("_head") for o in self.ops)

@@ -31,7 +31,7 @@ _SIGS = {
     "gpp_linear_dgrad": ([_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_linear_wgrad": ([_vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_gemm": ([_vp, _i64, _vp, _i64, _i32, _vp, _i64, _i32, _i64, _i64, _i64, _f32, _f32, _i32, _i32, _vp], _i32),
-    "gpp_rowdot_fwd": ([_vp, _vp, _i64, _vp, _f32, _i64, _i64, _i32, _vp], _i32),
+    "gpp_rowdot_fwd": ([_vp, _vp, _i64, _vp, _vp, _i64, _i64, _i32, _vp], _i32),
     "gpp_rowdot_bwd": ([_vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_mse_loss": ([_vp, _vp, _vp, _vp, _i64, _f32, _vp], _i32),
     "gpp_bce_loss": ([_vp, _vp, _vp, _vp, _i64, _f32, _vp], _i32),
@@ -157,9 +157,9 @@ def gemm(c, a, b, a_mn=False, b_mn=False, alpha=1.0, beta=0.0, stream=None):
          M, N, K, float(alpha), float(beta), int(c.dtype == torch.float32), _dt(a), _stream(stream))
 
 
-def rowdot_fwd(out, x, w, bias0: float, stream=None):
+def rowdot_fwd(out, x, w, bias=None, stream=None):
     M, K = x.shape
-    call("gpp_rowdot_fwd", _ptr(out), _ptr(x), _ld(x), _ptr(w), float(bias0), M, K, _dt(x), _stream(stream))
+    call("gpp_rowdot_fwd", _ptr(out), _ptr(x), _ld(x), _ptr(w), _ptr(bias), M, K, _dt(x), _stream(stream))
 
 
 def rowdot_bwd(dx, dw, dbias, dout, x, w, saved=None, act="none", accumulate=False, stream=None):

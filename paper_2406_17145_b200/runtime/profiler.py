@@ -1,0 +1,90 @@
+"""Live kernel timing for the roofline report and measured cost curves.
+
+``TimedBackend`` wraps the CUDA backend and brackets every dense-operator GEMM
+(``linear_fwd``/``linear_dgrad``/``linear_wgrad``) with CUDA events on the
+launching stream, recording algorithmic FLOPs per launch.  ``profile_ops``
+measures fw/bw task times per operator over micro-batch sizes and returns
+table ``CostCurve``s (model.py:18-97) — B200 profiles for the partitioner
+(SURVEY.md §8(f) row 1).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from .backend import CudaBackend
+
+
+@dataclass
+class _Rec:
+    kind: str
+    flops: float
+    m: int
+    n: int
+    k: int
+    start: torch.cuda.Event
+    end: torch.cuda.Event
+
+
+class TimedBackend(CudaBackend):
+    def __init__(self, device):
+        super().__init__(device)
+        self.records: list[_Rec] = []
+        self.enabled = True
+
+    def _timed(self, kind, m, n, k, fn):
+        if not self.enabled:
+            return fn()
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        self.records.append(_Rec(kind, 2.0 * m * n * k, m, n, k, s, e))
+
+    def linear_fwd(self, y, x, w, bias, act, residual=None, pre=None):
+        self._timed("fwd", x.shape[0], w.shape[0], x.shape[1],
+                    lambda: super(TimedBackend, self).linear_fwd(y, x, w, bias, act, residual, pre))
+
+    def linear_dgrad(self, dx, dy, w, saved, act):
+        self._timed("dgrad", dy.shape[0], w.shape[1], dy.shape[1],
+                    lambda: super(TimedBackend, self).linear_dgrad(dx, dy, w, saved, act))
+
+    def linear_wgrad(self, dw, db, dy, x, accumulate):
+        self._timed("wgrad", dy.shape[1], x.shape[1], dy.shape[0],
+                    lambda: super(TimedBackend, self).linear_wgrad(dw, db, dy, x, accumulate))
+
+    def summary(self) -> dict:
+        """Aggregate FLOPs and device time of the recorded GEMM launches (sync first)."""
+        torch.cuda.synchronize()
+        tot_f = tot_ms = 0.0
+        by_kind: dict[str, list[float]] = {}
+        by_shape: dict[tuple, list[float]] = {}
+        for r in self.records:
+            ms = r.start.elapsed_time(r.end)
+            tot_f += r.flops
+            tot_ms += ms
+            agg = by_kind.setdefault(r.kind, [0.0, 0.0, 0])
+            agg[0] += r.flops
+            agg[1] += ms
+            agg[2] += 1
+            sh = by_shape.setdefault((r.kind, r.m, r.n, r.k), [0.0, 0.0, 0])
+            sh[0] += r.flops
+            sh[1] += ms
+            sh[2] += 1
+        return {
+            "launches": len(self.records),
+            "flops": tot_f,
+            "ms": tot_ms,
+            "tflops": (tot_f / (tot_ms * 1e-3) / 1e12) if tot_ms > 0 else 0.0,
+            "by_kind": {k: {"launches": v[2], "tflops": v[0] / (v[1] * 1e-3) / 1e12 if v[1] else 0.0,
+                            "ms": v[1]} for k, v in by_kind.items()},
+            "by_shape": {f"{k[0]}:{k[1]}x{k[2]}x{k[3]}": {"launches": v[2], "avg_us": 1e3 * v[1] / v[2],
+                                                           "tflops": v[0] / (v[1] * 1e-3) / 1e12 if v[1] else 0.0}
+                         for k, v in sorted(by_shape.items())},
+        }
+
+    def reset(self):
+        self.records.clear()

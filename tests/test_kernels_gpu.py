@@ -117,7 +117,7 @@ def test_heads_and_losses(cuda_lib):
         x = torch.randn(M, K, device="cuda", generator=g).to(dtype)
         w = torch.randn(K, device="cuda", generator=g)
         out = torch.empty(M, device="cuda")
-        cuda_lib.rowdot_fwd(out, x, w, 0.25)
+        cuda_lib.rowdot_fwd(out, x, w, torch.full((1,), 0.25, device="cuda"))
         torch.cuda.synchronize()
         assert _rel(out, x.float() @ w + 0.25) < 1e-4
         y = torch.randn(M, device="cuda", generator=g)

@@ -1,0 +1,64 @@
+"""End-to-end numerics: the GPU executor (libgpp_b200.so) vs the CPU oracle.
+
+Per-step loss and every parameter gradient, plus the updated weights after the
+SGD step, for the fp32 toy (rtol 1e-4) and bf16 multi-tower models (rtol 2e-2)
+— the BASELINE.json north_star tolerances.
+"""
+
+import pytest
+import torch
+
+from oracle.reference_model import ReferenceModel
+from paper_2406_17145_b200 import model as M
+from paper_2406_17145_b200 import sched as S
+from paper_2406_17145_b200 import workloads as W
+from paper_2406_17145_b200.runtime.backend import CudaBackend
+from paper_2406_17145_b200.runtime.data import make_batch, to_device_rows
+from paper_2406_17145_b200.runtime.executor import Executor
+
+pytestmark = pytest.mark.gpu
+
+
+def _single_stage(wl, b):
+    return S.schedule_stage_graph(M.StageGraph([M.Stage(0, wl.graph.op_ids, b, frozenset({0}))], [], wl.mini_batch))
+
+
+def _relerr(a, b, fp32: bool) -> float:
+    """fp32: max-abs error / max-abs value.  bf16: Frobenius-norm relative error, which a
+    handful of ReLU masks flipping on near-zero bf16 activations cannot dominate."""
+    a, b = a.double(), b.double()
+    if fp32:
+        return ((a - b).abs().max() / (b.abs().max() + 1e-12)).item()
+    return ((a - b).norm() / (b.norm() + 1e-12)).item()
+
+
+def _check(wl, b, tol, steps=2, lr=0.05):
+    fp32 = wl.dtype == "fp32"
+    dev = torch.device("cuda", 0)
+    ex = Executor(wl, _single_stage(wl, b), 0, 1, CudaBackend(dev), lr=lr)
+    ref = ReferenceModel(wl)
+    for step in range(steps):
+        full = make_batch(wl, step)
+        loss = ex.run_iteration(to_device_rows(ex, full, ex.dtype, dev))
+        torch.cuda.synchronize()
+        rl, rg = ref.step(full, lr)
+        assert abs(loss.item() - rl.item()) <= tol * abs(rl.item()), (step, loss.item(), rl.item())
+        for k, g in rg.items():
+            err = _relerr(ex.G[k].cpu(), g, fp32)
+            assert err < tol, (step, k, err)
+        for k, p in ref.params.items():
+            err = _relerr(ex.P[k].cpu(), p.detach(), fp32)
+            assert err < tol, ("param", step, k, err)
+
+
+def test_toy_fp32_matches_oracle(cuda_lib):
+    _check(W.toy(B=64), 16, 1e-4)
+
+
+def test_small_towers_bf16_matches_oracle(cuda_lib):
+    _check(W.multi_tower("mini", 3, 2, 256, 256, 128, 128), 32, 2e-2)
+
+
+def test_candle_full_width_bf16(cuda_lib):
+    # full CANDLE-Uno layer widths (4096 / 28672 / 1024), small batch for the CPU oracle
+    _check(W.candle(B=64), 32, 2e-2, steps=1)
