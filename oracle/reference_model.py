@@ -70,6 +70,12 @@ class ReferenceModel:
                 raise NotImplementedError(spec.kind)
         return total
 
+    def load_params(self, params: dict):
+        """Re-synchronise to another run's master weights (per-step parity without drift)."""
+        with torch.no_grad():
+            for k, p in self.params.items():
+                p.copy_(params[k].detach().float().cpu().reshape(p.shape))
+
     def step(self, batch, lr: float):
         """loss, grads (dict) and the SGD update applied in place."""
         for p in self.params.values():

@@ -17,118 +17,17 @@
 //                        bias / activation / residual / act'-mask -> global
 // Operand tiles are 128B-swizzled (TMA SWIZZLE_128B == UMMA SWIZZLE_128B).
 #include <cuda.h>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
 #include "gemm.cuh"
+#include "tc_ptx.cuh"
 
 namespace gpp {
 namespace tc {
 
-constexpr int BM = 128;
-constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
 constexpr int NUM_THREADS = 192;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-
-// tcgen05.commit: mbarrier arrive once all previously issued MMAs of this thread completed.
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-
-// Shared-memory matrix descriptor (SM100 "version 1"), SWIZZLE_128B.
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
-  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-  d |= static_cast<uint64_t>(1) << 46;  // descriptor version for sm_100
-  d |= static_cast<uint64_t>(2) << 61;  // layout: SWIZZLE_128B
-  return d;
-}
-
-// Instruction descriptor for kind::f16: bf16 x bf16 -> f32, M=128, N=BN.
-template <int BN, bool A_MN, bool B_MN>
-__host__ __device__ constexpr uint32_t idesc_bf16() {
-  return (1u << 4)                          // D format f32
-         | (1u << 7)                        // A format bf16
-         | (1u << 10)                       // B format bf16
-         | ((A_MN ? 1u : 0u) << 15)         // A major
-         | ((B_MN ? 1u : 0u) << 16)         // B major
-         | (static_cast<uint32_t>(BN >> 3) << 17) |
-         (static_cast<uint32_t>(BM >> 4) << 24);
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-        "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 
 // Epilogue of one thread: 32 consecutive columns [col0, col0+32) of one row.
 template <int EPI>
@@ -331,6 +230,166 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+
+// ------------------------------------------------------------------------
+// Persistent CTA-pair GEMM: cluster (2,1,1), tcgen05.mma.cta_group::2 with
+// M = 256 (128 rows per CTA) x N = BN, TMEM accumulators double-buffered
+// (2 x BN columns) so the epilogue of tile t overlaps the MMAs of tile t+1.
+//   CTA rank r loads A rows [m0 + 128 r, +128) and B rows [n0 + r BN/2, +BN/2);
+//   both CTAs' TMA bytes complete on the leader's full barrier; the leader's
+//   single MMA thread commits (multicast) to both CTAs' empty / accum-full
+//   barriers; all 8 epilogue warps arrive on the leader's accum-empty barrier.
+// ------------------------------------------------------------------------
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
+                        const __grid_constant__ CUtensorMap tma_b, EpiParams ep, int M, int N,
+                        int K) {
+  constexpr int A_BYTES = BM * BK * 2;            // 16 KB: this CTA's 128 rows of A
+  constexpr int B_BYTES = (BN / 2) * BK * 2;      // this CTA's BN/2 rows of B
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;          // two accumulators
+  constexpr uint32_t IDESC = idesc_bf16<BN, A_MN, B_MN, 2 * BM>();
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;       // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;           // [2] (leader's copy is the live one)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = (rank == 0);
+  const int cluster_id = blockIdx.x >> 1;
+  const int num_clusters = gridDim.x >> 1;
+  const int m_tiles = (M + 2 * BM - 1) / (2 * BM);
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs) ----------------
+      uint32_t it = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
+        const int a_row = m_blk * 2 * BM + static_cast<int>(rank) * BM;
+        const int b_row = n_blk * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          uint8_t* a_dst = smem + s * STAGE_BYTES;
+          uint8_t* b_dst = a_dst + A_BYTES;
+          if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
+          if constexpr (!A_MN) {
+            tma_load_2d_pair(a_dst, &tma_a, &full_bar[s], kb * BK, a_row);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c)
+              tma_load_2d_pair(a_dst + c * 8192, &tma_a, &full_bar[s], a_row + c * 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d_pair(b_dst, &tma_b, &full_bar[s], kb * BK, b_row);
+          } else {
+#pragma unroll
+            for (int c = 0; c < (BN / 2) / 64; ++c)
+              tma_load_2d_pair(b_dst + c * 8192, &tma_b, &full_bar[s], b_row + c * 64, kb * BK);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ---------------- MMA issuer (leader CTA only) ----------------
+      uint32_t it = 0, lt = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++lt) {
+        const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+        mbar_wait_cluster(&tempty_bar[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t b_base = a_base + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t a_off = A_MN ? k * 2048 : k * 32;
+            const uint32_t b_off = B_MN ? k * 2048 : k * 32;
+            const uint64_t adesc = sdesc_sw128(a_base + a_off, A_MN ? 8192 : 16, 1024);
+            const uint64_t bdesc = sdesc_sw128(b_base + b_off, B_MN ? 8192 : 16, 1024);
+            umma_bf16_pair(d_tmem, adesc, bdesc, IDESC, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit_pair(&empty_bar[s], 0x3);
+        }
+        umma_commit_pair(&tfull_bar[acc], 0x3);
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5 of both CTAs) ----------------
+    const int q = warp & 3;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    uint32_t lt = 0;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++lt) {
+      const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+      const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
+      mbar_wait(&tfull_bar[acc], aph);
+      tc_fence_after();
+      const int row = m_blk * 2 * BM + static_cast<int>(rank) * BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
+        epilogue_chunk<EPI>(ep, v, row, n_blk * BN + c * 32, M, N);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
 // ------------------------------------------------------------------------
 // Host side: TMA descriptors (cached) and dispatch.
 // ------------------------------------------------------------------------
@@ -443,11 +502,74 @@ static int launch_tc(const void* a, int64_t lda, const void* b, int64_t ldb, con
   return GPP_OK;
 }
 
+
+static bool pair_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GPP_GEMM_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
+static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb,
+                          const EpiParams& ep, int64_t M, int64_t N, int64_t K,
+                          cudaStream_t stream) {
+  CUtensorMap ma, mb;
+  int rc;
+  if (!A_MN) rc = make_map(&ma, a, K, M, lda, BK, BM);
+  else rc = make_map(&ma, a, M, K, lda, 64, BK);
+  if (rc) return rc;
+  if (!B_MN) rc = make_map(&mb, b, K, N, ldb, BK, BN / 2);
+  else rc = make_map(&mb, b, N, K, ldb, 64, BK);
+  if (rc) return rc;
+  constexpr int STAGE_BYTES = (BM + BN / 2) * BK * 2;
+  constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr_set = true;
+  }
+  const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+  int64_t clusters = num_sms() / 2;
+  if (tiles < clusters) clusters = tiles;
+  gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(2 * clusters),
+                                                     NUM_THREADS, SMEM, stream>>>(
+      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("gemm_tc_pair launch: ") + cudaGetErrorString(e));
+    return GPP_ERR_CUDA;
+  }
+  count_launch();
+  return GPP_OK;
+}
+
 template <bool A_MN, bool B_MN, int EPI>
 static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
                        const EpiParams& ep, int64_t M, int64_t N, int64_t K,
                        cudaStream_t stream) {
   const int64_t mb = (M + BM - 1) / BM;
+  if (M > BM && pair_enabled()) {
+    // CTA-pair 256 x BN tiles; BN=128 when 256-wide tiles leave most pairs idle.
+    const int64_t pairs256 = ((M + 255) / 256) * ((N + 255) / 256);
+    if (N > 128 && pairs256 >= 48)
+      return launch_tc_pair<256, 6, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, stream);
+    return launch_tc_pair<128, 8, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, stream);
+  }
   // Prefer the 128x256 tile (full-rate single-CTA UMMA) unless it leaves most SMs idle.
   const int64_t tiles256 = mb * ((N + 255) / 256);
   if (N > 128 && tiles256 >= 96)

@@ -120,6 +120,94 @@ __global__ void colsum_kernel(float* out, const T* x, int64_t ldx, const float* 
   }
 }
 
+
+// Bias-gradient column sums, deterministic two-pass.  Pass 1: block (64 columns x
+// 8 warps) over a row split, lanes read 2 adjacent columns (one 4-byte bf16x2 /
+// 8-byte float2 load -> 128/256 B per warp-row); fixed-order smem reduction into
+// partial[split][col].  Pass 2 sums the partials in split order.
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_part_kernel(float* part, const T* x, int64_t ldx,
+                                                          const float* wts, int64_t M, int64_t N,
+                                                          int64_t rows_per_split) {
+  __shared__ float red[8][65];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 64 + lane * 2;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_split;
+  const int64_t r1 = min(M, r0 + rows_per_split);
+  float s0 = 0.f, s1 = 0.f;
+  if (col + 1 < N && ((ldx & 1) == 0)) {
+    for (int64_t m = r0 + w; m < r1; m += 8) {
+      const T* p = x + m * ldx + col;
+      float a, b;
+      if constexpr (sizeof(T) == 2) {
+        const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(p);
+        a = __low2float(v); b = __high2float(v);
+      } else {
+        const float2 v = *reinterpret_cast<const float2*>(p);
+        a = v.x; b = v.y;
+      }
+      const float wt = wts ? wts[m] : 1.f;
+      s0 = fmaf(wt, a, s0);
+      s1 = fmaf(wt, b, s1);
+    }
+  } else {
+    for (int64_t m = r0 + w; m < r1; m += 8) {
+      const float wt = wts ? wts[m] : 1.f;
+      if (col < N) s0 = fmaf(wt, to_f<T>(x[m * ldx + col]), s0);
+      if (col + 1 < N) s1 = fmaf(wt, to_f<T>(x[m * ldx + col + 1]), s1);
+    }
+  }
+  red[w][lane * 2] = s0;
+  red[w][lane * 2 + 1] = s1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][threadIdx.x];
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * 64 + threadIdx.x;
+    if (c < N) part[static_cast<int64_t>(blockIdx.y) * N + c] = t;
+  }
+}
+
+__global__ void colsum_final_kernel(float* out, const float* part, int splits, int64_t N,
+                                    int accumulate) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  float t = 0.f;
+  for (int s = 0; s < splits; ++s) t += part[static_cast<int64_t>(s) * N + c];
+  out[c] = accumulate ? out[c] + t : t;
+}
+
+// Persistent per-device scratch for the partial sums (allocated on first use, outside
+// any graph capture: the first call happens in warm-up).
+constexpr int64_t kScratchFloats = 4 << 20;
+float* colsum_scratch() {
+  static float* bufs[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!bufs[dev]) cudaMalloc(&bufs[dev], kScratchFloats * sizeof(float));
+  return bufs[dev];
+}
+
+template <typename T>
+int colsum_launch(float* out, const T* x, int64_t ldx, const float* wts, int64_t M, int64_t N,
+                  int accumulate, cudaStream_t s) {
+  const int64_t col_blocks = (N + 63) / 64;
+  int splits = static_cast<int>((148 * 4 + col_blocks - 1) / col_blocks);
+  splits = splits < 1 ? 1 : (splits > 64 ? 64 : splits);
+  if (splits > (M + 63) / 64) splits = static_cast<int>((M + 63) / 64);
+  if (splits < 1) splits = 1;
+  while (splits > 1 && static_cast<int64_t>(splits) * N > kScratchFloats) --splits;
+  float* part = colsum_scratch();
+  if (!part) { set_error("colsum scratch allocation failed"); return GPP_ERR_CUDA; }
+  const int64_t rps = (M + splits - 1) / splits;
+  colsum_part_kernel<T><<<dim3(static_cast<unsigned>(col_blocks), splits), 256, 0, s>>>(part, x, ldx, wts, M, N, rps);
+  GPP_LAUNCH_CHECK();
+  colsum_final_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, s>>>(out, part, splits, N, accumulate);
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
 // ---------------- losses (single block, deterministic reductions) ----------------
 __global__ void mse_kernel(float* loss_acc, float* dpred, const float* pred, const float* y,
                            int64_t M, float scale) {
@@ -308,12 +396,10 @@ int gpp_rowdot_bwd(void* dx, int64_t lddx, float* dw, float* dbias, const float*
     GPP_LAUNCH_CHECK();
   }
   if (dw) {
-    const unsigned g = static_cast<unsigned>((K + 31) / 32);
-    if (dtype == GPP_BF16)
-      colsum_kernel<bf16><<<g, 256, 0, s>>>(dw, static_cast<const bf16*>(x), ldx, dout, M, K, accumulate);
-    else
-      colsum_kernel<float><<<g, 256, 0, s>>>(dw, static_cast<const float*>(x), ldx, dout, M, K, accumulate);
-    GPP_LAUNCH_CHECK();
+    const int rc = dtype == GPP_BF16
+        ? colsum_launch<bf16>(dw, static_cast<const bf16*>(x), ldx, dout, M, K, accumulate, s)
+        : colsum_launch<float>(dw, static_cast<const float*>(x), ldx, dout, M, K, accumulate, s);
+    if (rc) return rc;
   }
   if (dbias) {
     colsum_kernel<float><<<1, 256, 0, s>>>(dbias, dout, 1, nullptr, M, 1, accumulate);
@@ -357,13 +443,9 @@ int gpp_colsum(float* out, const void* x, int64_t ldx, int64_t M, int64_t N, int
                int dtype, void* stream) {
   GPP_ARG_CHECK(out && x && M > 0 && N > 0, "bad argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const unsigned g = static_cast<unsigned>((N + 31) / 32);
-  if (dtype == GPP_BF16)
-    colsum_kernel<bf16><<<g, 256, 0, s>>>(out, static_cast<const bf16*>(x), ldx, nullptr, M, N, accumulate);
-  else
-    colsum_kernel<float><<<g, 256, 0, s>>>(out, static_cast<const float*>(x), ldx, nullptr, M, N, accumulate);
-  GPP_LAUNCH_CHECK();
-  return GPP_OK;
+  return dtype == GPP_BF16
+      ? colsum_launch<bf16>(out, static_cast<const bf16*>(x), ldx, nullptr, M, N, accumulate, s)
+      : colsum_launch<float>(out, static_cast<const float*>(x), ldx, nullptr, M, N, accumulate, s);
 }
 
 int gpp_sgd_step(float* master, void* shadow_bf16, const float* grad, int64_t n, float lr,

@@ -71,6 +71,10 @@ class NoFeasibleStrategy(RuntimeError):
 class PartitionOptions:
     per_stage_schedules: bool = False  # SPEC.md:320 opt-in per-stage (b, k)
     epsilon_rel: float = 1e-3           # eps = 1e-3 * MAXTPS
+    # "spec": stop when t_r - t_l <= eps_rel * MAXTPS.  "relative": stop when
+    # t_r - t_l <= eps_rel * t_r — MAXTPS is priced at the smallest b, where launch overheads
+    # dominate, so the SPEC rule can leave the optimum unresolved by >20% on B200 curves.
+    epsilon_mode: str = "relative"
     weight_multiplier: float = DEFAULT_WEIGHT_MULTIPLIER
     max_exhaustive_branches: int = 6
     micro_batches: tuple[int, ...] | None = None  # restrict b candidates (e.g. fixed-b sweeps)
@@ -388,7 +392,7 @@ def _optimize_on(g_eval: ComputationGraph, g_out: ComputationGraph, cluster: Dev
     if best is None:
         raise NoFeasibleStrategy("no strategy fits the memory budget even at MAXTPS")
     t_l, t_r = 0.0, maxtps
-    while t_r - t_l > eps:
+    while t_r - t_l > (eps if opts.epsilon_mode == "spec" else opts.epsilon_rel * t_r):
         t_m = (t_l + t_r) / 2.0
         cand, st = search_stage_graph(ng, tree, cluster, B, t_m, opts, configs, uniform)
         probes += 1

@@ -248,12 +248,14 @@ class Executor:
 
     def _alloc_buffers(self):
         m, g = self.m, self.wl.graph
-        self.out, self.recv, self.gbuf, self.grecv, self.gsend = {}, {}, {}, {}, {}
+        self.out, self.recv, self.gbuf, self.grecv, self.gsend, self.pre = {}, {}, {}, {}, {}, {}
         self.pred, self.dpred = {}, {}
         for o in self.ops:
             spec = self.layers[o]
             if spec.kind in ("dense", "concat"):
                 self.out[o] = self._ring((m, _width(spec)))
+                if self.eff_act(o) == "gelu":  # GELU' needs the pre-activation downstream
+                    self.pre[o] = self._ring((m, _width(spec)))
                 if o in self.out_remote:
                     self.grecv[o] = self._ring((m, _width(spec)))
                 elif g.successors(o):
@@ -301,6 +303,15 @@ class Executor:
             raise NotImplementedError(f"op {o} ({spec.kind}) needs exactly one input")
         return self._x_of(preds[0], slot)
 
+    def _saved_for(self, u: int, x: torch.Tensor, slot: int):
+        """act'-saved tensor of producer u: its output for RELU, its pre-activation for GELU."""
+        act = self.eff_act(u)
+        if act == "gelu":
+            if u not in self.pre:
+                raise NotImplementedError(f"GELU pre-activation of op {u} is not on this stage")
+            return self.pre[u][slot], act
+        return x, act
+
     def _dx_target(self, u: int, slot: int) -> torch.Tensor:
         return self.gbuf[u][slot] if u in self.gbuf else self.gsend[u][slot]
 
@@ -330,12 +341,17 @@ class Executor:
             spec = self.layers[o]
             if spec.kind == "dense":
                 x = self._input(o, j, slot, batch)
-                be.linear_fwd(self.out[o][slot], x, self.W[(o, "w")], self.P[(o, "b")], spec.act)
+                pre = self.pre[o][slot] if o in self.pre else None
+                be.linear_fwd(self.out[o][slot], x, self.W[(o, "w")], self.P[(o, "b")], spec.act, pre=pre)
             elif spec.kind == "concat":
                 off = 0
                 for u in self.wl.graph.predecessors(o):
                     w_u = _width(self.wl.layers[u])
                     be.copy_rows(self.out[o][slot][:, off:off + w_u], self._x_of(u, slot))
+                    if o in self.pre:
+                        if u not in self.pre:
+                            raise NotImplementedError(f"GELU pre-activation of op {u} is not on this stage")
+                        be.copy_rows(self.pre[o][slot][:, off:off + w_u], self.pre[u][slot])
                     off += w_u
             elif spec.kind in ("mse_head", "bce_head"):
                 x = self._input(o, j, slot, batch)
@@ -375,7 +391,8 @@ class Executor:
                 be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
                 if needs_dx:
                     u = preds[0]
-                    be.linear_dgrad(self._dx_target(u, slot), dz, self.W[(o, "w")], x, self.eff_act(u))
+                    saved, act = self._saved_for(u, x, slot)
+                    be.linear_dgrad(self._dx_target(u, slot), dz, self.W[(o, "w")], saved, act)
             elif spec.kind == "concat":
                 dz = self._dz_of(o, slot)
                 off = 0
@@ -387,15 +404,17 @@ class Executor:
                 x = self._input(o, j, slot, batch)
                 u = preds[0] if needs_dx else None
                 dx = self._dx_target(u, slot) if needs_dx else None
+                saved, act = self._saved_for(u, x, slot) if needs_dx else (None, "none")
                 be.rowdot_bwd(dx, self.G[(o, "w")], self.G[(o, "b")], self.dpred[o][slot], x,
-                              self.P[(o, "w")], x, self.eff_act(u) if needs_dx else "none", accumulate)
+                              self.P[(o, "w")], saved, act, accumulate)
             elif spec.kind == "ce_head":
                 x = self._input(o, j, slot, batch)
                 dl = self.dpred[o][slot]
                 be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dl, x, accumulate)
                 if needs_dx:
                     u = preds[0]
-                    be.linear_dgrad(self._dx_target(u, slot), dl, self.W[(o, "w")], x, self.eff_act(u))
+                    saved, act = self._saved_for(u, x, slot)
+                    be.linear_dgrad(self._dx_target(u, slot), dl, self.W[(o, "w")], saved, act)
         sends = []
         for pc in self.recv_fw[j]:  # our input gradients go back along task j's forward pieces
             buf = self.gsend[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows]

@@ -97,7 +97,7 @@ def _head(oid, name, kind, din, nout, bytes_el, label_key, fp32=False):
 
 
 def multi_tower(name: str, towers: int, layers: int, width: int, in_dim: int, tail_hidden: int,
-                B: int, dtype: str = "bf16") -> Workload:
+                B: int, dtype: str = "bf16", act: str = "relu") -> Workload:
     """CANDLE-Uno-style towers -> concat -> [tail Linear+ReLU] -> MSE head."""
     fp32 = dtype == "fp32"
     el = 4 if fp32 else 2
@@ -108,7 +108,8 @@ def multi_tower(name: str, towers: int, layers: int, width: int, in_dim: int, ta
         prev = None
         for l in range(layers):
             din = in_dim if l == 0 else width
-            op, spec = _dense(oid, f"t{t}_ff{l}", din, width, "relu", el, data_key=f"x{t}" if l == 0 else None, fp32=fp32)
+            a = act
+            op, spec = _dense(oid, f"t{t}_ff{l}", din, width, a, el, data_key=f"x{t}" if l == 0 else None, fp32=fp32)
             ops.append(op)
             specs[oid] = spec
             if prev is not None:
@@ -125,7 +126,7 @@ def multi_tower(name: str, towers: int, layers: int, width: int, in_dim: int, ta
     oid += 1
     prev, dprev = cat, towers * width
     if tail_hidden:
-        op, spec = _dense(oid, "tail_ff", dprev, tail_hidden, "relu", el, fp32=fp32)
+        op, spec = _dense(oid, "tail_ff", dprev, tail_hidden, act, el, fp32=fp32)
         ops.append(op)
         specs[oid] = spec
         edges.append((prev, oid))
