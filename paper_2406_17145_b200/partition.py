@@ -250,13 +250,11 @@ class _DP:
         rest_virtual_from[n] = True
         for q in range(n - 1, start - 1, -1):
             rest_virtual_from[q] = rest_virtual_from[q + 1] and self.is_virtual(units[q])
-        for q in range(start + 1, n + 1):
+        if start > 0:  # whole remainder as one stage (start == 0: the node's own base case)
+            best = self._consider(best, self._base(_as_series(list(units[start:])), c_f, c_b, d))
+        for q in range(start + 1, n):
             seg_units = units[start:q]
             seg = _as_series(list(seg_units))
-            if q == n:
-                if start > 0:  # whole remainder as one stage (start == 0: the node's base case)
-                    best = self._consider(best, self._base(seg, c_f, c_b, d))
-                continue
             if rest_virtual_from[q]:
                 best = self._consider(best, self._segment(seg, c_f, c_b, d))
                 continue
@@ -279,8 +277,9 @@ class _DP:
                     if r1 is None:
                         continue
                     best = self._consider(best, _Frag(r1.i_f, r1.stages + r2.stages, max(r1.mem, r2.mem)))
-            if not any_ok and len(seg_units) > 1:
-                # TPS of a longer first segment on the same devices only grows.
+            if not any_ok and len(seg_units) > 1 and d > 1:
+                # TPS of a longer first segment on the same devices only grows; the
+                # whole-remainder case (q == n) was already taken care of above.
                 tps_all = [self.tps(seg.ops, c_f[0], d1) for d1 in range(1, d)]
                 if all(t is not None and t > self.t_max for t in tps_all):
                     break
@@ -338,13 +337,18 @@ def search_stage_graph(ng, tree, cluster, B, t_m, opts, configs, uniform):
     dp = _DP(ng, cluster, B, t_m, configs, opts, uniform)
     best = None
     best_key = None
-    for c in configs:
-        frag = dp.solve(tree, c, None, cluster.num_devices)
-        if frag is None or not frag.stages:
-            continue
-        k = (frag.mem, len(frag.stages), frag.key()[3])
-        if best is None or k < best_key:
-            best, best_key = frag, k
+    # All devices first; fewer only if nothing fits (C3 does not require covering the
+    # cluster, model.py:473-481, and MAXTPS is priced on ONE device, so it stays safe).
+    for d_total in range(cluster.num_devices, 0, -1):
+        for c in configs:
+            frag = dp.solve(tree, c, None, d_total)
+            if frag is None or not frag.stages:
+                continue
+            k = (frag.mem, len(frag.stages), frag.key()[3])
+            if best is None or k < best_key:
+                best, best_key = frag, k
+        if best is not None:
+            break
     return best, len(dp.memo)
 
 
