@@ -84,6 +84,16 @@ int gpp_linear_wgrad(float* dw, int64_t lddw, float* dbias, const void* dy, int6
                      const void* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
                      int accumulate, int dtype, void* stream);
 
+/* wgrad of the LAST micro-batch fused with SGD (stages without data parallelism):
+ *   g = dy[M,N]^T x[M,K] (+ grad if accumulate);  [grad = g if store_grad];
+ *   master[N,K] -= lr * g;  shadow = bf16(master)   (shadow ignored for GPP_F32).
+ * Replaces gpp_linear_wgrad + the weight part of gpp_sgd_step (saves the fp32
+ * gradient round trip through HBM). */
+int gpp_linear_wgrad_sgd(float* master, int64_t ldm, void* shadow, int64_t lds, float* grad,
+                         int64_t ldg, float lr, int accumulate, int store_grad, const void* dy,
+                         int64_t lddy, const void* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
+                         int dtype, void* stream);
+
 /* Generic C[M,N] = alpha * sum_k A(m,k) B(n,k) (+ beta*C).
  * a_mn / b_mn = 0: operand stored [rows][ld] with k contiguous (K-major);
  *             = 1: operand stored [k][ld] with the row index contiguous (MN-major).

@@ -66,6 +66,20 @@ class TorchBackend:
             else:
                 db.copy_(s)
 
+    def linear_wgrad_sgd(self, master, shadow, grad, dy, x, lr, accumulate, store_grad):
+        g = dy.float().t() @ x.float()
+        if accumulate:
+            g = g + grad
+        if store_grad:
+            grad.copy_(g)
+        master.sub_(lr * g)
+        if shadow is not None:
+            shadow.copy_(master)
+
+    def colsum(self, out, x, accumulate):
+        s = x.float().sum(0)
+        out.add_(s) if accumulate else out.copy_(s)
+
     def rowdot_fwd(self, out, x, w, bias):
         v = x.float() @ w
         if bias is not None:

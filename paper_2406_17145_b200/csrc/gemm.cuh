@@ -8,7 +8,9 @@ enum {
   EPI_FWD = 0,    // out(dtype) = act(alpha*acc + bias) [+ residual];  optional pre-act store
   EPI_DGRAD = 1,  // out(dtype) = alpha*acc * act'(saved)
   EPI_F32 = 2,    // out(f32)   = alpha*acc + beta*out
-  EPI_BF16 = 3    // out(dtype) = alpha*acc + beta*out
+  EPI_BF16 = 3,   // out(dtype) = alpha*acc + beta*out
+  EPI_SGD = 4     // wgrad + fused SGD: g = alpha*acc (+ grad if beta); [grad = g];
+                  // out(f32 master) -= lr*g; pre(bf16 shadow) = bf16(master)
 };
 
 struct EpiParams {
@@ -22,6 +24,10 @@ struct EpiParams {
   float alpha;
   float beta;
   int act;
+  float lr;          // EPI_SGD
+  float* grad;       // EPI_SGD: fp32 gradient buffer (read if beta != 0, written if store_grad)
+  int64_t ldgrad;
+  int store_grad;
 };
 
 // bf16 operands, tcgen05 + TMA (gemm_sm100.cu).

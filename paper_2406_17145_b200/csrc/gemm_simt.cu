@@ -21,6 +21,14 @@ __device__ __forceinline__ void epi_scalar(const EpiParams& ep, float acc, int r
       v *= act_bwd(static_cast<const float*>(ep.aux)[static_cast<int64_t>(row) * ep.ldaux + col],
                    ep.act);
   }
+  if constexpr (EPI == EPI_SGD) {
+    float* grad = ep.grad + static_cast<int64_t>(row) * ep.ldgrad + col;
+    const float g = v + (ep.beta != 0.f ? *grad : 0.f);
+    if (ep.store_grad) *grad = g;
+    float* master = static_cast<float*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col;
+    *master -= ep.lr * g;
+    return;
+  }
   float* out = static_cast<float*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col;
   if constexpr (EPI == EPI_F32 || EPI == EPI_BF16) {
     if (ep.beta != 0.f) v += ep.beta * *out;
@@ -113,6 +121,7 @@ int simt_gemm(int epi, const void* a, int64_t lda, int a_mn, const void* b, int6
     case EPI_FWD: return simt::launch<EPI_FWD>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);
     case EPI_DGRAD: return simt::launch<EPI_DGRAD>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);
     case EPI_F32: return simt::launch<EPI_F32>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);
+    case EPI_SGD: return simt::launch<EPI_SGD>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);
     default: return simt::launch<EPI_BF16>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);
   }
 }

@@ -28,85 +28,276 @@ namespace gpp {
 namespace tc {
 
 constexpr int NUM_THREADS = 192;
+constexpr int PAIR_EPI_WARPS = 8;                          // two epilogue warpgroups
+constexpr int PAIR_THREADS = 64 + 32 * PAIR_EPI_WARPS;     // + TMA warp + MMA warp
+
+// 32 bf16 from global (16-byte vector loads when aligned and in bounds).
+__device__ __forceinline__ void load_bf16x32(const bf16* p, bool vec, int n_valid, float (&o)[32]) {
+  if (vec) {
+    uint4 r[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        o[i * 8 + 2 * j] = f.x;
+        o[i * 8 + 2 * j + 1] = f.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = j < n_valid ? __bfloat162float(p[j]) : 0.f;
+  }
+}
+
+__device__ __forceinline__ void store_bf16x32(bf16* p, bool vec, int n_valid, const float (&f)[32]) {
+  if (vec) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 pk;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(f[j + 0], f[j + 1]);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(f[j + 2], f[j + 3]);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(f[j + 4], f[j + 5]);
+      __nv_bfloat162 h3 = __floats2bfloat162_rn(f[j + 6], f[j + 7]);
+      pk.x = *reinterpret_cast<uint32_t*>(&h0);
+      pk.y = *reinterpret_cast<uint32_t*>(&h1);
+      pk.z = *reinterpret_cast<uint32_t*>(&h2);
+      pk.w = *reinterpret_cast<uint32_t*>(&h3);
+      *reinterpret_cast<uint4*>(p + j) = pk;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < n_valid) p[j] = __float2bfloat16_rn(f[j]);
+  }
+}
+
+__device__ __forceinline__ bool al16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
 
 // Epilogue of one thread: 32 consecutive columns [col0, col0+32) of one row.
+// `aux` (residual / act'-saved, 32 values) is loaded by the caller BEFORE the TMEM
+// load so its global latency overlaps tcgen05.ld.
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const uint32_t (&v)[32],
-                                               int row, int col0, int M, int N) {
+                                               const float (&aux)[32], int row, int col0, int M,
+                                               int N) {
   if (row >= M || col0 >= N) return;
-  const bool full = (col0 + 32 <= N);
+  const int n_valid = N - col0 < 32 ? N - col0 : 32;
+  const bool full = n_valid == 32;
   float f[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * ep.alpha;
 
-  if constexpr (EPI == EPI_F32) {
+  if constexpr (EPI == EPI_SGD) {
+    float* master = reinterpret_cast<float*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col0;
+    float* grad = ep.grad + static_cast<int64_t>(row) * ep.ldgrad + col0;
+    bf16* shadow = static_cast<bf16*>(ep.pre) + static_cast<int64_t>(row) * ep.ldpre + col0;
+    if (full && al16(master) && al16(grad) && al16(shadow)) {
+      float m[32];
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        const float4 mv = *reinterpret_cast<const float4*>(master + j);
+        m[j] = mv.x; m[j + 1] = mv.y; m[j + 2] = mv.z; m[j + 3] = mv.w;
+      }
+      if (ep.beta != 0.f) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 g = *reinterpret_cast<const float4*>(grad + j);
+          f[j] += g.x; f[j + 1] += g.y; f[j + 2] += g.z; f[j + 3] += g.w;
+        }
+      }
+      if (ep.store_grad) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(grad + j) = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) m[j] -= ep.lr * f[j];
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(master + j) = make_float4(m[j], m[j + 1], m[j + 2], m[j + 3]);
+      store_bf16x32(shadow, true, 32, m);
+    } else {
+      for (int j = 0; j < n_valid; ++j) {
+        float g = f[j] + (ep.beta != 0.f ? grad[j] : 0.f);
+        if (ep.store_grad) grad[j] = g;
+        const float mj = master[j] - ep.lr * g;
+        master[j] = mj;
+        shadow[j] = __float2bfloat16_rn(mj);
+      }
+    }
+    return;
+  } else if constexpr (EPI == EPI_F32) {
     float* out = reinterpret_cast<float*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col0;
-    const bool vec = full && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-    if (vec) {
+    if (full && al16(out)) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
         float4 o = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
         if (ep.beta != 0.f) {
-          float4 c = *reinterpret_cast<const float4*>(out + j);
+          const float4 c = *reinterpret_cast<const float4*>(out + j);
           o.x += ep.beta * c.x; o.y += ep.beta * c.y; o.z += ep.beta * c.z; o.w += ep.beta * c.w;
         }
         *reinterpret_cast<float4*>(out + j) = o;
       }
     } else {
-      for (int j = 0; j < 32 && col0 + j < N; ++j) {
-        float o = f[j];
-        if (ep.beta != 0.f) o += ep.beta * out[j];
-        out[j] = o;
-      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < n_valid) out[j] = ep.beta != 0.f ? f[j] + ep.beta * out[j] : f[j];
     }
     return;
   } else {
     if constexpr (EPI == EPI_FWD) {
       if (ep.bias != nullptr) {
+        if (full && al16(ep.bias + col0)) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) f[j] += (full || col0 + j < N) ? __ldg(ep.bias + col0 + j) : 0.f;
+          for (int j = 0; j < 32; j += 4) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + j));
+            f[j] += b.x; f[j + 1] += b.y; f[j + 2] += b.z; f[j + 3] += b.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] += j < n_valid ? __ldg(ep.bias + col0 + j) : 0.f;
+        }
       }
       if (ep.pre != nullptr) {
         bf16* pre = static_cast<bf16*>(ep.pre) + static_cast<int64_t>(row) * ep.ldpre + col0;
-        for (int j = 0; j < 32 && col0 + j < N; ++j) pre[j] = __float2bfloat16_rn(f[j]);
+        store_bf16x32(pre, full && al16(pre), n_valid, f);
       }
 #pragma unroll
       for (int j = 0; j < 32; ++j) f[j] = act_fwd(f[j], ep.act);
       if (ep.aux != nullptr) {
-        const bf16* res = static_cast<const bf16*>(ep.aux) + static_cast<int64_t>(row) * ep.ldaux + col0;
-        for (int j = 0; j < 32 && col0 + j < N; ++j) f[j] += __bfloat162float(res[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] += aux[j];
       }
     } else if constexpr (EPI == EPI_DGRAD) {
       if (ep.act != GPP_ACT_NONE) {
-        const bf16* sv = static_cast<const bf16*>(ep.aux) + static_cast<int64_t>(row) * ep.ldaux + col0;
-        for (int j = 0; j < 32 && col0 + j < N; ++j) f[j] *= act_bwd(__bfloat162float(sv[j]), ep.act);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] *= act_bwd(aux[j], ep.act);
       }
     }
     bf16* out = reinterpret_cast<bf16*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + col0;
     if constexpr (EPI == EPI_BF16) {
       if (ep.beta != 0.f) {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) f[j] += ep.beta * __bfloat162float(out[j]);
+        float c[32];
+        load_bf16x32(out, full && al16(out), n_valid, c);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] += ep.beta * c[j];
       }
     }
-    const bool vec = full && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-    if (vec) {
+    store_bf16x32(out, full && al16(out), n_valid, f);
+  }
+}
+
+
+// fp32-output epilogues (EPI_F32 / EPI_SGD) through a per-warp 32x32 smem transpose:
+// each thread owns one accumulator ROW, but global fp32 rows are written (and the
+// master weights read) 128 B per 8 lanes, 4 rows per warp instruction.
+constexpr int STAGE_LD = 36;  // floats per staged row (16 B aligned, conflict-free phases)
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_f32_coalesced(const EpiParams& ep, const uint32_t (&v)[32],
+                                                       float* stage, int row0, int col0, int M,
+                                                       int N, int lane) {
+  const int sub = lane >> 3;
+  const int c4 = (lane & 7) * 4;
+  const int col = col0 + c4;
+  const int nv = N - col < 4 ? N - col : 4;
+  // Issue every global read of this lane's 8 row-pieces up front (one memory latency
+  // per chunk instead of one per row): master (+ old grad) for SGD, old out for beta.
+  float4 mres[8], gres[8];
+  bool vec[8];
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        uint4 pk;
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(f[j + 0], f[j + 1]);
-        __nv_bfloat162 h1 = __floats2bfloat162_rn(f[j + 2], f[j + 3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(f[j + 4], f[j + 5]);
-        __nv_bfloat162 h3 = __floats2bfloat162_rn(f[j + 6], f[j + 7]);
-        pk.x = *reinterpret_cast<uint32_t*>(&h0);
-        pk.y = *reinterpret_cast<uint32_t*>(&h1);
-        pk.z = *reinterpret_cast<uint32_t*>(&h2);
-        pk.w = *reinterpret_cast<uint32_t*>(&h3);
-        *reinterpret_cast<uint4*>(out + j) = pk;
+  for (int i = 0; i < 8; ++i) {
+    const int grow = row0 + 4 * i + sub;
+    vec[i] = false;
+    if (grow >= M || col >= N) continue;
+    if constexpr (EPI == EPI_SGD) {
+      const float* master = reinterpret_cast<const float*>(ep.out) + static_cast<int64_t>(grow) * ep.ldo + col;
+      const float* grad = ep.grad + static_cast<int64_t>(grow) * ep.ldgrad + col;
+      const bf16* shadow = static_cast<const bf16*>(ep.pre) + static_cast<int64_t>(grow) * ep.ldpre + col;
+      vec[i] = nv == 4 && al16(master) && al16(grad) && ((reinterpret_cast<uintptr_t>(shadow) & 7) == 0);
+      if (vec[i]) {
+        mres[i] = *reinterpret_cast<const float4*>(master);
+        if (ep.beta != 0.f) gres[i] = *reinterpret_cast<const float4*>(grad);
       }
     } else {
-      for (int j = 0; j < 32 && col0 + j < N; ++j) out[j] = __float2bfloat16_rn(f[j]);
+      const float* out = reinterpret_cast<const float*>(ep.out) + static_cast<int64_t>(grow) * ep.ldo + col;
+      vec[i] = nv == 4 && al16(out);
+      if (vec[i] && ep.beta != 0.f) gres[i] = *reinterpret_cast<const float4*>(out);
     }
   }
+  float* mine = stage + lane * STAGE_LD;
+#pragma unroll
+  for (int j = 0; j < 32; j += 4)
+    *reinterpret_cast<float4*>(mine + j) =
+        make_float4(__uint_as_float(v[j]) * ep.alpha, __uint_as_float(v[j + 1]) * ep.alpha,
+                    __uint_as_float(v[j + 2]) * ep.alpha, __uint_as_float(v[j + 3]) * ep.alpha);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 4 * i + sub;
+    const int grow = row0 + r;
+    if (grow >= M || col >= N) continue;
+    const float4 a = *reinterpret_cast<const float4*>(stage + r * STAGE_LD + c4);
+    float g[4] = {a.x, a.y, a.z, a.w};
+    if constexpr (EPI == EPI_SGD) {
+      float* master = reinterpret_cast<float*>(ep.out) + static_cast<int64_t>(grow) * ep.ldo + col;
+      float* grad = ep.grad + static_cast<int64_t>(grow) * ep.ldgrad + col;
+      bf16* shadow = static_cast<bf16*>(ep.pre) + static_cast<int64_t>(grow) * ep.ldpre + col;
+      if (vec[i]) {
+        if (ep.beta != 0.f) {
+          g[0] += gres[i].x; g[1] += gres[i].y; g[2] += gres[i].z; g[3] += gres[i].w;
+        }
+        if (ep.store_grad) *reinterpret_cast<float4*>(grad) = make_float4(g[0], g[1], g[2], g[3]);
+        float4 m = mres[i];
+        m.x -= ep.lr * g[0]; m.y -= ep.lr * g[1]; m.z -= ep.lr * g[2]; m.w -= ep.lr * g[3];
+        *reinterpret_cast<float4*>(master) = m;
+        __nv_bfloat162 lo = __floats2bfloat162_rn(m.x, m.y);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(m.z, m.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(shadow) = pk;
+      } else {
+        for (int t = 0; t < nv; ++t) {
+          float gt = g[t] + (ep.beta != 0.f ? grad[t] : 0.f);
+          if (ep.store_grad) grad[t] = gt;
+          const float mt = master[t] - ep.lr * gt;
+          master[t] = mt;
+          shadow[t] = __float2bfloat16_rn(mt);
+        }
+      }
+    } else {
+      float* out = reinterpret_cast<float*>(ep.out) + static_cast<int64_t>(grow) * ep.ldo + col;
+      if (vec[i]) {
+        if (ep.beta != 0.f) {
+          g[0] += ep.beta * gres[i].x; g[1] += ep.beta * gres[i].y;
+          g[2] += ep.beta * gres[i].z; g[3] += ep.beta * gres[i].w;
+        }
+        *reinterpret_cast<float4*>(out) = make_float4(g[0], g[1], g[2], g[3]);
+      } else {
+        for (int t = 0; t < nv; ++t) out[t] = ep.beta != 0.f ? g[t] + ep.beta * out[t] : g[t];
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// Prefetch the chunk's aux operand (residual for EPI_FWD, act'-saved for EPI_DGRAD).
+template <int EPI>
+__device__ __forceinline__ void epilogue_aux(const EpiParams& ep, int row, int col0, int M, int N,
+                                             float (&aux)[32]) {
+  const bool need = (EPI == EPI_FWD && ep.aux != nullptr) ||
+                    (EPI == EPI_DGRAD && ep.act != GPP_ACT_NONE);
+  if (!need || row >= M || col0 >= N) return;
+  const int n_valid = N - col0 < 32 ? N - col0 : 32;
+  const bf16* p = static_cast<const bf16*>(ep.aux) + static_cast<int64_t>(row) * ep.ldaux + col0;
+  load_bf16x32(p, n_valid == 32 && al16(p), n_valid, aux);
 }
 
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
@@ -215,8 +406,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t v[32];
+      float aux[32];
+      epilogue_aux<EPI>(ep, row, n_blk * BN + c * 32, M, N, aux);
       tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c * 32, v);
-      epilogue_chunk<EPI>(ep, v, row, n_blk * BN + c * 32, M, N);
+      epilogue_chunk<EPI>(ep, v, aux, row, n_blk * BN + c * 32, M, N);
     }
   }
 
@@ -241,7 +434,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 //   barriers; all 8 epilogue warps arrive on the leader's accum-empty barrier.
 // ------------------------------------------------------------------------
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
                         const __grid_constant__ CUtensorMap tma_b, EpiParams ep, int M, int N,
                         int K) {
@@ -259,6 +452,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;       // [2]
   uint64_t* tempty_bar = tfull_bar + 2;           // [2] (leader's copy is the live one)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);  // 4 warps x 32 x 36
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -280,7 +474,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 8);
+      mbar_init(&tempty_bar[a], 2 * PAIR_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -367,12 +561,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
       mbar_wait(&tfull_bar[acc], aph);
       tc_fence_after();
-      const int row = m_blk * 2 * BM + static_cast<int>(rank) * BM + q * 32 + lane;
+      const int row0 = m_blk * 2 * BM + static_cast<int>(rank) * BM + q * 32;
+      const int row = row0 + lane;
+      const int group = (warp - 2) / 4;  // epilogue warpgroup: takes every other 32-col chunk
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = group; c < BN / 32; c += PAIR_EPI_WARPS / 4) {
         uint32_t v[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
-        epilogue_chunk<EPI>(ep, v, row, n_blk * BN + c * 32, M, N);
+        if constexpr (EPI == EPI_F32 || EPI == EPI_SGD) {
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
+          epilogue_f32_coalesced<EPI>(ep, v, epi_stage + (warp - 2) * 32 * STAGE_LD, row0,
+                                      n_blk * BN + c * 32, M, N, lane);
+        } else {
+          float aux[32];
+          epilogue_aux<EPI>(ep, row, n_blk * BN + c * 32, M, N, aux);
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
+          epilogue_chunk<EPI>(ep, v, aux, row, n_blk * BN + c * 32, M, N);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -536,7 +740,7 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   else rc = make_map(&mb, b, N, K, ldb, 64, BK);
   if (rc) return rc;
   constexpr int STAGE_BYTES = (BM + BN / 2) * BK * 2;
-  constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + PAIR_EPI_WARPS * 32 * STAGE_LD * 4;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI>,
@@ -547,7 +751,7 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   int64_t clusters = num_sms() / 2;
   if (tiles < clusters) clusters = tiles;
   gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(2 * clusters),
-                                                     NUM_THREADS, SMEM, stream>>>(
+                                                     PAIR_THREADS, SMEM, stream>>>(
       ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -567,8 +771,8 @@ static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
     // CTA-pair 256 x BN tiles; BN=128 when 256-wide tiles leave most pairs idle.
     const int64_t pairs256 = ((M + 255) / 256) * ((N + 255) / 256);
     if (N > 128 && pairs256 >= 48)
-      return launch_tc_pair<256, 6, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, stream);
-    return launch_tc_pair<128, 8, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, stream);
+      return launch_tc_pair<256, 5, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, stream);
+    return launch_tc_pair<128, 7, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, stream);
   }
   // Prefer the 128x256 tile (full-rate single-CTA UMMA) unless it leaves most SMs idle.
   const int64_t tiles256 = mb * ((N + 255) / 256);
@@ -613,6 +817,8 @@ int tc_gemm(int epi, const void* a, int64_t lda, int a_mn, const void* b, int64_
       return tc::dispatch_layout<EPI_DGRAD>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);
     case EPI_F32:
       return tc::dispatch_layout<EPI_F32>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);
+    case EPI_SGD:
+      return tc::dispatch_layout<EPI_SGD>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);
     default:
       return tc::dispatch_layout<EPI_BF16>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);
   }

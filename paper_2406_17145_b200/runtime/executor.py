@@ -107,7 +107,8 @@ class Executor:
     """One rank's share of a GPP strategy."""
 
     def __init__(self, wl: Workload, sg: StageGraph, rank: int, world: int, backend,
-                 lr: float = 1e-3, seed: int = 0, use_dist: bool | None = None):
+                 lr: float = 1e-3, seed: int = 0, use_dist: bool | None = None,
+                 fuse_optimizer: bool = True, keep_grads: bool = False):
         self.wl, self.sg, self.rank, self.world, self.be = wl, sg, rank, world, backend
         self.lr = float(lr)
         self.seed = seed
@@ -115,6 +116,8 @@ class Executor:
         self.dev = backend.device
         self.dtype = torch.float32 if wl.dtype == "fp32" else torch.bfloat16
         self.use_dist = (world > 1) if use_dist is None else use_dist
+        self.keep_grads = keep_grads
+        self._fuse_req = fuse_optimizer
         g = wl.graph
         self.owner = {op: st.id for st in sg.stages for op in st.op_ids}
         mine = [st for st in sg.stages if rank in st.devices]
@@ -138,6 +141,9 @@ class Executor:
             succ = g.successors(o)
             if len(succ) > 1:
                 raise NotImplementedError(f"op {o} fans out to {len(succ)} consumers (unsupported)")
+        # SGD fused into the last micro-batch's wgrad epilogue: only without data
+        # parallelism (a DP stage must all-reduce its gradients first).
+        self.fuse = self._fuse_req and self.d == 1 and hasattr(backend, "linear_wgrad_sgd")
         self._build_plan()
         self._alloc_params()
         self._alloc_buffers()
@@ -201,6 +207,7 @@ class Executor:
             self.recv_fw[j] = _order(self.recv_fw[j])
             self.send_fw[j] = _order(self.send_fw[j])
         self.first_bw = next(t.index for t in st.schedule if t.direction == "bw")
+        self.last_bw = [t.index for t in st.schedule if t.direction == "bw"][-1]
 
     def eff_act(self, u: int) -> str:
         spec = self.wl.layers[u]
@@ -221,6 +228,10 @@ class Executor:
             for name, t in init_params(self.layers[o], o, self.seed):
                 specs.append((o, name, t))
                 total += -(-t.numel() // _ALIGN) * _ALIGN
+        # dense weights first: with the fused optimizer they are updated by their wgrad
+        # epilogues and the flat SGD kernel only walks the remainder [rest_off:]
+        fusable = lambda o, name: self.layers[o].kind == "dense" and name == "w"
+        specs.sort(key=lambda t: 0 if fusable(t[0], t[1]) else 1)
         total = max(total, _ALIGN)
         self.master = torch.zeros(total, dtype=torch.float32, device=self.dev)
         self.grad = torch.zeros(total, dtype=torch.float32, device=self.dev)
@@ -229,7 +240,10 @@ class Executor:
         self.G: dict[tuple[int, str], torch.Tensor] = {}     # fp32 grad views
         self.W: dict[tuple[int, str], torch.Tensor] = {}     # compute-dtype weight views
         off = 0
+        self.rest_off = None
         for o, name, t in specs:
+            if self.rest_off is None and not fusable(o, name):
+                self.rest_off = off
             n = t.numel()
             self.master[off:off + n].copy_(t.reshape(-1))
             self.P[(o, name)] = self.master[off:off + n].view(t.shape)
@@ -239,6 +253,8 @@ class Executor:
             else:
                 self.W[(o, name)] = self.P[(o, name)]
             off += -(-n // _ALIGN) * _ALIGN
+        if self.rest_off is None:
+            self.rest_off = off
         if self.shadow is not None:
             self.shadow.copy_(self.master.to(torch.bfloat16))
         self.param_count = sum(t.numel() for _, _, t in specs)
@@ -388,11 +404,18 @@ class Executor:
             if spec.kind == "dense":
                 x = self._input(o, j, slot, batch)
                 dz = self._dz_of(o, slot)
-                be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
+                # dgrad first: the fused update below rewrites the weights it reads
                 if needs_dx:
                     u = preds[0]
                     saved, act = self._saved_for(u, x, slot)
                     be.linear_dgrad(self._dx_target(u, slot), dz, self.W[(o, "w")], saved, act)
+                if self.fuse and j == self.last_bw:
+                    # weight gradient + SGD in one epilogue; bias gradient -> flat SGD later
+                    be.linear_wgrad_sgd(self.P[(o, "w")], self.W[(o, "w")] if self.shadow is not None else None,
+                                        self.G[(o, "w")], dz, x, self.lr, accumulate, self.keep_grads)
+                    be.colsum(self.G[(o, "b")], dz, accumulate)
+                else:
+                    be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
             elif spec.kind == "concat":
                 dz = self._dz_of(o, slot)
                 off = 0
@@ -444,7 +467,12 @@ class Executor:
         if self.d > 1:
             dist.all_reduce(self.grad, group=self.dp_group)
         if step_optimizer:
-            self.be.sgd_step(self.master, self.shadow, self.grad, self.lr)
+            if self.fuse:
+                if self.rest_off < self.master.numel():
+                    sh = self.shadow[self.rest_off:] if self.shadow is not None else None
+                    self.be.sgd_step(self.master[self.rest_off:], sh, self.grad[self.rest_off:], self.lr)
+            else:
+                self.be.sgd_step(self.master, self.shadow, self.grad, self.lr)
         return self.loss_acc
 
     @property

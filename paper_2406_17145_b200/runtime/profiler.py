@@ -56,6 +56,11 @@ class TimedBackend(CudaBackend):
         self._timed("wgrad", dy.shape[1], x.shape[1], dy.shape[0],
                     lambda: super(TimedBackend, self).linear_wgrad(dw, db, dy, x, accumulate))
 
+    def linear_wgrad_sgd(self, master, shadow, grad, dy, x, lr, accumulate, store_grad):
+        self._timed("wgrad", dy.shape[1], x.shape[1], dy.shape[0],
+                    lambda: super(TimedBackend, self).linear_wgrad_sgd(master, shadow, grad, dy, x, lr,
+                                                                       accumulate, store_grad))
+
     def summary(self) -> dict:
         """Aggregate FLOPs and device time of the recorded GEMM launches (sync first)."""
         torch.cuda.synchronize()

@@ -53,7 +53,7 @@ def _worker(rank, world, port, layout, B, outdir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         wl, sg = _stage_graph(layout, B)
-        ex = Executor(wl, sg, rank, world, TorchBackend(), lr=LR)
+        ex = Executor(wl, sg, rank, world, TorchBackend(), lr=LR, keep_grads=True)
         res = {"loss": [], "grads": []}
         for step in range(STEPS):
             full = make_batch(wl, step)
@@ -102,7 +102,7 @@ def test_unequal_microbatch_and_dp_gloo():
 
 def test_single_rank_matches_reference():
     wl, sg = _stage_graph([(TOWER_A + TOWER_B + TAIL, 16, [0])], 64)
-    ex = Executor(wl, sg, 0, 1, TorchBackend(), lr=LR)
+    ex = Executor(wl, sg, 0, 1, TorchBackend(), lr=LR, keep_grads=True)
     ref = ReferenceModel(wl)
     for step in range(STEPS):
         full = make_batch(wl, step)
