@@ -34,7 +34,8 @@ import math
 from dataclasses import dataclass, field
 from typing import Iterable
 
-from .cost import DEFAULT_WEIGHT_MULTIPLIER, IndivisibleMicroBatchError, StageCostInput, estimate_tps, stage_memory
+from .cost import (DEFAULT_WEIGHT_MULTIPLIER, IndivisibleMicroBatchError, StageCostInput, dp_sync_time,
+                   estimate_tps, stage_memory)
 from .model import ComputationGraph, DeviceCluster, Operator, Stage, StageGraph, induced_stage_edges
 from .sched import compute_in_flight, round_up, schedule_stage_graph
 from .spgraph import (
@@ -78,6 +79,9 @@ class PartitionOptions:
     weight_multiplier: float = DEFAULT_WEIGHT_MULTIPLIER
     max_exhaustive_branches: int = 6
     micro_batches: tuple[int, ...] | None = None  # restrict b candidates (e.g. fixed-b sweeps)
+    # SPEC cost model charges the DP all-reduce once per MICRO-batch (cost.py:68-70).  The
+    # B200 executor all-reduces once per ITERATION; True prices that.
+    sync_per_iteration: bool = False
 
 
 @dataclass
@@ -168,7 +172,11 @@ class _DP:
         if key not in self._tps_cache:
             cb = stage_comm_bytes(self.ng, ops)
             try:
-                v = estimate_tps(StageCostInput(tuple(self.real_ops(ops)), b, d, cb, cb, self.cluster))
+                real = tuple(self.real_ops(ops))
+                v = estimate_tps(StageCostInput(real, b, d, cb, cb, self.cluster))
+                if self.opts.sync_per_iteration and d > 1:
+                    sync = dp_sync_time(sum(o.param_bytes for o in real), d, self.cluster.intra_bw)
+                    v = v - sync / b + sync / self.B
             except IndivisibleMicroBatchError:
                 v = None
             self._tps_cache[key] = v

@@ -31,11 +31,45 @@ def dist_env() -> tuple[int, int, int]:
 
 
 def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions | None = None,
-         mem_bytes: float = 180e9) -> P.Strategy:
-    """Run the GPP (or SPP baseline) partitioner + scheduler for ``n_gpus`` B200s."""
+         mem_bytes: float = 180e9, sweep: bool | None = None, min_microbatches: int = 1,
+         max_microbatches: int = 32) -> P.Strategy:
+    """Run the GPP (or SPP baseline) partitioner + scheduler for ``n_gpus`` B200s.
+
+    The TPS objective (Eq. 1) is a steady-state measure: with launch overheads in the
+    cost curves it always prefers one giant micro-batch, i.e. no pipelining at all.
+    Like the paper's evaluation ("We sweep over all possible micro-batch sizes ...
+    to maximize training throughput"), ``sweep`` runs the optimizer
+    once per uniform micro-batch size b (B/b in [min_microbatches, max_microbatches])
+    and keeps the strategy with the shortest simulated iteration (sim.simulate),
+    which does see warm-up / cool-down bubbles.  Single-GPU plans skip the sweep.
+    """
+    from ..sim import simulate
+
     cluster = b200_cluster(n_gpus, mem_bytes)
     fn = P.optimize if mode == "gpp" else P.spp_optimize
-    st = fn(wl.graph, cluster, wl.mini_batch, opts)
+    opts = opts or P.PartitionOptions(sync_per_iteration=True)
+    if sweep is None:
+        sweep = n_gpus > 1 and opts.micro_batches is None
+    if not sweep:
+        st = fn(wl.graph, cluster, wl.mini_batch, opts)
+    else:
+        B = wl.mini_batch
+        best, best_t = None, None
+        for b, _ in P.candidate_configs(B):
+            if not (min_microbatches <= B // b <= max_microbatches):
+                continue
+            o = P.PartitionOptions(**{**opts.__dict__, "micro_batches": (b,)})
+            try:
+                cand = fn(wl.graph, cluster, B, o)
+            except P.NoFeasibleStrategy:
+                continue
+            t = simulate(cand.stage_graph, cluster, wl.graph, sync_epilogue=True).iteration_ms
+            if best_t is None or t < best_t:
+                best, best_t = cand, t
+        if best is None:
+            st = fn(wl.graph, cluster, wl.mini_batch, opts)
+        else:
+            st = best
     rep = validate_strategy(wl.graph, cluster, st.stage_graph)
     if rep:
         raise RuntimeError(f"partitioner produced an invalid strategy: {rep}")

@@ -93,3 +93,55 @@ class TimedBackend(CudaBackend):
 
     def reset(self):
         self.records.clear()
+
+
+# ---------------------------------------------------------------------------
+# Measured cost curves: table CostCurves from B200 timings.
+# ---------------------------------------------------------------------------
+
+
+def _time_us(fn, reps: int) -> float:
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) * 1e3 / reps
+
+
+def profile_dense(din: int, dout: int, act: str, batches, device, dtype=torch.bfloat16, reps: int = 10,
+                  has_dgrad: bool = True) -> dict:
+    """fw and bw (dgrad + fused wgrad/SGD + bias colsum) milliseconds of Linear(din, dout)
+    at each micro-batch size in ``batches``, through the production kernels."""
+    be = CudaBackend(device)
+    w = (torch.randn(dout, din, device=device) / din**0.5).to(dtype)
+    master = torch.randn(dout, din, device=device) / din**0.5
+    grad = torch.zeros(dout, din, device=device)
+    bias = torch.zeros(dout, device=device)
+    gb = torch.zeros(dout, device=device)
+    out = {"b": [], "fwd_ms": [], "bwd_ms": []}
+    for b in batches:
+        x = torch.randn(b, din, device=device).to(dtype)
+        y = torch.empty(b, dout, device=device, dtype=dtype)
+        dz = torch.randn(b, dout, device=device).to(dtype)
+        dx = torch.empty(b, din, device=device, dtype=dtype)
+        f = _time_us(lambda: be.linear_fwd(y, x, w, bias, act), reps)
+
+        def bw():
+            if has_dgrad:
+                be.linear_dgrad(dx, dz, w, x, act)
+            if dtype == torch.bfloat16:
+                be.linear_wgrad_sgd(master, w, grad, dz, x, 0.0, False, False)
+                be.colsum(gb, dz, False)
+            else:
+                be.linear_wgrad(grad, gb, dz, x, False)
+
+        bwt = _time_us(bw, reps)
+        out["b"].append(int(b))
+        out["fwd_ms"].append(f / 1e3)
+        out["bwd_ms"].append(bwt / 1e3)
+    return out

@@ -112,6 +112,7 @@ def simulate(
     g: ComputationGraph | NormalizedGraph | None = None,
     durations: Callable[[int, str], float] | None = None,
     weight_multiplier: float = DEFAULT_WEIGHT_MULTIPLIER,
+    sync_epilogue: bool = False,
 ) -> SimReport:
     """Simulate one iteration of a configured StageGraph.
 
@@ -196,6 +197,15 @@ def simulate(
             raise Deadlock(blocked)
 
     iteration = max((t1 for _, t1 in times.values()), default=0.0)
+    if sync_epilogue and cluster is not None and cg is not None:
+        # weight-update epilogue: a DP stage all-reduces its gradients once per iteration
+        # after its last task (SPEC.md:469 makes this configurable; default 0)
+        from .cost import dp_sync_time
+        for st in s.stages:
+            if st.dp_degree > 1:
+                last = max(t1 for (sid, _, _), (_, t1) in times.items() if sid == st.id)
+                params = sum(cg.by_id[o].param_bytes for o in st.op_ids if o in cg.by_id)
+                iteration = max(iteration, last + dp_sync_time(params, st.dp_degree, cluster.intra_bw))
     busy = {st.id: sum(dcache[(st.id, t.direction)] for t in st.schedule) for st in s.stages}
     idle = {sid: iteration - b for sid, b in busy.items()}
     peak: dict[int, int] = {}
