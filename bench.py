@@ -190,7 +190,7 @@ def main():
     full = make_batch(wl, 0, keys=keys)
     dev_batch = to_device_rows(ex, full, ex.dtype, dev) if ex.stage else {}
     graphed = None
-    if world == 1 and not args.no_graph and ex.stage is not None:
+    if not args.no_graph and (ex.stage is not None or world > 1):
         from paper_2406_17145_b200.runtime.graph import GraphedIteration
 
         n_before = lib.launch_count()

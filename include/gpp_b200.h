@@ -141,6 +141,21 @@ int gpp_copy_rows(void* dst, int64_t lddst, const void* src, int64_t ldsrc, int6
 /* dst_f32[i] = float(src[i]) or dst_bf16[i] = bf16(src_f32[i]). */
 int gpp_cast(void* dst, int dst_dtype, const void* src, int src_dtype, int64_t n, void* stream);
 
+/* ---- transport (NCCL resolved at run time from the loaded libnccl.so.2) --------------
+ * Stage-edge P2P pieces and the per-iteration DP all-reduce; one
+ * communicator per ordered rank pair so forward and backward traffic never serialise. */
+int gpp_nccl_available(void);
+int gpp_nccl_unique_id(void* out128);
+/* Initialise n communicators in one NCCL group: comm i has nranks[i] members, this
+ * process is rank ranks[i], unique id at ids + 128*i; handles written to comms[i]. */
+int gpp_comm_init_group(int n, const void* ids, const int* nranks, const int* ranks, void** comms);
+int gpp_comm_destroy(void* comm);
+int gpp_send(void* comm, const void* buf, int64_t bytes, int peer, void* stream);
+int gpp_recv(void* comm, void* buf, int64_t bytes, int peer, void* stream);
+int gpp_allreduce_f32(void* comm, void* buf, int64_t count, void* stream);
+int gpp_group_start(void);
+int gpp_group_end(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,7 @@ struct EpiParams {
   float* grad;       // EPI_SGD: fp32 gradient buffer (read if beta != 0, written if store_grad)
   int64_t ldgrad;
   int store_grad;
+  int64_t split_stride;  // split-K: partial s is written at (float*)out + s * split_stride
 };
 
 // bf16 operands, tcgen05 + TMA (gemm_sm100.cu).

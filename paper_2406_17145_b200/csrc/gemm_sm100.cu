@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 
 #include "gemm.cuh"
@@ -303,7 +304,8 @@ __device__ __forceinline__ void epilogue_aux(const EpiParams& ep, int row, int c
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
-                   const __grid_constant__ CUtensorMap tma_b, EpiParams ep, int M, int N, int K) {
+                   const __grid_constant__ CUtensorMap tma_b, EpiParams ep, int M, int N, int K,
+                   int k_splits) {
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -321,9 +323,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_blocks = (N + BN - 1) / BN;
-  const int m_blk = blockIdx.x / n_blocks;
-  const int n_blk = blockIdx.x % n_blocks;
-  const int num_kb = (K + BK - 1) / BK;
+  const int tile = static_cast<int>(blockIdx.x) / k_splits;
+  const int split = static_cast<int>(blockIdx.x) % k_splits;
+  const int m_blk = tile / n_blocks;
+  const int n_blk = tile % n_blocks;
+  const int kb_per = ((K + BK - 1) / BK + k_splits - 1) / k_splits;
+  const int kb0 = split * kb_per;
+  const int num_kb = min((K + BK - 1) / BK, kb0 + kb_per) - kb0;
+  EpiParams epu = ep;
+  if (k_splits > 1) epu.out = reinterpret_cast<float*>(ep.out) + split * ep.split_stride;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
@@ -358,18 +366,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint8_t* b_dst = a_dst + A_BYTES;
         mbar_expect_tx(&full_bar[s], STAGE_BYTES);
         if constexpr (!A_MN) {
-          tma_load_2d(a_dst, &tma_a, &full_bar[s], kb * BK, m_blk * BM);
+          tma_load_2d(a_dst, &tma_a, &full_bar[s], (kb0 + kb) * BK, m_blk * BM);
         } else {
 #pragma unroll
           for (int c = 0; c < BM / 64; ++c)
-            tma_load_2d(a_dst + c * 8192, &tma_a, &full_bar[s], m_blk * BM + c * 64, kb * BK);
+            tma_load_2d(a_dst + c * 8192, &tma_a, &full_bar[s], m_blk * BM + c * 64, (kb0 + kb) * BK);
         }
         if constexpr (!B_MN) {
-          tma_load_2d(b_dst, &tma_b, &full_bar[s], kb * BK, n_blk * BN);
+          tma_load_2d(b_dst, &tma_b, &full_bar[s], (kb0 + kb) * BK, n_blk * BN);
         } else {
 #pragma unroll
           for (int c = 0; c < BN / 64; ++c)
-            tma_load_2d(b_dst + c * 8192, &tma_b, &full_bar[s], n_blk * BN + c * 64, kb * BK);
+            tma_load_2d(b_dst + c * 8192, &tma_b, &full_bar[s], n_blk * BN + c * 64, (kb0 + kb) * BK);
         }
       }
     }
@@ -407,9 +415,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t v[32];
       float aux[32];
-      epilogue_aux<EPI>(ep, row, n_blk * BN + c * 32, M, N, aux);
+      epilogue_aux<EPI>(epu, row, n_blk * BN + c * 32, M, N, aux);
       tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c * 32, v);
-      epilogue_chunk<EPI>(ep, v, aux, row, n_blk * BN + c * 32, M, N);
+      epilogue_chunk<EPI>(epu, v, aux, row, n_blk * BN + c * 32, M, N);
     }
   }
 
@@ -437,7 +445,7 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
                         const __grid_constant__ CUtensorMap tma_b, EpiParams ep, int M, int N,
-                        int K) {
+                        int K, int k_splits) {
   constexpr int A_BYTES = BM * BK * 2;            // 16 KB: this CTA's 128 rows of A
   constexpr int B_BYTES = (BN / 2) * BK * 2;      // this CTA's BN/2 rows of B
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -462,8 +470,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   const int num_clusters = gridDim.x >> 1;
   const int m_tiles = (M + 2 * BM - 1) / (2 * BM);
   const int n_tiles = (N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
-  const int num_kb = (K + BK - 1) / BK;
+  const int num_units = m_tiles * n_tiles * k_splits;   // (tile, K-split) work units
+  const int kb_total = (K + BK - 1) / BK;
+  const int kb_per = (kb_total + k_splits - 1) / k_splits;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
@@ -494,7 +503,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs) ----------------
       uint32_t it = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      for (int u = cluster_id; u < num_units; u += num_clusters) {
+        const int tile = u / k_splits, kb0 = (u % k_splits) * kb_per;
+        const int num_kb = min(kb_total, kb0 + kb_per) - kb0;
         const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
         const int a_row = m_blk * 2 * BM + static_cast<int>(rank) * BM;
         const int b_row = n_blk * BN + static_cast<int>(rank) * (BN / 2);
@@ -506,18 +517,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
           uint8_t* b_dst = a_dst + A_BYTES;
           if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
           if constexpr (!A_MN) {
-            tma_load_2d_pair(a_dst, &tma_a, &full_bar[s], kb * BK, a_row);
+            tma_load_2d_pair(a_dst, &tma_a, &full_bar[s], (kb0 + kb) * BK, a_row);
           } else {
 #pragma unroll
             for (int c = 0; c < BM / 64; ++c)
-              tma_load_2d_pair(a_dst + c * 8192, &tma_a, &full_bar[s], a_row + c * 64, kb * BK);
+              tma_load_2d_pair(a_dst + c * 8192, &tma_a, &full_bar[s], a_row + c * 64, (kb0 + kb) * BK);
           }
           if constexpr (!B_MN) {
-            tma_load_2d_pair(b_dst, &tma_b, &full_bar[s], kb * BK, b_row);
+            tma_load_2d_pair(b_dst, &tma_b, &full_bar[s], (kb0 + kb) * BK, b_row);
           } else {
 #pragma unroll
             for (int c = 0; c < (BN / 2) / 64; ++c)
-              tma_load_2d_pair(b_dst + c * 8192, &tma_b, &full_bar[s], b_row + c * 64, kb * BK);
+              tma_load_2d_pair(b_dst + c * 8192, &tma_b, &full_bar[s], b_row + c * 64, (kb0 + kb) * BK);
           }
         }
       }
@@ -526,7 +537,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     if (leader && lane == 0) {
       // ---------------- MMA issuer (leader CTA only) ----------------
       uint32_t it = 0, lt = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++lt) {
+      for (int u = cluster_id; u < num_units; u += num_clusters, ++lt) {
+        const int kb0 = (u % k_splits) * kb_per;
+        const int num_kb = min(kb_total, kb0 + kb_per) - kb0;
         const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
         mbar_wait_cluster(&tempty_bar[acc], aph ^ 1);
         tc_fence_after();
@@ -556,7 +569,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     const int q = warp & 3;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     uint32_t lt = 0;
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++lt) {
+    for (int u = cluster_id; u < num_units; u += num_clusters, ++lt) {
+      const int tile = u / k_splits;
+      EpiParams epu = ep;
+      if (k_splits > 1) epu.out = reinterpret_cast<float*>(ep.out) + (u % k_splits) * ep.split_stride;
       const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
       const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
       mbar_wait(&tfull_bar[acc], aph);
@@ -569,13 +585,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         uint32_t v[32];
         if constexpr (EPI == EPI_F32 || EPI == EPI_SGD) {
           tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
-          epilogue_f32_coalesced<EPI>(ep, v, epi_stage + (warp - 2) * 32 * STAGE_LD, row0,
+          epilogue_f32_coalesced<EPI>(epu, v, epi_stage + (warp - 2) * 32 * STAGE_LD, row0,
                                       n_blk * BN + c * 32, M, N, lane);
         } else {
           float aux[32];
-          epilogue_aux<EPI>(ep, row, n_blk * BN + c * 32, M, N, aux);
+          epilogue_aux<EPI>(epu, row, n_blk * BN + c * 32, M, N, aux);
           tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
-          epilogue_chunk<EPI>(ep, v, aux, row, n_blk * BN + c * 32, M, N);
+          epilogue_chunk<EPI>(epu, v, aux, row, n_blk * BN + c * 32, M, N);
         }
       }
       tc_fence_before();
@@ -673,7 +689,7 @@ static int make_map(CUtensorMap* out, const void* ptr, int64_t inner, int64_t ou
 
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 static int launch_tc(const void* a, int64_t lda, const void* b, int64_t ldb, const EpiParams& ep,
-                     int64_t M, int64_t N, int64_t K, cudaStream_t stream) {
+                     int64_t M, int64_t N, int64_t K, int k_splits, cudaStream_t stream) {
   CUtensorMap ma, mb;
   int rc;
   // K-major operand: inner = K, outer = rows;  MN-major: inner = rows, outer = K.
@@ -693,10 +709,9 @@ static int launch_tc(const void* a, int64_t lda, const void* b, int64_t ldb, con
     attr_set = true;
   }
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(tiles), NUM_THREADS, SMEM,
-                                                stream>>>(ma, mb, ep, static_cast<int>(M),
-                                                          static_cast<int>(N),
-                                                          static_cast<int>(K));
+  gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(tiles * k_splits),
+                                                NUM_THREADS, SMEM, stream>>>(
+      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("gemm_tc launch: ") + cudaGetErrorString(e));
@@ -716,6 +731,16 @@ static bool pair_enabled() {
   return v == 1;
 }
 
+static int max_splits_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GPP_GEMM_MAX_SPLITS");
+    v = e ? atoi(e) : 16;
+    if (v < 1) v = 1;
+  }
+  return v;
+}
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -729,7 +754,7 @@ static int num_sms() {
 
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb,
-                          const EpiParams& ep, int64_t M, int64_t N, int64_t K,
+                          const EpiParams& ep, int64_t M, int64_t N, int64_t K, int k_splits,
                           cudaStream_t stream) {
   CUtensorMap ma, mb;
   int rc;
@@ -747,12 +772,12 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr_set = true;
   }
-  const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+  const int64_t units = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * k_splits;
   int64_t clusters = num_sms() / 2;
-  if (tiles < clusters) clusters = tiles;
+  if (units < clusters) clusters = units;
   gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(2 * clusters),
                                                      PAIR_THREADS, SMEM, stream>>>(
-      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K));
+      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("gemm_tc_pair launch: ") + cudaGetErrorString(e));
@@ -762,23 +787,142 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   return GPP_OK;
 }
 
+// ---- split-K: fp32 partials in a per-device workspace, then one reduce + epilogue ----
+
+static float* splitk_workspace(size_t floats, cudaStream_t stream) {
+  static float* bufs[64] = {nullptr};
+  static size_t caps[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (caps[dev] >= floats) return bufs[dev];
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &st);
+  if (st != cudaStreamCaptureStatusNone) {
+    set_error("split-K workspace must be sized before CUDA-graph capture (run one eager step first)");
+    return nullptr;
+  }
+  size_t want = floats < (size_t(16) << 20) ? (size_t(16) << 20) : floats;
+  if (bufs[dev]) {
+    cudaStreamSynchronize(stream);
+    cudaFree(bufs[dev]);
+  }
+  if (cudaMalloc(&bufs[dev], want * sizeof(float)) != cudaSuccess) {
+    bufs[dev] = nullptr;
+    caps[dev] = 0;
+    set_error("split-K workspace allocation failed");
+    return nullptr;
+  }
+  caps[dev] = want;
+  return bufs[dev];
+}
+
+template <int EPI>
+__device__ __forceinline__ void epi_elem(const EpiParams& ep, float acc, int64_t row, int64_t col) {
+  float v = acc * ep.alpha;
+  if constexpr (EPI == EPI_FWD) {
+    if (ep.bias) v += ep.bias[col];
+    if (ep.pre) static_cast<bf16*>(ep.pre)[row * ep.ldpre + col] = __float2bfloat16_rn(v);
+    v = act_fwd(v, ep.act);
+    if (ep.aux) v += __bfloat162float(static_cast<const bf16*>(ep.aux)[row * ep.ldaux + col]);
+    static_cast<bf16*>(ep.out)[row * ep.ldo + col] = __float2bfloat16_rn(v);
+  } else if constexpr (EPI == EPI_DGRAD) {
+    if (ep.act != GPP_ACT_NONE)
+      v *= act_bwd(__bfloat162float(static_cast<const bf16*>(ep.aux)[row * ep.ldaux + col]), ep.act);
+    static_cast<bf16*>(ep.out)[row * ep.ldo + col] = __float2bfloat16_rn(v);
+  } else if constexpr (EPI == EPI_F32) {
+    float* o = static_cast<float*>(ep.out) + row * ep.ldo + col;
+    *o = ep.beta != 0.f ? v + ep.beta * *o : v;
+  } else if constexpr (EPI == EPI_BF16) {
+    bf16* o = static_cast<bf16*>(ep.out) + row * ep.ldo + col;
+    *o = __float2bfloat16_rn(ep.beta != 0.f ? v + ep.beta * __bfloat162float(*o) : v);
+  } else {  // EPI_SGD
+    float* g = ep.grad + row * ep.ldgrad + col;
+    const float gv = v + (ep.beta != 0.f ? *g : 0.f);
+    if (ep.store_grad) *g = gv;
+    float* m = static_cast<float*>(ep.out) + row * ep.ldo + col;
+    const float mv = *m - ep.lr * gv;
+    *m = mv;
+    static_cast<bf16*>(ep.pre)[row * ep.ldpre + col] = __float2bfloat16_rn(mv);
+  }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits,
+                                                            int64_t stride, EpiParams ep, int M,
+                                                            int N) {
+  const int64_t total = static_cast<int64_t>(M) * N;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc = 0.f;
+    for (int sp = 0; sp < splits; ++sp) acc += ws[sp * stride + i];
+    epi_elem<EPI>(ep, acc, i / N, i % N);
+  }
+}
+
+// How many K-slices: fill idle SMs when the tile count is small, keep >= 2 k-blocks each.
+static int choose_splits(int64_t tiles, int64_t slots, int64_t num_kb) {
+  if (tiles * 2 > slots) return 1;
+  int64_t s = slots / tiles;
+  if (s > num_kb / 2) s = num_kb / 2;
+  if (s > max_splits_env()) s = max_splits_env();
+  return s < 1 ? 1 : static_cast<int>(s);
+}
+
 template <bool A_MN, bool B_MN, int EPI>
 static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
                        const EpiParams& ep, int64_t M, int64_t N, int64_t K,
                        cudaStream_t stream) {
-  const int64_t mb = (M + BM - 1) / BM;
-  if (M > BM && pair_enabled()) {
+  const int64_t num_kb = (K + BK - 1) / BK;
+  const bool pair = M > BM && pair_enabled();
+  int bn;
+  int64_t tiles, slots;
+  if (pair) {
     // CTA-pair 256 x BN tiles; BN=128 when 256-wide tiles leave most pairs idle.
     const int64_t pairs256 = ((M + 255) / 256) * ((N + 255) / 256);
-    if (N > 128 && pairs256 >= 48)
-      return launch_tc_pair<256, 5, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, stream);
-    return launch_tc_pair<128, 7, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, stream);
+    bn = (N > 128 && pairs256 >= 48) ? 256 : 128;
+    tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
+    slots = num_sms() / 2;
+  } else {
+    const int64_t tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256);
+    bn = (N > 128 && tiles256 >= 96) ? 256 : 128;
+    tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+    slots = num_sms();
   }
-  // Prefer the 128x256 tile (full-rate single-CTA UMMA) unless it leaves most SMs idle.
-  const int64_t tiles256 = mb * ((N + 255) / 256);
-  if (N > 128 && tiles256 >= 96)
-    return launch_tc<256, 4, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, stream);
-  return launch_tc<128, 6, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, stream);
+  const int splits = choose_splits(tiles, slots, num_kb);
+
+  auto run = [&](auto epi_tag, const EpiParams& e, int ks) -> int {
+    constexpr int E = decltype(epi_tag)::value;
+    if (pair) {
+      if (bn == 256) return launch_tc_pair<256, 5, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
+      return launch_tc_pair<128, 7, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
+    }
+    if (bn == 256) return launch_tc<256, 4, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
+    return launch_tc<128, 6, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
+  };
+  if (splits == 1) return run(std::integral_constant<int, EPI>{}, ep, 1);
+
+  float* ws = splitk_workspace(static_cast<size_t>(splits) * M * N, stream);
+  if (!ws) return GPP_ERR_CUDA;
+  EpiParams part{};
+  part.out = ws;
+  part.ldo = N;
+  part.alpha = 1.f;
+  part.beta = 0.f;
+  part.split_stride = M * N;
+  int rc = run(std::integral_constant<int, EPI_F32>{}, part, splits);
+  if (rc) return rc;
+  const int64_t total = M * N;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 148 * 8) grid = 148 * 8;
+  splitk_reduce_kernel<EPI><<<static_cast<unsigned>(grid), 256, 0, stream>>>(
+      ws, splits, M * N, ep, static_cast<int>(M), static_cast<int>(N));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("splitk_reduce launch: ") + cudaGetErrorString(e));
+    return GPP_ERR_CUDA;
+  }
+  count_launch();
+  return GPP_OK;
 }
 
 template <int EPI>

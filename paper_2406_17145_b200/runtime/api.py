@@ -112,10 +112,7 @@ def execute(wl: Workload, sg: StageGraph, iters: int = 1, lr: float = 1e-3, seed
         torch.cuda.synchronize()
         times.append(t0.elapsed_time(t1))
         if loss is not None and ex.is_head:
-            l = loss.clone()
-            if ex.d > 1:
-                dist.all_reduce(l, group=ex.dp_group)
-            losses.append(float(l.item()))
+            losses.append(ex.stage_loss(loss))
     ms = sum(times) / max(1, len(times))
     return RunReport(losses, times, wl.mini_batch / (ms / 1e3) if ms > 0 else 0.0,
                      ex.stage.id if ex.stage else None)

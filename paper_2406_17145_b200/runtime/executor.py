@@ -108,7 +108,7 @@ class Executor:
 
     def __init__(self, wl: Workload, sg: StageGraph, rank: int, world: int, backend,
                  lr: float = 1e-3, seed: int = 0, use_dist: bool | None = None,
-                 fuse_optimizer: bool = True, keep_grads: bool = False):
+                 fuse_optimizer: bool = True, keep_grads: bool = False, transport: str = "auto"):
         self.wl, self.sg, self.rank, self.world, self.be = wl, sg, rank, world, backend
         self.lr = float(lr)
         self.seed = seed
@@ -118,6 +118,7 @@ class Executor:
         self.use_dist = (world > 1) if use_dist is None else use_dist
         self.keep_grads = keep_grads
         self._fuse_req = fuse_optimizer
+        self._transport_kind = transport
         g = wl.graph
         self.owner = {op: st.id for st in sg.stages for op in st.op_ids}
         mine = [st for st in sg.stages if rank in st.devices]
@@ -150,13 +151,12 @@ class Executor:
 
     # ------------------------------------------------------------------ plan
     def _make_groups(self):
-        """Process groups: one per ordered (src, dst) rank pair with traffic, one per DP stage.
-        Every rank creates every group in the same order (torch.distributed requirement)."""
-        self.p2p_groups: dict[tuple[int, int], object] = {}
+        """Transport: one channel per ordered (src, dst) rank pair with traffic, one DP group per
+        DP stage.  Every rank builds every channel in the same order (collective setup)."""
+        self.tp = None
         self.dp_group = None
         if not self.use_dist:
             return
-        g = self.wl.graph
         pairs = set()
         for (a, b) in sorted(self.sg.edges):
             sa, sb = self.sg.by_id[a], self.sg.by_id[b]
@@ -164,14 +164,17 @@ class Executor:
                 for c in sb.devices:
                     pairs.add((p, c))
                     pairs.add((c, p))
-        for (a, b) in sorted(pairs):
-            grp = dist.new_group(ranks=sorted({a, b}))
-            self.p2p_groups[(a, b)] = grp
-        for st in self.sg.stages:
-            if st.dp_degree > 1:
-                grp = dist.new_group(ranks=sorted(st.devices))
-                if self.rank in st.devices:
-                    self.dp_group = grp
+        dp_groups = [tuple(sorted(st.devices)) for st in self.sg.stages if st.dp_degree > 1]
+        kind = self._transport_kind
+        if kind == "auto":
+            kind = "nccl" if self.dev.type == "cuda" else "torch"
+        if kind == "nccl":
+            from .transport import NcclTransport
+            self.tp = NcclTransport(self.rank, pairs, dp_groups, self.dev)
+        else:
+            from .transport import TorchTransport
+            self.tp = TorchTransport(self.rank, pairs, dp_groups)
+            self.dp_group = self.tp.dp
 
     def _build_plan(self):
         g = self.wl.graph
@@ -335,9 +338,6 @@ class Executor:
         return self.grecv[o][slot] if o in self.grecv else self.gbuf[o][slot]
 
     # ------------------------------------------------------------- transport
-    def _grp(self, a: int, b: int):
-        return self.p2p_groups[(a, b)]
-
     def _wait_sends(self, key):
         for w in self._send_works.pop(key, []):
             w.wait()
@@ -348,7 +348,7 @@ class Executor:
         works = []
         for pc in self.recv_fw[j]:
             buf = self.recv[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows]
-            works.append(dist.irecv(buf, src=pc.producer, group=self._grp(pc.producer, self.rank)))
+            works.append(self.tp.irecv(buf, pc.producer))
         for w in works:
             w.wait()
         self._wait_sends(("fw", slot))
@@ -383,7 +383,7 @@ class Executor:
         sends = []
         for pc in self.send_fw[j]:
             buf = self.out[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows]
-            sends.append(dist.isend(buf, dst=pc.consumer, group=self._grp(self.rank, pc.consumer)))
+            sends.append(self.tp.isend(buf, pc.consumer))
         if sends:
             self._send_works[("fw", slot)] = sends
 
@@ -392,7 +392,7 @@ class Executor:
         works = []
         for pc in self.send_fw[j]:  # grads come back along the forward pieces of task j
             buf = self.grecv[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows]
-            works.append(dist.irecv(buf, src=pc.consumer, group=self._grp(pc.consumer, self.rank)))
+            works.append(self.tp.irecv(buf, pc.consumer))
         for w in works:
             w.wait()
         self._wait_sends(("bw", slot))
@@ -409,7 +409,12 @@ class Executor:
                     u = preds[0]
                     saved, act = self._saved_for(u, x, slot)
                     be.linear_dgrad(self._dx_target(u, slot), dz, self.W[(o, "w")], saved, act)
-                if self.fuse and j == self.last_bw:
+                if self.d > 1 and j == self.last_bw:
+                    # DP stage: this weight's gradient is final -> overlap its all-reduce
+                    # with the rest of the backward pass (bucket = one layer's weight)
+                    be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
+                    self._ar_handles.append(self.tp.allreduce_async(self.G[(o, "w")]))
+                elif self.fuse and j == self.last_bw:
                     # weight gradient + SGD in one epilogue; bias gradient -> flat SGD later
                     be.linear_wgrad_sgd(self.P[(o, "w")], self.W[(o, "w")] if self.shadow is not None else None,
                                         self.G[(o, "w")], dz, x, self.lr, accumulate, self.keep_grads)
@@ -441,7 +446,7 @@ class Executor:
         sends = []
         for pc in self.recv_fw[j]:  # our input gradients go back along task j's forward pieces
             buf = self.gsend[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows]
-            sends.append(dist.isend(buf, dst=pc.producer, group=self._grp(self.rank, pc.producer)))
+            sends.append(self.tp.isend(buf, pc.producer))
         if sends:
             self._send_works[("bw", slot)] = sends
 
@@ -455,6 +460,7 @@ class Executor:
         if self.stage is None:
             return None
         self.loss_acc.zero_()
+        self._ar_handles = []
         seen_bw = False
         for t in self.stage.schedule:
             if t.direction == "fw":
@@ -465,7 +471,11 @@ class Executor:
         for key in list(self._send_works):
             self._wait_sends(key)
         if self.d > 1:
-            dist.all_reduce(self.grad, group=self.dp_group)
+            # the non-weight remainder (biases, heads) in one bucket, then join the DP stream
+            if self.rest_off < self.grad.numel():
+                self._ar_handles.append(self.tp.allreduce_async(self.grad[self.rest_off:]))
+            self.tp.join(self._ar_handles)
+            self._ar_handles = []
         if step_optimizer:
             if self.fuse:
                 if self.rest_off < self.master.numel():
@@ -474,6 +484,13 @@ class Executor:
             else:
                 self.be.sgd_step(self.master, self.shadow, self.grad, self.lr)
         return self.loss_acc
+
+    def stage_loss(self, loss: torch.Tensor) -> float:
+        """Loss of the whole mini-batch on a head rank (sums the DP replicas' shares)."""
+        l = loss.clone()
+        if self.d > 1:
+            self.tp.allreduce(l)
+        return float(l.item())
 
     @property
     def is_head(self) -> bool:

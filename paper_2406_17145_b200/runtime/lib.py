@@ -41,6 +41,15 @@ _SIGS = {
     "gpp_sgd_step": ([_vp, _vp, _vp, _i64, _f32, _vp], _i32),
     "gpp_copy_rows": ([_vp, _i64, _vp, _i64, _i64, _i64, _i32, _vp], _i32),
     "gpp_cast": ([_vp, _i32, _vp, _i32, _i64, _vp], _i32),
+    "gpp_nccl_available": ([], _i32),
+    "gpp_nccl_unique_id": ([_vp], _i32),
+    "gpp_comm_init_group": ([_i32, _vp, _vp, _vp, _vp], _i32),
+    "gpp_comm_destroy": ([_vp], _i32),
+    "gpp_send": ([_vp, _vp, _i64, _i32, _vp], _i32),
+    "gpp_recv": ([_vp, _vp, _i64, _i32, _vp], _i32),
+    "gpp_allreduce_f32": ([_vp, _vp, _i64, _vp], _i32),
+    "gpp_group_start": ([], _i32),
+    "gpp_group_end": ([], _i32),
     "gpp_layernorm_fwd": ([_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _vp], _i32),
     "gpp_layernorm_bwd": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_attention_fwd": ([_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),

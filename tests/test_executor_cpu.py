@@ -60,10 +60,7 @@ def _worker(rank, world, port, layout, B, outdir):
             batch = to_device_rows(ex, full, torch.float32, "cpu")
             loss = ex.run_iteration(batch)
             if ex.is_head:
-                l = loss.clone()
-                if ex.d > 1:
-                    dist.all_reduce(l, group=ex.dp_group)
-                res["loss"].append(l.item())
+                res["loss"].append(ex.stage_loss(loss))
             res["grads"].append({k: v.clone() for k, v in ex.G.items()})
         torch.save(res, os.path.join(outdir, f"rank{rank}.pt"))
     finally:

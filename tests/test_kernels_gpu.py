@@ -9,7 +9,8 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(128, 256, 64), (256, 512, 128), (1000, 520, 200), (384, 128, 4096), (1024, 4096, 1024)]
+SHAPES = [(128, 256, 64), (256, 512, 128), (1000, 520, 200), (384, 128, 4096), (1024, 4096, 1024),
+          (16, 4096, 4096), (1024, 1024, 28672), (96, 136, 2000)]  # last 3: split-K paths
 
 
 def _rel(a, b):
@@ -179,3 +180,22 @@ def test_sgd_and_colsum(cuda_lib):
     cuda_lib.colsum(out, x)
     torch.cuda.synchronize()
     assert _rel(out, x.sum(0)) < 1e-5
+
+
+@pytest.mark.parametrize("M", [64, 1024])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_wgrad_sgd_fused(cuda_lib, M, accumulate):
+    N, K = 1024, 512
+    g = torch.Generator(device="cuda").manual_seed(M + accumulate)
+    dy = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    master = torch.randn(N, K, device="cuda", generator=g)
+    shadow = torch.empty(N, K, device="cuda", dtype=torch.bfloat16)
+    grad = torch.randn(N, K, device="cuda", generator=g)
+    grad0, master0 = grad.clone(), master.clone()
+    cuda_lib.linear_wgrad_sgd(master, shadow, grad, dy, x, 0.01, accumulate=accumulate, store_grad=True)
+    torch.cuda.synchronize()
+    gref = dy.float().t() @ x.float() + (grad0 if accumulate else 0)
+    assert _rel(grad, gref) < 1e-4
+    assert torch.allclose(master, master0 - 0.01 * gref, rtol=1e-5, atol=1e-5)
+    assert torch.equal(shadow, master.bfloat16())

@@ -29,7 +29,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, layout, B, outdir):
+def _worker(rank, world, port, layout, B, outdir, graphed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
@@ -48,15 +48,28 @@ def _worker(rank, world, port, layout, B, outdir):
         dev = torch.device("cuda", rank)
         ex = Executor(wl, sg, rank, world, CudaBackend(dev), lr=LR, keep_grads=True)
         res = {"loss": [], "grads": []}
+        g = None
         for step in range(STEPS):
             full = make_batch(wl, step)
-            loss = ex.run_iteration(to_device_rows(ex, full, ex.dtype, dev))
+            batch = to_device_rows(ex, full, ex.dtype, dev)
+            if graphed:
+                from paper_2406_17145_b200.runtime.graph import GraphedIteration
+                if g is None:
+                    # capture AFTER computing nothing: warm-up inside would advance the weights,
+                    # so capture on a throwaway executor state and re-sync the params after
+                    snap = ex.master.clone()
+                    g = GraphedIteration(ex, batch, n_buffers=1, warmup=1)
+                    ex.master.copy_(snap)
+                    if ex.shadow is not None:
+                        ex.shadow.copy_(ex.master.to(ex.shadow.dtype))
+                for k in g.bufs[0]:
+                    g.bufs[0][k].copy_(batch[k])
+                loss = g.replay(0)
+            else:
+                loss = ex.run_iteration(batch)
             torch.cuda.synchronize()
             if ex.is_head:
-                l = loss.clone()
-                if ex.d > 1:
-                    dist.all_reduce(l, group=ex.dp_group)
-                res["loss"].append(l.item())
+                res["loss"].append(ex.stage_loss(loss))
             res["grads"].append({k: v.detach().cpu().clone() for k, v in ex.G.items()})
         torch.save(res, os.path.join(outdir, f"rank{rank}.pt"))
         dist.barrier()
@@ -64,7 +77,7 @@ def _worker(rank, world, port, layout, B, outdir):
         dist.destroy_process_group()
 
 
-def _run(layout, B, world):
+def _run(layout, B, world, graphed=False):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     from oracle.reference_model import ReferenceModel
@@ -72,7 +85,7 @@ def _run(layout, B, world):
     from paper_2406_17145_b200.runtime.data import make_batch
 
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), layout, B, d), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), layout, B, d, graphed), nprocs=world, join=True)
         outs = [torch.load(os.path.join(d, f"rank{r}.pt")) for r in range(world)]
     wl = W.toy(B=B)
     ref = ReferenceModel(wl)
@@ -94,3 +107,12 @@ def test_two_stage_gpp_nccl():
 
 def test_four_rank_unequal_b_and_dp_nccl():
     _run([(TOWER_A, 16, [0]), (TOWER_B, 32, [1, 2]), (TAIL, 8, [3])], 64, 4)
+
+
+def test_two_stage_gpp_nccl_cuda_graph():
+    """The whole rank iteration (kernels + NCCL P2P pieces) captured into a CUDA graph."""
+    _run([(TOWER_A, 16, [0]), (TOWER_B + TAIL, 16, [1])], 64, 2, graphed=True)
+
+
+def test_four_rank_dp_nccl_cuda_graph():
+    _run([(TOWER_A, 16, [0]), (TOWER_B, 32, [1, 2]), (TAIL, 8, [3])], 64, 4, graphed=True)
