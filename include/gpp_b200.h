@@ -21,7 +21,7 @@
  *   gpp_colsum                  bias gradient
  *   gpp_sgd_step                fused optimizer over a stage's parameters
  *   gpp_layernorm_fwd / _bwd    MMT pre-LN
- *   gpp_embbag_fwd / gpp_embbag_bwd_sgd    DLRM embedding-bag with fused sparse update
+ *   gpp_embbag_fwd / gpp_embbag_sgd        DLRM embedding-bag and its sparse SGD scatter
  *   gpp_interaction_fwd / _bwd  DLRM dot interaction
  *   gpp_copy_rows               strided row-block copy (concat slices, DP re-shard,
  *                               same-device stage edges)
@@ -141,6 +141,22 @@ int gpp_copy_rows(void* dst, int64_t lddst, const void* src, int64_t ldsrc, int6
 /* dst_f32[i] = float(src[i]) or dst_bf16[i] = bf16(src_f32[i]). */
 int gpp_cast(void* dst, int dst_dtype, const void* src, int src_dtype, int64_t n, void* stream);
 
+/* ---- DLRM: embedding bags and the dot interaction ------------- */
+/* pooled[m, :D] = sum_b table[idx[m*ldi + b], :D]; fp32 table [rows, D], bf16 pooled, D = 64. */
+int gpp_embbag_fwd(void* out, int64_t ldo, const float* table, const int64_t* idx, int64_t ldi,
+                   int64_t M, int64_t bag, int64_t D, int64_t rows, void* stream);
+/* Synchronous sparse SGD: table[idx[m, b], :] -= lr * dpooled[m, :] for all (m, b)
+ * (fp32 atomics; applied once per iteration over the whole mini-batch). */
+int gpp_embbag_sgd(float* table, const void* dpooled, int64_t ldd, const int64_t* idx, int64_t ldi,
+                   int64_t M, int64_t bag, int64_t D, int64_t rows, float lr, void* stream);
+/* z [M, F*D] (feature 0 = dense/bottom vector): out[:, 0:D] = z_0, then the F(F-1)/2
+ * pairwise dots <z_i, z_j> (i > j, row-major lower triangle), zero padding to out_cols. */
+int gpp_interaction_fwd(void* out, int64_t ldo, int64_t out_cols, const void* z, int64_t ldz,
+                        int64_t M, int64_t F, int64_t D, void* stream);
+/* dz from dout; mask_first applies relu'(z_0) to feature 0's gradient. */
+int gpp_interaction_bwd(void* dz, int64_t lddz, const void* dout, int64_t lddo, const void* z,
+                        int64_t ldz, int64_t M, int64_t F, int64_t D, int mask_first, void* stream);
+
 /* ---- transport (NCCL resolved at run time from the loaded libnccl.so.2) --------------
  * Stage-edge P2P pieces and the per-iteration DP all-reduce; one
  * communicator per ordered rank pair so forward and backward traffic never serialise. */
@@ -153,6 +169,8 @@ int gpp_comm_destroy(void* comm);
 int gpp_send(void* comm, const void* buf, int64_t bytes, int peer, void* stream);
 int gpp_recv(void* comm, void* buf, int64_t bytes, int peer, void* stream);
 int gpp_allreduce_f32(void* comm, void* buf, int64_t count, void* stream);
+/* recv[r*bytes_per_rank ...] = send of DP rank r (embedding-gradient exchange). */
+int gpp_allgather(void* comm, const void* send, void* recv, int64_t bytes_per_rank, void* stream);
 int gpp_group_start(void);
 int gpp_group_end(void);
 

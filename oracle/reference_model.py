@@ -53,6 +53,18 @@ class ReferenceModel:
                 out[o] = _round(y, self.bf16)
             elif spec.kind == "concat":
                 out[o] = torch.cat([out[u] for u in g.predecessors(o)], dim=1)
+            elif spec.kind == "embbag":
+                pooled = torch.nn.functional.embedding_bag(batch[spec.data_key], P[(o, "table")], mode="sum")
+                out[o] = _round(pooled, self.bf16)
+            elif spec.kind == "interaction":
+                zz = torch.stack([out[u] for u in g.predecessors(o)], dim=1)  # [B, F, D]
+                F = zz.shape[1]
+                dots = torch.bmm(zz, zz.transpose(1, 2))
+                ii = torch.tensor([i for i in range(F) for j in range(i)])
+                jj = torch.tensor([j for i in range(F) for j in range(i)])
+                pad = spec.out_dim - zz.shape[2] - len(ii)
+                y = torch.cat([zz[:, 0], dots[:, ii, jj], torch.zeros(zz.shape[0], pad)], dim=1)
+                out[o] = _round(y, self.bf16)
             elif spec.kind == "mse_head":
                 pred = x @ P[(o, "w")] + P[(o, "b")][0]
                 l = ((pred - batch[spec.label_key].float()) ** 2).sum() / B

@@ -124,3 +124,39 @@ class TorchBackend:
         master.sub_(lr * grad)
         if shadow is not None:
             shadow.copy_(master)
+
+    # DLRM ------------------------------------------------------------------
+    def embbag_fwd(self, out, table, idx):
+        out.copy_(table[idx].sum(1))
+
+    def embbag_sgd(self, table, dpooled, idx, lr):
+        M, bag = idx.shape
+        upd = (-lr * dpooled.float())[:, None, :].expand(M, bag, table.shape[1]).reshape(-1, table.shape[1])
+        table.index_add_(0, idx.reshape(-1), upd)
+
+    @staticmethod
+    def _pairs(F):
+        return [(i, j) for i in range(F) for j in range(i)]
+
+    def interaction_fwd(self, out, z, F, out_cols):
+        zz = z.float().reshape(z.shape[0], F, 64)
+        dots = torch.bmm(zz, zz.transpose(1, 2))
+        ii = torch.tensor([p[0] for p in self._pairs(F)])
+        jj = torch.tensor([p[1] for p in self._pairs(F)])
+        res = torch.zeros(z.shape[0], out_cols)
+        res[:, :64] = zz[:, 0]
+        res[:, 64:64 + len(ii)] = dots[:, ii, jj]
+        out.copy_(res)
+
+    def interaction_bwd(self, dz, dout, z, F, mask_first):
+        zz = z.float().reshape(z.shape[0], F, 64)
+        P = len(self._pairs(F))
+        g = torch.zeros(z.shape[0], F, F)
+        for p, (i, j) in enumerate(self._pairs(F)):
+            g[:, i, j] = dout[:, 64 + p].float()
+            g[:, j, i] = dout[:, 64 + p].float()
+        d = torch.bmm(g, zz)
+        d[:, 0] += dout[:, :64].float()
+        if mask_first:
+            d[:, 0] *= (zz[:, 0] > 0).float()
+        dz.copy_(d.reshape(z.shape[0], F * 64))

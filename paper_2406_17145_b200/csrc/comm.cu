@@ -25,6 +25,7 @@ struct Nccl {
   int (*send)(const void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   int (*recv)(void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   int (*allReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*allGather)(const void*, void*, size_t, int, Comm, cudaStream_t) = nullptr;
   int (*groupStart)() = nullptr;
   int (*groupEnd)() = nullptr;
   const char* (*getErrorString)(int) = nullptr;
@@ -45,6 +46,8 @@ Nccl& nccl() {
     n.recv = reinterpret_cast<int (*)(void*, size_t, int, int, Comm, cudaStream_t)>(dlsym(h, "ncclRecv"));
     n.allReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, Comm, cudaStream_t)>(
         dlsym(h, "ncclAllReduce"));
+    n.allGather = reinterpret_cast<int (*)(const void*, void*, size_t, int, Comm, cudaStream_t)>(
+        dlsym(h, "ncclAllGather"));
     n.groupStart = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupStart"));
     n.groupEnd = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupEnd"));
     n.getErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
@@ -113,6 +116,13 @@ int gpp_allreduce_f32(void* comm, void* buf, int64_t count, void* stream) {
   GPP_ARG_CHECK(comm && buf && count >= 0, "bad argument");
   return nccl_status(nccl().allReduce(buf, buf, static_cast<size_t>(count), NCCL_FLOAT32, NCCL_SUM, comm,
                                       static_cast<cudaStream_t>(stream)), "ncclAllReduce");
+}
+
+int gpp_allgather(void* comm, const void* send, void* recv, int64_t bytes_per_rank, void* stream) {
+  GPP_ARG_CHECK(comm && send && recv && bytes_per_rank >= 0, "bad argument");
+  if (!nccl().allGather) { set_error("ncclAllGather unavailable"); return GPP_ERR_UNSUPPORTED; }
+  return nccl_status(nccl().allGather(send, recv, static_cast<size_t>(bytes_per_rank), NCCL_UINT8, comm,
+                                      static_cast<cudaStream_t>(stream)), "ncclAllGather");
 }
 
 int gpp_group_start(void) { return nccl_status(nccl().groupStart(), "ncclGroupStart"); }

@@ -64,3 +64,16 @@ class CudaBackend:
 
     def sgd_step(self, master, shadow, grad, lr):
         lib.sgd_step(master, shadow, grad, lr)
+
+    # DLRM ------------------------------------------------------------------
+    def embbag_fwd(self, out, table, idx):
+        lib.embbag_fwd(out, table, idx)
+
+    def embbag_sgd(self, table, dpooled, idx, lr):
+        lib.embbag_sgd(table, dpooled, idx, lr)
+
+    def interaction_fwd(self, out, z, F, out_cols):
+        lib.interaction_fwd(out, z, F, out_cols)
+
+    def interaction_bwd(self, dz, dout, z, F, mask_first):
+        lib.interaction_bwd(dz, dout, z, F, mask_first)

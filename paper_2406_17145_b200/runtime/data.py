@@ -23,6 +23,10 @@ def make_batch(wl: Workload, step: int, seed: int = 0, keys=None) -> dict[str, t
         B = wl.mini_batch
         if kind == "normal":
             t = torch.randn((B, *shape), generator=g)
+        elif kind.startswith("normal_pad:"):  # n real features, zero-padded to shape (TMA: ld % 8)
+            real = int(kind.split(":")[1])
+            t = torch.zeros((B, *shape))
+            t[..., :real] = torch.randn((B, *shape[:-1], real), generator=g)
         elif kind == "binary":
             t = (torch.rand((B, *shape), generator=g) > 0.5).float()
         elif kind.startswith("label:"):

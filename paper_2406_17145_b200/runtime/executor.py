@@ -96,7 +96,17 @@ def init_params(spec: LayerSpec, op_id: int, seed: int) -> list[tuple[str, torch
         w = torch.randn(spec.in_dim, generator=g) / spec.in_dim**0.5
         b = torch.randn(1, generator=g) * 0.01
         return [("w", w), ("b", b)]
+    if spec.kind == "embbag":
+        return [("table", torch.randn(spec.in_dim, spec.out_dim, generator=g) * 0.05)]
     return []
+
+
+def init_table(spec: LayerSpec, op_id: int, seed: int, device) -> torch.Tensor:
+    """Embedding table: CPU-identical init when small (oracle-checkable), device RNG when big."""
+    if spec.in_dim * spec.out_dim <= (1 << 22):
+        return init_params(spec, op_id, seed)[0][1].to(device)
+    g = torch.Generator(device=device).manual_seed(seed * 1_000_003 + op_id * 7919 + 17)
+    return torch.randn(spec.in_dim, spec.out_dim, generator=g, device=device) * 0.05
 
 
 def _width(spec: LayerSpec) -> int:
@@ -227,7 +237,11 @@ class Executor:
     def _alloc_params(self):
         specs = []
         total = 0
+        self.tables: dict[int, torch.Tensor] = {}
         for o in self.ops:
+            if self.layers[o].kind == "embbag":  # big sparse tables live outside the flat buffers
+                self.tables[o] = init_table(self.layers[o], o, self.seed, self.dev)
+                continue
             for name, t in init_params(self.layers[o], o, self.seed):
                 specs.append((o, name, t))
                 total += -(-t.numel() // _ALIGN) * _ALIGN
@@ -260,6 +274,8 @@ class Executor:
             self.rest_off = off
         if self.shadow is not None:
             self.shadow.copy_(self.master.to(torch.bfloat16))
+        for o, t in self.tables.items():
+            self.P[(o, "table")] = t
         self.param_count = sum(t.numel() for _, _, t in specs)
 
     def _ring(self, shape, dtype=None):
@@ -269,6 +285,7 @@ class Executor:
         m, g = self.m, self.wl.graph
         self.out, self.recv, self.gbuf, self.grecv, self.gsend, self.pre = {}, {}, {}, {}, {}, {}
         self.pred, self.dpred = {}, {}
+        self.emb_grad, self.zbuf, self.dzbuf = {}, {}, {}
         for o in self.ops:
             spec = self.layers[o]
             if spec.kind in ("dense", "concat"):
@@ -285,6 +302,23 @@ class Executor:
             elif spec.kind == "ce_head":
                 self.pred[o] = self._ring((m, spec.out_dim))
                 self.dpred[o] = self._ring((m, spec.out_dim))
+            elif spec.kind == "embbag":
+                self.out[o] = self._ring((m, spec.out_dim))
+                if o in self.out_remote:
+                    self.grecv[o] = self._ring((m, spec.out_dim))
+                elif g.successors(o):
+                    self.gbuf[o] = self._ring((m, spec.out_dim))
+                # pooled-output gradients of the whole iteration -> one sparse SGD scatter
+                self.emb_grad[o] = torch.zeros((self.n * m, spec.out_dim), dtype=self.dtype, device=self.dev)
+            elif spec.kind == "interaction":
+                F = spec.in_dim
+                self.out[o] = self._ring((m, spec.out_dim))
+                self.zbuf[o] = self._ring((m, F * 64))
+                self.dzbuf[o] = torch.zeros((m, F * 64), dtype=self.dtype, device=self.dev)
+                if o in self.out_remote:
+                    self.grecv[o] = self._ring((m, spec.out_dim))
+                elif g.successors(o):
+                    self.gbuf[o] = self._ring((m, spec.out_dim))
             else:
                 raise NotImplementedError(f"layer kind {spec.kind}")
         for u in self.in_remote:
@@ -375,6 +409,15 @@ class Executor:
                 y = batch[spec.label_key][j * self.m:(j + 1) * self.m]
                 loss = be.mse_loss if spec.kind == "mse_head" else be.bce_loss
                 loss(self.loss_acc, self.dpred[o][slot], self.pred[o][slot], y, scale)
+            elif spec.kind == "embbag":
+                idx = batch[spec.data_key][j * self.m:(j + 1) * self.m]
+                be.embbag_fwd(self.out[o][slot], self.tables[o], idx)
+            elif spec.kind == "interaction":
+                off = 0
+                for u in self.wl.graph.predecessors(o):
+                    be.copy_rows(self.zbuf[o][slot][:, off:off + 64], self._x_of(u, slot))
+                    off += 64
+                be.interaction_fwd(self.out[o][slot], self.zbuf[o][slot], spec.in_dim, spec.out_dim)
             elif spec.kind == "ce_head":
                 x = self._input(o, j, slot, batch)
                 be.linear_fwd(self.pred[o][slot], x, self.W[(o, "w")], self.P[(o, "b")], "none")
@@ -421,6 +464,19 @@ class Executor:
                     be.colsum(self.G[(o, "b")], dz, accumulate)
                 else:
                     be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
+            elif spec.kind == "embbag":
+                be.copy_rows(self.emb_grad[o][j * self.m:(j + 1) * self.m], self._dz_of(o, slot))
+            elif spec.kind == "interaction":
+                us = list(preds)
+                first_act = self.eff_act(us[0])
+                if first_act not in ("none", "relu") or any(self.eff_act(u) != "none" for u in us[1:]):
+                    raise NotImplementedError("interaction inputs: ReLU/none first feature, linear others")
+                be.interaction_bwd(self.dzbuf[o], self._dz_of(o, slot), self.zbuf[o][slot], spec.in_dim,
+                                   first_act == "relu")
+                off = 0
+                for u in us:
+                    be.copy_rows(self._dx_target(u, slot), self.dzbuf[o][:, off:off + 64])
+                    off += 64
             elif spec.kind == "concat":
                 dz = self._dz_of(o, slot)
                 off = 0
@@ -477,6 +533,16 @@ class Executor:
             self.tp.join(self._ar_handles)
             self._ar_handles = []
         if step_optimizer:
+            for o, table in self.tables.items():
+                idx = batch[self.layers[o].data_key]
+                g_o = self.emb_grad[o]
+                if self.d > 1:  # every replica applies every replica's sparse updates
+                    gi = torch.empty((self.d * idx.shape[0], idx.shape[1]), dtype=idx.dtype, device=idx.device)
+                    gg = torch.empty((self.d * g_o.shape[0], g_o.shape[1]), dtype=g_o.dtype, device=g_o.device)
+                    self.tp.allgather(gi, idx.contiguous())
+                    self.tp.allgather(gg, g_o)
+                    idx, g_o = gi, gg
+                self.be.embbag_sgd(table, g_o, idx, self.lr)
             if self.fuse:
                 if self.rest_off < self.master.numel():
                     sh = self.shadow[self.rest_off:] if self.shadow is not None else None

@@ -48,16 +48,17 @@ _SIGS = {
     "gpp_send": ([_vp, _vp, _i64, _i32, _vp], _i32),
     "gpp_recv": ([_vp, _vp, _i64, _i32, _vp], _i32),
     "gpp_allreduce_f32": ([_vp, _vp, _i64, _vp], _i32),
+    "gpp_allgather": ([_vp, _vp, _vp, _i64, _vp], _i32),
     "gpp_group_start": ([], _i32),
     "gpp_group_end": ([], _i32),
     "gpp_layernorm_fwd": ([_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _vp], _i32),
     "gpp_layernorm_bwd": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_attention_fwd": ([_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_attention_bwd": ([_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
-    "gpp_embbag_fwd": ([_vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
-    "gpp_embbag_bwd_sgd": ([_vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
-    "gpp_interaction_fwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp], _i32),
-    "gpp_interaction_bwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp], _i32),
+    "gpp_embbag_fwd": ([_vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp], _i32),
+    "gpp_embbag_sgd": ([_vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
+    "gpp_interaction_fwd": ([_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
+    "gpp_interaction_bwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _vp], _i32),
 }
 
 
@@ -213,3 +214,26 @@ def sgd_step(master, shadow, grad, lr: float, stream=None):
 def copy_rows(dst, src, stream=None):
     rows, cols = src.shape
     call("gpp_copy_rows", _ptr(dst), _ld(dst), _ptr(src), _ld(src), rows, cols, src.element_size(), _stream(stream))
+
+
+def embbag_fwd(out, table, idx, stream=None):
+    M, bag = idx.shape
+    call("gpp_embbag_fwd", _ptr(out), _ld(out), _ptr(table), _ptr(idx), _ld(idx), M, bag, table.shape[1],
+         table.shape[0], _stream(stream))
+
+
+def embbag_sgd(table, dpooled, idx, lr, stream=None):
+    M, bag = idx.shape
+    call("gpp_embbag_sgd", _ptr(table), _ptr(dpooled), _ld(dpooled), _ptr(idx), _ld(idx), M, bag,
+         table.shape[1], table.shape[0], float(lr), _stream(stream))
+
+
+def interaction_fwd(out, z, F, out_cols, stream=None):
+    M = z.shape[0]
+    call("gpp_interaction_fwd", _ptr(out), _ld(out), out_cols, _ptr(z), _ld(z), M, F, 64, _stream(stream))
+
+
+def interaction_bwd(dz, dout, z, F, mask_first, stream=None):
+    M = z.shape[0]
+    call("gpp_interaction_bwd", _ptr(dz), _ld(dz), _ptr(dout), _ld(dout), _ptr(z), _ld(z), M, F, 64,
+         int(bool(mask_first)), _stream(stream))

@@ -55,6 +55,9 @@ class TorchTransport:
         dist.all_reduce(t, group=self.dp)
         return None
 
+    def allgather(self, out, t):
+        dist.all_gather_into_tensor(out, t, group=self.dp)
+
     def join(self, handles):
         pass
 
@@ -149,6 +152,10 @@ class NcclTransport:
         done = torch.cuda.Event()
         done.record(self.dp_stream)
         return _Done(done)
+
+    def allgather(self, out, t):
+        self._lib.call("gpp_allgather", self.dp_comm, t.data_ptr(), out.data_ptr(), t.numel() * t.element_size(),
+                       torch.cuda.current_stream().cuda_stream)
 
     def join(self, handles):
         for h in handles:

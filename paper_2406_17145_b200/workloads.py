@@ -202,7 +202,71 @@ def case_study(blocks: int = 4, branches: int = 2) -> ComputationGraph:
     return ComputationGraph(ops, edges)
 
 
-PRESETS = {"toy": toy, "candle": candle}
+def dlrm(B: int = 512, tables: int = 26, rows: int = 1_000_000, bag: int = 100, hidden: int = 4096,
+         dense_in: int = 13, emb: int = 64) -> Workload:
+    """BASELINE configs[3]: DLRM — bottom MLP dense_in -> hidden x3 -> 64, `tables` embedding
+    bags (rows x 64, bag 100, sum-pooled), dot interaction (64 + F(F-1)/2 = 415, padded to
+    416), top MLP 416 -> hidden x3 -> 1, BCE.
+    Op ids: bottom MLP first (feature 0 of the interaction), then the tables."""
+    ops, specs, edges, data = [], {}, [], {}
+    din = -(-dense_in // 8) * 8  # zero-padded so the TMA row pitch is 16-byte aligned
+    data["dense"] = ((din,), f"normal_pad:{dense_in}")
+    oid = 0
+    prev = None
+    dims = [din, hidden, hidden, hidden, emb]
+    for l in range(4):
+        op, spec = _dense(oid, f"bot{l}", dims[l], dims[l + 1], "relu", 2, data_key="dense" if l == 0 else None)
+        ops.append(op)
+        specs[oid] = spec
+        if prev is not None:
+            edges.append((prev, oid))
+        prev = oid
+        oid += 1
+    bottom_end = prev
+    table_ids = []
+    for t in range(tables):
+        fbytes = bag * emb * 4 + bag * 8 + emb * 2          # gather fp32 rows + idx + pooled write
+        bbytes = 2 * bag * emb * 4 + bag * 8 + emb * 2      # deferred scatter: RMW of every looked-up row
+        op = Operator(oid, f"emb{t}", param_bytes=4.0 * rows * emb, act_bytes_per_sample=0.0,
+                      out_bytes_per_sample=2.0 * emb,
+                      fwd_cost=CostCurve.affine(LAUNCH_MS, fbytes / BYTES_PER_MS),
+                      bwd_cost=CostCurve.affine(LAUNCH_MS, bbytes / BYTES_PER_MS))
+        ops.append(op)
+        specs[oid] = LayerSpec("embbag", rows, emb, data_key=f"idx{t}", extra=(bag,))
+        data[f"idx{t}"] = ((bag,), f"index:{rows}")
+        table_ids.append(oid)
+        oid += 1
+    F = tables + 1
+    inter_out = -(-(emb + F * (F - 1) // 2) // 8) * 8
+    inter = oid
+    ibytes = 2.0 * (F * emb + inter_out)
+    ops.append(Operator(inter, "interaction", act_bytes_per_sample=2.0 * F * emb, out_bytes_per_sample=2.0 * inter_out,
+                        fwd_cost=CostCurve.affine(LAUNCH_MS * (F + 1), 2 * ibytes / BYTES_PER_MS),
+                        bwd_cost=CostCurve.affine(LAUNCH_MS * (F + 1), 3 * ibytes / BYTES_PER_MS)))
+    specs[inter] = LayerSpec("interaction", F, inter_out, extra=(emb, emb + F * (F - 1) // 2))
+    edges += [(bottom_end, inter)] + [(t, inter) for t in table_ids]
+    oid += 1
+    prev, dprev = inter, inter_out
+    for l in range(3):
+        op, spec = _dense(oid, f"top{l}", dprev, hidden, "relu", 2)
+        ops.append(op)
+        specs[oid] = spec
+        edges.append((prev, oid))
+        prev, dprev = oid, hidden
+        oid += 1
+    op, spec = _head(oid, "head_bce", "bce_head", dprev, 1, 2, "y")
+    ops.append(op)
+    specs[oid] = spec
+    edges.append((prev, oid))
+    data["y"] = ((), "binary")
+    flops = sum(6.0 * s.in_dim * max(1, s.out_dim) for s in specs.values() if s.kind in ("dense", "bce_head"))
+    flops += 6.0 * F * (F - 1) / 2 * emb
+    byts = tables * (3 * bag * emb * 4 + 2 * bag * 8 + 2 * emb * 2)
+    return Workload("dlrm", ComputationGraph(ops, edges), specs, data, B, "bf16",
+                    flops_per_sample=flops, bytes_per_sample=float(byts))
+
+
+PRESETS = {"toy": toy, "candle": candle, "dlrm": dlrm}
 
 
 def make(name: str, **kw) -> Workload:

@@ -199,3 +199,43 @@ def test_wgrad_sgd_fused(cuda_lib, M, accumulate):
     assert _rel(grad, gref) < 1e-4
     assert torch.allclose(master, master0 - 0.01 * gref, rtol=1e-5, atol=1e-5)
     assert torch.equal(shadow, master.bfloat16())
+
+
+def test_embbag_and_interaction_kernels(cuda_lib):
+    g = torch.Generator(device="cuda").manual_seed(21)
+    rows, M, bag, F = 5000, 300, 100, 27
+    table = torch.randn(rows, 64, device="cuda", generator=g)
+    idx = torch.randint(0, rows, (M, bag), device="cuda", generator=g)
+    out = torch.empty(M, 64, device="cuda", dtype=torch.bfloat16)
+    cuda_lib.embbag_fwd(out, table, idx)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.embedding_bag(idx, table, mode="sum")
+    assert _rel(out, ref) < 1e-2
+    dp = torch.randn(M, 64, device="cuda", generator=g).bfloat16()
+    t2 = table.clone()
+    cuda_lib.embbag_sgd(t2, dp, idx, 0.1)
+    exp = table.clone().index_add_(0, idx.reshape(-1), (-0.1 * dp.float())[:, None, :].expand(M, bag, 64).reshape(-1, 64))
+    torch.cuda.synchronize()
+    assert torch.allclose(t2, exp, rtol=1e-5, atol=1e-5)
+    z = torch.randn(M, F * 64, device="cuda", generator=g).bfloat16()
+    cols = 416
+    o = torch.empty(M, cols, device="cuda", dtype=torch.bfloat16)
+    cuda_lib.interaction_fwd(o, z, F, cols)
+    zz = z.float().reshape(M, F, 64)
+    d = torch.bmm(zz, zz.transpose(1, 2))
+    ii = torch.tensor([i for i in range(F) for j in range(i)], device="cuda")
+    jj = torch.tensor([j for i in range(F) for j in range(i)], device="cuda")
+    ref = torch.cat([zz[:, 0], d[:, ii, jj], torch.zeros(M, cols - 64 - len(ii), device="cuda")], 1)
+    torch.cuda.synchronize()
+    assert _rel(o, ref) < 1e-2
+    dout = torch.randn(M, cols, device="cuda", generator=g).bfloat16()
+    dz = torch.empty_like(z)
+    cuda_lib.interaction_bwd(dz, dout, z, F, True)
+    zt = zz.clone().requires_grad_(True)
+    dd = torch.bmm(zt, zt.transpose(1, 2))
+    y = torch.cat([zt[:, 0], dd[:, ii, jj]], 1)
+    y.backward(dout.float()[:, :64 + len(ii)])
+    gref = zt.grad.clone()
+    gref[:, 0] *= (zz[:, 0] > 0).float()
+    torch.cuda.synchronize()
+    assert _rel(dz.float().reshape(M, F, 64), gref) < 1e-2
