@@ -104,6 +104,8 @@ def _workload(name: str, world: int, per_gpu: int | None):
         return W.toy(B=(per_gpu or 64) * world)
     if name == "dlrm":
         return W.dlrm(B=(per_gpu or 8192) * world)
+    if name == "mmt":
+        return W.mmt(B=(per_gpu or 16) * world)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -127,7 +129,7 @@ def cpu_reference_run(wl_name: str, sample_B: int, steps: int):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    sample = {"candle": 32, "toy": 64, "dlrm": 16}[args.workload]
+    sample = {"candle": 32, "toy": 64, "dlrm": 16, "mmt": 1}[args.workload]
     val, dt = cpu_reference_run(args.workload, sample, max(1, min(args.steps, 3)))
     cores = torch.get_num_threads()
     line = {
@@ -149,7 +151,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="candle", choices=["candle", "toy", "dlrm"])
+    ap.add_argument("--workload", default="candle", choices=["candle", "toy", "dlrm", "mmt"])
     ap.add_argument("--mode", default="gpp", choices=["gpp", "spp"])
     ap.add_argument("--per-gpu-batch", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -306,7 +308,7 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
-            sample = {"candle": 32, "toy": 64, "dlrm": 16}[args.workload]
+            sample = {"candle": 32, "toy": 64, "dlrm": 16, "mmt": 1}[args.workload]
             cv, cdt = cpu_reference_run(args.workload, sample, 2)
             cpu = {"value": round(cv, 3), "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "port",
                    "sample": f"{args.workload}, 2 steps x B={sample}, monolithic torch-CPU training step "

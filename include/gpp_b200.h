@@ -20,7 +20,8 @@
  *   gpp_mse_loss / gpp_bce_loss / gpp_ce_loss   fused loss + dLoss kernels
  *   gpp_colsum                  bias gradient
  *   gpp_sgd_step                fused optimizer over a stage's parameters
- *   gpp_layernorm_fwd / _bwd    MMT pre-LN
+ *   gpp_layernorm_fwd / _bwd, gpp_softmax_fwd / _bwd, gpp_meanpool_fwd / _bwd,
+ *   gpp_gemm_batched            MMT pre-LN transformer layer (attention as batched GEMMs)
  *   gpp_embbag_fwd / gpp_embbag_sgd        DLRM embedding-bag and its sparse SGD scatter
  *   gpp_interaction_fwd / _bwd  DLRM dot interaction
  *   gpp_copy_rows               strided row-block copy (concat slices, DP re-shard,
@@ -140,6 +141,35 @@ int gpp_copy_rows(void* dst, int64_t lddst, const void* src, int64_t ldsrc, int6
                   int64_t cols, int elem_bytes, void* stream);
 /* dst_f32[i] = float(src[i]) or dst_bf16[i] = bf16(src_f32[i]). */
 int gpp_cast(void* dst, int dst_dtype, const void* src, int src_dtype, int64_t n, void* stream);
+
+/* ---- MMT transformer layer: pre-LN, attention softmax, mean-pool ---- */
+/* y = LN(x) * gamma + beta per row of D (D in {128,256,512,1024}); saves mean / rstd [T]. */
+int gpp_layernorm_fwd(void* y, float* mean, float* rstd, const void* x, const float* gamma,
+                      const float* beta, int64_t T, int64_t D, float eps, void* stream);
+/* dx = LN'(dy) (+ dres, the residual-branch gradient); dgamma/dbeta (+)= column sums. */
+int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, const void* x,
+                      const float* mean, const float* rstd, const float* gamma, const void* dres,
+                      int64_t T, int64_t D, int accumulate, void* stream);
+/* P[R, L] = softmax(scores) row-wise (fp32 scores, pre-scaled), bf16 out. */
+int gpp_softmax_fwd(void* p, const float* scores, int64_t R, int64_t L, void* stream);
+/* dS = scale * P * (dP - rowsum(dP * P)). */
+int gpp_softmax_bwd(void* ds, const void* p, const float* dp, int64_t R, int64_t L, float scale,
+                    void* stream);
+/* out[m, :D] = mean over S token rows of x[m*S : (m+1)*S, :D];  bwd broadcasts dout / S. */
+int gpp_meanpool_fwd(void* out, int64_t ldo, const void* x, int64_t M, int64_t S, int64_t D,
+                     void* stream);
+int gpp_meanpool_bwd(void* dx, const void* dout, int64_t lddo, int64_t M, int64_t S, int64_t D,
+                     void* stream);
+/* Batched GEMM over batch z = hi*nlo + lo (attention: z = sample*heads + head): each batch
+ * multiplies sub-matrices of the same operands at (m,k)/(n,k) coordinate offsets
+ * X0 + hi*X_hi + lo*X_lo and writes C at element offset c0 + hi*c_hi + lo*c_lo.
+ * spec = {nbatch, nlo, a_m0, a_m_hi, a_m_lo, a_k0, a_k_hi, a_k_lo, b_n0, b_n_hi, b_n_lo,
+ *         b_k0, b_k_hi, b_k_lo, c0, c_hi, c_lo};
+ * a_rows / b_rows = row counts of the full operands; K % 64 == 0. */
+int gpp_gemm_batched(void* c, int64_t ldc, const void* a, int64_t lda, int64_t a_rows, int a_mn,
+                     const void* b, int64_t ldb, int64_t b_rows, int b_mn, int64_t M, int64_t N,
+                     int64_t K, float alpha, float beta, int out_f32, const int64_t* spec,
+                     void* stream);
 
 /* ---- DLRM: embedding bags and the dot interaction ------------- */
 /* pooled[m, :D] = sum_b table[idx[m*ldi + b], :D]; fp32 table [rows, D], bf16 pooled, D = 64. */

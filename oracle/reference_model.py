@@ -53,6 +53,8 @@ class ReferenceModel:
                 out[o] = _round(y, self.bf16)
             elif spec.kind == "concat":
                 out[o] = torch.cat([out[u] for u in g.predecessors(o)], dim=1)
+            elif spec.kind == "mmt_layer":
+                out[o] = self._mmt_layer(o, spec, x)
             elif spec.kind == "embbag":
                 pooled = torch.nn.functional.embedding_bag(batch[spec.data_key], P[(o, "table")], mode="sum")
                 out[o] = _round(pooled, self.bf16)
@@ -81,6 +83,29 @@ class ReferenceModel:
             else:
                 raise NotImplementedError(spec.kind)
         return total
+
+    def _mmt_layer(self, o, spec, xflat):
+        """Pre-LN encoder layer with the device path's bf16 rounding points."""
+        S, d, H, ffn, pool = spec.extra
+        P, bf = self.params, self.bf16
+        R = lambda t: _round(t, bf)
+        W = lambda n: _round(P[(o, n)], bf)
+        B = xflat.shape[0]
+        x = xflat.reshape(B * S, d)
+        h1 = R(torch.nn.functional.layer_norm(x, (d,), P[(o, "ln1_g")], P[(o, "ln1_b")], eps=1e-5))
+        qkv = R(h1 @ W("wqkv").t() + P[(o, "bqkv")])
+        dh = d // H
+        q, k, v = (qkv[:, i * d:(i + 1) * d].reshape(B, S, H, dh).transpose(1, 2) for i in range(3))
+        scores = (q @ k.transpose(-1, -2)) / dh**0.5
+        pr = R(torch.softmax(scores, dim=-1))
+        att = R((pr @ v).transpose(1, 2).reshape(B * S, d))
+        y1 = R(att @ W("wo").t() + P[(o, "bo")] + x)
+        h2 = R(torch.nn.functional.layer_norm(y1, (d,), P[(o, "ln2_g")], P[(o, "ln2_b")], eps=1e-5))
+        f = R(torch.nn.functional.gelu(h2 @ W("w1").t() + P[(o, "b1")]))
+        y2 = R(f @ W("w2").t() + P[(o, "b2")] + y1)
+        if pool:
+            return R(y2.reshape(B, S, d).mean(1))
+        return y2.reshape(B, S * d)
 
     def load_params(self, params: dict):
         """Re-synchronise to another run's master weights (per-step parity without drift)."""

@@ -160,3 +160,61 @@ class TorchBackend:
         if mask_first:
             d[:, 0] *= (zz[:, 0] > 0).float()
         dz.copy_(d.reshape(z.shape[0], F * 64))
+
+    # MMT -------------------------------------------------------------------
+    def layernorm_fwd(self, y, mean, rstd, x, g, b, eps=1e-5):
+        xf = x.float()
+        mu = xf.mean(1)
+        var = ((xf - mu[:, None]) ** 2).mean(1)
+        rs = torch.rsqrt(var + eps)
+        y.copy_((xf - mu[:, None]) * rs[:, None] * g + b)
+        mean.copy_(mu)
+        rstd.copy_(rs)
+
+    def layernorm_bwd(self, dx, dg, db, dy, x, mean, rstd, g, dres=None, accumulate=False):
+        xf, dyf = x.float(), dy.float()
+        xh = (xf - mean[:, None]) * rstd[:, None]
+        gy = dyf * g
+        m1 = gy.mean(1, keepdim=True)
+        m2 = (gy * xh).mean(1, keepdim=True)
+        v = rstd[:, None] * (gy - m1 - xh * m2)
+        if dres is not None:
+            v = v + dres.float()
+        dx.copy_(v)
+        a, c = (dyf * xh).sum(0), dyf.sum(0)
+        if accumulate:
+            dg.add_(a)
+            db.add_(c)
+        else:
+            dg.copy_(a)
+            db.copy_(c)
+
+    def softmax_fwd(self, p, scores):
+        p.copy_(torch.softmax(scores, dim=1))
+
+    def softmax_bwd(self, ds, p, dp, scale):
+        pf = p.float()
+        ds.copy_(scale * pf * (dp - (dp * pf).sum(1, keepdim=True)))
+
+    def meanpool_fwd(self, out, x, M, S, D):
+        out.copy_(x.float().reshape(M, S, D).mean(1))
+
+    def meanpool_bwd(self, dx, dout, M, S, D):
+        dx.copy_((dout.float()[:, None, :] / S).expand(M, S, D).reshape(M * S, D))
+
+    def gemm_batched(self, c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, spec, alpha=1.0,
+                     out_f32=False):
+        (nb, nlo, am0, amh, aml, ak0, akh, akl, bn0, bnh, bnl, bk0, bkh, bkl, c0, chi, clo) = spec
+        A2 = a.reshape(a_rows, lda).float()
+        B2 = b.reshape(b_rows, ldb).float()
+        cf = c.reshape(-1)
+        for z in range(nb):
+            hi, lo = divmod(z, nlo)
+            am, ak = am0 + hi * amh + lo * aml, ak0 + hi * akh + lo * akl
+            bn, bk = bn0 + hi * bnh + lo * bnl, bk0 + hi * bkh + lo * bkl
+            Am = A2[ak:ak + K, am:am + M].t() if a_mn else A2[am:am + M, ak:ak + K]
+            Bm = B2[bk:bk + K, bn:bn + N].t() if b_mn else B2[bn:bn + N, bk:bk + K]
+            Cz = alpha * (Am @ Bm.t())
+            off = c0 + hi * chi + lo * clo
+            idx = off + torch.arange(M)[:, None] * ldc + torch.arange(N)[None, :]
+            cf[idx.reshape(-1)] = Cz.reshape(-1).to(cf.dtype)

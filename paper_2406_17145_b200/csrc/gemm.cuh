@@ -31,6 +31,21 @@ struct EpiParams {
   int64_t split_stride;  // split-K: partial s is written at (float*)out + s * split_stride
 };
 
+// Batched GEMM (attention): batch z = hi * nlo + lo.  Each batch multiplies logical
+// sub-matrices of the SAME 2-D operands, offset in (m, k) / (n, k) coordinates, and
+// writes C (and aux / pre) at element offset z_hi * c_hi + z_lo * c_lo.  Requires the
+// per-batch K to be a multiple of 64 (a K-tile never straddles two batches).
+struct BatchSpec {
+  int nbatch = 1, nlo = 1;
+  int a_m0 = 0, a_m_hi = 0, a_m_lo = 0, a_k0 = 0, a_k_hi = 0, a_k_lo = 0;
+  int b_n0 = 0, b_n_hi = 0, b_n_lo = 0, b_k0 = 0, b_k_hi = 0, b_k_lo = 0;
+  int64_t c0 = 0, c_hi = 0, c_lo = 0;
+};
+
+// Batched bf16 GEMM (1-CTA tcgen05 kernel over batch x tiles).
+int tc_gemm_batched(int epi, const void* a, int64_t lda, int64_t a_rows, int a_mn, const void* b,
+                    int64_t ldb, int64_t b_rows, int b_mn, const EpiParams& ep, const BatchSpec& bs,
+                    int64_t M, int64_t N, int64_t K, cudaStream_t stream);
 // bf16 operands, tcgen05 + TMA (gemm_sm100.cu).
 int tc_gemm(int epi, const void* a, int64_t lda, int a_mn, const void* b, int64_t ldb, int b_mn,
             const EpiParams& ep, int64_t M, int64_t N, int64_t K, cudaStream_t stream);

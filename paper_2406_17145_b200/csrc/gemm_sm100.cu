@@ -305,7 +305,7 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b, EpiParams ep, int M, int N, int K,
-                   int k_splits) {
+                   int k_splits, BatchSpec bs) {
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -323,8 +323,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_blocks = (N + BN - 1) / BN;
-  const int tile = static_cast<int>(blockIdx.x) / k_splits;
-  const int split = static_cast<int>(blockIdx.x) % k_splits;
+  const int m_blocks = (M + BM - 1) / BM;
+  const int per_batch = m_blocks * n_blocks * k_splits;
+  const int z = static_cast<int>(blockIdx.x) / per_batch;
+  const int z_hi = z / bs.nlo, z_lo = z % bs.nlo;
+  const int unit = static_cast<int>(blockIdx.x) % per_batch;
+  const int tile = unit / k_splits;
+  const int split = unit % k_splits;
+  const int am_off = bs.a_m0 + z_hi * bs.a_m_hi + z_lo * bs.a_m_lo;
+  const int ak_off = bs.a_k0 + z_hi * bs.a_k_hi + z_lo * bs.a_k_lo;
+  const int bn_off = bs.b_n0 + z_hi * bs.b_n_hi + z_lo * bs.b_n_lo;
+  const int bk_off = bs.b_k0 + z_hi * bs.b_k_hi + z_lo * bs.b_k_lo;
   const int m_blk = tile / n_blocks;
   const int n_blk = tile % n_blocks;
   const int kb_per = ((K + BK - 1) / BK + k_splits - 1) / k_splits;
@@ -332,6 +341,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int num_kb = min((K + BK - 1) / BK, kb0 + kb_per) - kb0;
   EpiParams epu = ep;
   if (k_splits > 1) epu.out = reinterpret_cast<float*>(ep.out) + split * ep.split_stride;
+  if (bs.nbatch > 1 || bs.c0 != 0) {
+    const int64_t c_off = bs.c0 + z_hi * bs.c_hi + z_lo * bs.c_lo;
+    const int esz = (EPI == EPI_F32 || EPI == EPI_SGD) ? 4 : 2;
+    epu.out = static_cast<char*>(epu.out) + c_off * esz;
+    if (ep.aux) epu.aux = static_cast<const char*>(ep.aux) + c_off * 2;
+    if (ep.pre) epu.pre = static_cast<char*>(ep.pre) + c_off * 2;
+  }
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
@@ -366,18 +382,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint8_t* b_dst = a_dst + A_BYTES;
         mbar_expect_tx(&full_bar[s], STAGE_BYTES);
         if constexpr (!A_MN) {
-          tma_load_2d(a_dst, &tma_a, &full_bar[s], (kb0 + kb) * BK, m_blk * BM);
+          tma_load_2d(a_dst, &tma_a, &full_bar[s], (kb0 + kb) * BK + ak_off, m_blk * BM + am_off);
         } else {
 #pragma unroll
           for (int c = 0; c < BM / 64; ++c)
-            tma_load_2d(a_dst + c * 8192, &tma_a, &full_bar[s], m_blk * BM + c * 64, (kb0 + kb) * BK);
+            tma_load_2d(a_dst + c * 8192, &tma_a, &full_bar[s], m_blk * BM + c * 64 + am_off, (kb0 + kb) * BK + ak_off);
         }
         if constexpr (!B_MN) {
-          tma_load_2d(b_dst, &tma_b, &full_bar[s], (kb0 + kb) * BK, n_blk * BN);
+          tma_load_2d(b_dst, &tma_b, &full_bar[s], (kb0 + kb) * BK + bk_off, n_blk * BN + bn_off);
         } else {
 #pragma unroll
           for (int c = 0; c < BN / 64; ++c)
-            tma_load_2d(b_dst + c * 8192, &tma_b, &full_bar[s], n_blk * BN + c * 64, (kb0 + kb) * BK);
+            tma_load_2d(b_dst + c * 8192, &tma_b, &full_bar[s], n_blk * BN + c * 64 + bn_off, (kb0 + kb) * BK + bk_off);
         }
       }
     }
@@ -689,15 +705,19 @@ static int make_map(CUtensorMap* out, const void* ptr, int64_t inner, int64_t ou
 
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 static int launch_tc(const void* a, int64_t lda, const void* b, int64_t ldb, const EpiParams& ep,
-                     int64_t M, int64_t N, int64_t K, int k_splits, cudaStream_t stream) {
+                     int64_t M, int64_t N, int64_t K, int k_splits, cudaStream_t stream,
+                     const BatchSpec& bs = BatchSpec(), int64_t a_inner = -1, int64_t a_outer = -1,
+                     int64_t b_inner = -1, int64_t b_outer = -1) {
   CUtensorMap ma, mb;
   int rc;
   // K-major operand: inner = K, outer = rows;  MN-major: inner = rows, outer = K.
-  if (!A_MN) rc = make_map(&ma, a, K, M, lda, BK, BM);
-  else rc = make_map(&ma, a, M, K, lda, 64, BK);
+  // Batched calls pass the full operand extents (a_inner/outer...) so per-batch offsets
+  // stay inside one descriptor.
+  if (!A_MN) rc = make_map(&ma, a, a_inner > 0 ? a_inner : K, a_outer > 0 ? a_outer : M, lda, BK, BM);
+  else rc = make_map(&ma, a, a_inner > 0 ? a_inner : M, a_outer > 0 ? a_outer : K, lda, 64, BK);
   if (rc) return rc;
-  if (!B_MN) rc = make_map(&mb, b, K, N, ldb, BK, BN);
-  else rc = make_map(&mb, b, N, K, ldb, 64, BK);
+  if (!B_MN) rc = make_map(&mb, b, b_inner > 0 ? b_inner : K, b_outer > 0 ? b_outer : N, ldb, BK, BN);
+  else rc = make_map(&mb, b, b_inner > 0 ? b_inner : N, b_outer > 0 ? b_outer : K, ldb, 64, BK);
   if (rc) return rc;
 
   constexpr int STAGE_BYTES = (BM + BN) * BK * 2;
@@ -709,9 +729,9 @@ static int launch_tc(const void* a, int64_t lda, const void* b, int64_t ldb, con
     attr_set = true;
   }
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(tiles * k_splits),
+  gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(tiles * k_splits * bs.nbatch),
                                                 NUM_THREADS, SMEM, stream>>>(
-      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits);
+      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits, bs);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("gemm_tc launch: ") + cudaGetErrorString(e));
@@ -947,7 +967,42 @@ int check_operands(const void* a, int64_t lda, int a_mn, const void* b, int64_t 
   return GPP_OK;
 }
 
+template <bool A_MN, bool B_MN, int EPI>
+static int batched_bn(const void* a, int64_t lda, int64_t a_rows, const void* b, int64_t ldb,
+                      int64_t b_rows, const EpiParams& ep, const BatchSpec& bs, int64_t M, int64_t N,
+                      int64_t K, cudaStream_t stream) {
+  // full operand extents: K-major -> (inner = ld, outer = rows); MN-major -> (inner = ld, outer = rows)
+  const int64_t ai = lda, ao = a_rows, bi = ldb, bo = b_rows;
+  if (N > 128)
+    return launch_tc<256, 4, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, 1, stream, bs, ai, ao, bi, bo);
+  return launch_tc<128, 6, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, 1, stream, bs, ai, ao, bi, bo);
+}
+
+template <int EPI>
+static int batched_layout(const void* a, int64_t lda, int64_t a_rows, int a_mn, const void* b,
+                          int64_t ldb, int64_t b_rows, int b_mn, const EpiParams& ep,
+                          const BatchSpec& bs, int64_t M, int64_t N, int64_t K, cudaStream_t s) {
+  if (!a_mn && !b_mn) return batched_bn<false, false, EPI>(a, lda, a_rows, b, ldb, b_rows, ep, bs, M, N, K, s);
+  if (!a_mn && b_mn) return batched_bn<false, true, EPI>(a, lda, a_rows, b, ldb, b_rows, ep, bs, M, N, K, s);
+  if (a_mn && !b_mn) return batched_bn<true, false, EPI>(a, lda, a_rows, b, ldb, b_rows, ep, bs, M, N, K, s);
+  return batched_bn<true, true, EPI>(a, lda, a_rows, b, ldb, b_rows, ep, bs, M, N, K, s);
+}
+
 }  // namespace tc
+
+int tc_gemm_batched(int epi, const void* a, int64_t lda, int64_t a_rows, int a_mn, const void* b,
+                    int64_t ldb, int64_t b_rows, int b_mn, const EpiParams& ep, const BatchSpec& bs,
+                    int64_t M, int64_t N, int64_t K, cudaStream_t stream) {
+  GPP_ARG_CHECK(M > 0 && N > 0 && K > 0 && bs.nbatch >= 1 && bs.nlo >= 1, "bad shape");
+  GPP_ARG_CHECK(K % 64 == 0, "batched GEMM needs K % 64 == 0 (no K-tile may straddle batches)");
+  GPP_ARG_CHECK((reinterpret_cast<uintptr_t>(a) & 15) == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0 &&
+                    lda % 8 == 0 && ldb % 8 == 0, "TMA alignment");
+  switch (epi) {
+    case EPI_FWD: return tc::batched_layout<EPI_FWD>(a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, ep, bs, M, N, K, stream);
+    case EPI_F32: return tc::batched_layout<EPI_F32>(a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, ep, bs, M, N, K, stream);
+    default: return tc::batched_layout<EPI_BF16>(a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, ep, bs, M, N, K, stream);
+  }
+}
 
 // Entry points used by capi.cu.
 int tc_gemm(int epi, const void* a, int64_t lda, int a_mn, const void* b, int64_t ldb, int b_mn,

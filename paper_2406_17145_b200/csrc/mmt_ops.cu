@@ -1,0 +1,381 @@
+// Multi-Modal Transformer (MMT) layer operators around the tcgen05 GEMMs (
+// SURVEY.md §2.3): pre-LN LayerNorm fwd/bwd, attention softmax fwd/bwd over fp32 scores,
+// token mean-pool fwd/bwd, and the batched attention GEMM entry point.  Warp-per-row,
+// registers only, fp32 statistics; deterministic column reductions via partial buffers.
+#include "gemm.cuh"
+
+namespace gpp {
+namespace {
+
+__device__ __forceinline__ float wsum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float wmax(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ---- LayerNorm: y = (x - mu) * rstd * g + b   (D <= 32 * 64, D % 64 == 0) --------------
+template <int PER>  // elements per lane = D / 32
+__global__ void __launch_bounds__(256) ln_fwd_kernel(bf16* __restrict__ y, float* __restrict__ mean,
+                                                     float* __restrict__ rstd,
+                                                     const bf16* __restrict__ x,
+                                                     const float* __restrict__ g,
+                                                     const float* __restrict__ b, int64_t T, int D,
+                                                     float eps) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= T) return;
+  const bf16* xr = x + r * D;
+  float v[PER];
+#pragma unroll
+  for (int i = 0; i < PER / 2; ++i) {
+    const float2 f = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(xr)[lane + 32 * i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) s += v[i];
+  const float mu = wsum(s) / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) q += (v[i] - mu) * (v[i] - mu);
+  const float rs = rsqrtf(wsum(q) / D + eps);
+  bf16* yr = y + r * D;
+#pragma unroll
+  for (int i = 0; i < PER / 2; ++i) {
+    const int c = 2 * (lane + 32 * i);
+    const float a0 = (v[2 * i] - mu) * rs * g[c] + b[c];
+    const float a1 = (v[2 * i + 1] - mu) * rs * g[c + 1] + b[c + 1];
+    reinterpret_cast<__nv_bfloat162*>(yr)[lane + 32 * i] = __floats2bfloat162_rn(a0, a1);
+  }
+  if (lane == 0) {
+    mean[r] = mu;
+    rstd[r] = rs;
+  }
+}
+
+// dx = rstd * (dyg - mean(dyg) - xhat * mean(dyg * xhat)) [+ dres];  per-block partial
+// sums of dgamma = sum dy*xhat and dbeta = sum dy into part[blockIdx.x][2*D].
+template <int PER>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(bf16* __restrict__ dx, float* __restrict__ part,
+                                                     const bf16* __restrict__ dy,
+                                                     const bf16* __restrict__ x,
+                                                     const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd,
+                                                     const float* __restrict__ g,
+                                                     const bf16* __restrict__ dres, int64_t T, int D,
+                                                     int rows_per_block) {
+  extern __shared__ float red[];  // [8 warps][2 * D]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float dg[PER], db[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) dg[i] = db[i] = 0.f;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_block;
+  for (int64_t r = r0 + w; r < r0 + rows_per_block && r < T; r += 8) {
+    const float mu = mean[r], rs = rstd[r];
+    float xh[PER], gy[PER];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER / 2; ++i) {
+      const int c = 2 * (lane + 32 * i);
+      const float2 xv = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(x + r * D)[lane + 32 * i]);
+      const float2 dv = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(dy + r * D)[lane + 32 * i]);
+      xh[2 * i] = (xv.x - mu) * rs;
+      xh[2 * i + 1] = (xv.y - mu) * rs;
+      gy[2 * i] = dv.x * g[c];
+      gy[2 * i + 1] = dv.y * g[c + 1];
+      dg[2 * i] += dv.x * xh[2 * i];
+      dg[2 * i + 1] += dv.y * xh[2 * i + 1];
+      db[2 * i] += dv.x;
+      db[2 * i + 1] += dv.y;
+      s1 += gy[2 * i] + gy[2 * i + 1];
+      s2 += gy[2 * i] * xh[2 * i] + gy[2 * i + 1] * xh[2 * i + 1];
+    }
+    const float m1 = wsum(s1) / D, m2 = wsum(s2) / D;
+#pragma unroll
+    for (int i = 0; i < PER / 2; ++i) {
+      float a0 = rs * (gy[2 * i] - m1 - xh[2 * i] * m2);
+      float a1 = rs * (gy[2 * i + 1] - m1 - xh[2 * i + 1] * m2);
+      if (dres) {
+        const float2 rv = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(dres + r * D)[lane + 32 * i]);
+        a0 += rv.x;
+        a1 += rv.y;
+      }
+      reinterpret_cast<__nv_bfloat162*>(dx + r * D)[lane + 32 * i] = __floats2bfloat162_rn(a0, a1);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PER / 2; ++i) {
+    const int c = 2 * (lane + 32 * i);
+    red[w * 2 * D + c] = dg[2 * i];
+    red[w * 2 * D + c + 1] = dg[2 * i + 1];
+    red[w * 2 * D + D + c] = db[2 * i];
+    red[w * 2 * D + D + c + 1] = db[2 * i + 1];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 2 * D; c += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k * 2 * D + c];
+    part[static_cast<int64_t>(blockIdx.x) * 2 * D + c] = t;
+  }
+}
+
+__global__ void ln_bwd_final_kernel(float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                    const float* __restrict__ part, int nblocks, int D,
+                                    int accumulate) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= 2 * D) return;
+  float t = 0.f;
+  for (int k = 0; k < nblocks; ++k) t += part[static_cast<int64_t>(k) * 2 * D + c];
+  float* o = c < D ? dgamma + c : dbeta + (c - D);
+  *o = accumulate ? *o + t : t;
+}
+
+// ---- attention softmax: P = softmax(s) row-wise (fp32 scores, already scaled) ------------
+template <int PER>
+__global__ void __launch_bounds__(256) softmax_fwd_kernel(bf16* __restrict__ p,
+                                                          const float* __restrict__ s, int64_t R,
+                                                          int L) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= R) return;
+  float v[PER];
+  const float4* sr = reinterpret_cast<const float4*>(s + r * L);
+#pragma unroll
+  for (int i = 0; i < PER / 4; ++i) {
+    const float4 f = sr[lane + 32 * i];
+    v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) mx = fmaxf(mx, v[i]);
+  mx = wmax(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    v[i] = __expf(v[i] - mx);
+    sum += v[i];
+  }
+  const float inv = 1.f / wsum(sum);
+  __nv_bfloat162* pr = reinterpret_cast<__nv_bfloat162*>(p + r * L);
+#pragma unroll
+  for (int i = 0; i < PER / 4; ++i) {
+    pr[2 * (lane + 32 * i)] = __floats2bfloat162_rn(v[4 * i] * inv, v[4 * i + 1] * inv);
+    pr[2 * (lane + 32 * i) + 1] = __floats2bfloat162_rn(v[4 * i + 2] * inv, v[4 * i + 3] * inv);
+  }
+}
+
+// dS = scale * P * (dP - sum(dP * P))   (bf16 out; P bf16, dP fp32)
+template <int PER>
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(bf16* __restrict__ ds,
+                                                          const bf16* __restrict__ p,
+                                                          const float* __restrict__ dp, int64_t R,
+                                                          int L, float scale) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= R) return;
+  float pv[PER], gv[PER];
+  const float4* dr = reinterpret_cast<const float4*>(dp + r * L);
+  const __nv_bfloat162* prr = reinterpret_cast<const __nv_bfloat162*>(p + r * L);
+  float dot = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER / 4; ++i) {
+    const float4 f = dr[lane + 32 * i];
+    const float2 a = __bfloat1622float2(prr[2 * (lane + 32 * i)]);
+    const float2 b = __bfloat1622float2(prr[2 * (lane + 32 * i) + 1]);
+    gv[4 * i] = f.x; gv[4 * i + 1] = f.y; gv[4 * i + 2] = f.z; gv[4 * i + 3] = f.w;
+    pv[4 * i] = a.x; pv[4 * i + 1] = a.y; pv[4 * i + 2] = b.x; pv[4 * i + 3] = b.y;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dot += gv[4 * i + j] * pv[4 * i + j];
+  }
+  dot = wsum(dot);
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(ds + r * L);
+#pragma unroll
+  for (int i = 0; i < PER / 4; ++i) {
+    float t[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t[j] = scale * pv[4 * i + j] * (gv[4 * i + j] - dot);
+    o[2 * (lane + 32 * i)] = __floats2bfloat162_rn(t[0], t[1]);
+    o[2 * (lane + 32 * i) + 1] = __floats2bfloat162_rn(t[2], t[3]);
+  }
+}
+
+// ---- token mean-pool over S rows per sample (branch output of MMT) ------------------------
+__global__ void meanpool_fwd_kernel(bf16* __restrict__ out, int64_t ldo, const bf16* __restrict__ x,
+                                    int64_t M, int S, int D) {
+  const int64_t m = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M || c >= D) return;
+  const bf16* xm = x + m * S * D + c;
+  float s = 0.f;
+  for (int t = 0; t < S; ++t) s += __bfloat162float(xm[static_cast<int64_t>(t) * D]);
+  out[m * ldo + c] = __float2bfloat16_rn(s / S);
+}
+
+__global__ void meanpool_bwd_kernel(bf16* __restrict__ dx, const bf16* __restrict__ dout,
+                                    int64_t lddo, int64_t M, int S, int D) {
+  const int64_t n = M * S * D;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = i / (static_cast<int64_t>(S) * D);
+    const int c = static_cast<int>(i % D);
+    dx[i] = __float2bfloat16_rn(__bfloat162float(dout[m * lddo + c]) / S);
+  }
+}
+
+float* ln_scratch(size_t floats) {
+  static float* bufs[64] = {nullptr};
+  static size_t caps[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (caps[dev] < floats) {
+    if (bufs[dev]) cudaFree(bufs[dev]);
+    size_t want = floats < (size_t(4) << 20) ? (size_t(4) << 20) : floats;
+    if (cudaMalloc(&bufs[dev], want * sizeof(float)) != cudaSuccess) {
+      bufs[dev] = nullptr;
+      caps[dev] = 0;
+      return nullptr;
+    }
+    caps[dev] = want;
+  }
+  return bufs[dev];
+}
+
+}  // namespace
+}  // namespace gpp
+
+using namespace gpp;
+
+
+extern "C" {
+
+int gpp_layernorm_fwd(void* y, float* mean, float* rstd, const void* x, const float* gamma,
+                      const float* beta, int64_t T, int64_t D, float eps, void* stream) {
+  GPP_ARG_CHECK(y && mean && rstd && x && gamma && beta && T > 0, "bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned grid = static_cast<unsigned>((T + 7) / 8);
+  const int d = static_cast<int>(D);
+  switch (D) {
+    case 128: ln_fwd_kernel<4><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
+    case 256: ln_fwd_kernel<8><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
+    case 512: ln_fwd_kernel<16><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
+    case 1024: ln_fwd_kernel<32><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
+    default: set_error("layernorm: D must be 128/256/512/1024"); return GPP_ERR_UNSUPPORTED;
+  }
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, const void* x,
+                      const float* mean, const float* rstd, const float* gamma, const void* dres,
+                      int64_t T, int64_t D, int accumulate, void* stream) {
+  GPP_ARG_CHECK(dx && dgamma && dbeta && dy && x && mean && rstd && gamma && T > 0, "bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int rpb = 64;
+  const int nblk = static_cast<int>((T + rpb - 1) / rpb);
+  float* part = ln_scratch(static_cast<size_t>(nblk) * 2 * D);
+  if (!part) { set_error("layernorm scratch allocation failed"); return GPP_ERR_CUDA; }
+  const size_t smem = 8 * 2 * D * sizeof(float);
+  const int d = static_cast<int>(D);
+  auto* dxp = static_cast<bf16*>(dx);
+  auto* dyp = static_cast<const bf16*>(dy);
+  auto* xp = static_cast<const bf16*>(x);
+  auto* drp = static_cast<const bf16*>(dres);
+  switch (D) {
+    case 128: ln_bwd_kernel<4><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
+    case 256: ln_bwd_kernel<8><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
+    case 512: ln_bwd_kernel<16><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
+    case 1024:
+      cudaFuncSetAttribute(ln_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      ln_bwd_kernel<32><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
+    default: set_error("layernorm: D must be 128/256/512/1024"); return GPP_ERR_UNSUPPORTED;
+  }
+  GPP_LAUNCH_CHECK();
+  ln_bwd_final_kernel<<<static_cast<unsigned>((2 * D + 255) / 256), 256, 0, s>>>(dgamma, dbeta, part, nblk, d, accumulate);
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_softmax_fwd(void* p, const float* scores, int64_t R, int64_t L, void* stream) {
+  GPP_ARG_CHECK(p && scores && R > 0, "bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned grid = static_cast<unsigned>((R + 7) / 8);
+  switch (L) {
+    case 128: softmax_fwd_kernel<4><<<grid, 256, 0, s>>>(static_cast<bf16*>(p), scores, R, 128); break;
+    case 256: softmax_fwd_kernel<8><<<grid, 256, 0, s>>>(static_cast<bf16*>(p), scores, R, 256); break;
+    case 512: softmax_fwd_kernel<16><<<grid, 256, 0, s>>>(static_cast<bf16*>(p), scores, R, 512); break;
+    case 1024: softmax_fwd_kernel<32><<<grid, 256, 0, s>>>(static_cast<bf16*>(p), scores, R, 1024); break;
+    default: set_error("softmax: L must be 128/256/512/1024"); return GPP_ERR_UNSUPPORTED;
+  }
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_softmax_bwd(void* ds, const void* p, const float* dp, int64_t R, int64_t L, float scale,
+                    void* stream) {
+  GPP_ARG_CHECK(ds && p && dp && R > 0, "bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned grid = static_cast<unsigned>((R + 7) / 8);
+  auto* o = static_cast<bf16*>(ds);
+  auto* pp = static_cast<const bf16*>(p);
+  switch (L) {
+    case 128: softmax_bwd_kernel<4><<<grid, 256, 0, s>>>(o, pp, dp, R, 128, scale); break;
+    case 256: softmax_bwd_kernel<8><<<grid, 256, 0, s>>>(o, pp, dp, R, 256, scale); break;
+    case 512: softmax_bwd_kernel<16><<<grid, 256, 0, s>>>(o, pp, dp, R, 512, scale); break;
+    case 1024: softmax_bwd_kernel<32><<<grid, 256, 0, s>>>(o, pp, dp, R, 1024, scale); break;
+    default: set_error("softmax: L must be 128/256/512/1024"); return GPP_ERR_UNSUPPORTED;
+  }
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_meanpool_fwd(void* out, int64_t ldo, const void* x, int64_t M, int64_t S, int64_t D,
+                     void* stream) {
+  GPP_ARG_CHECK(out && x && M > 0 && S > 0 && D > 0, "bad argument");
+  dim3 grid(static_cast<unsigned>((D + 127) / 128), static_cast<unsigned>(M));
+  meanpool_fwd_kernel<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<bf16*>(out), ldo, static_cast<const bf16*>(x), M, static_cast<int>(S), static_cast<int>(D));
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_meanpool_bwd(void* dx, const void* dout, int64_t lddo, int64_t M, int64_t S, int64_t D,
+                     void* stream) {
+  GPP_ARG_CHECK(dx && dout && M > 0, "bad argument");
+  int64_t n = M * S * D;
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  meanpool_bwd_kernel<<<static_cast<unsigned>(g), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<bf16*>(dx), static_cast<const bf16*>(dout), lddo, M, static_cast<int>(S), static_cast<int>(D));
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+// Batched GEMM (attention): spec = {nbatch, nlo, a_m0, a_m_hi, a_m_lo, a_k0, a_k_hi, a_k_lo,
+// b_n0, b_n_hi, b_n_lo, b_k0, b_k_hi, b_k_lo, c0, c_hi, c_lo} (17 ints); a_rows / b_rows =
+// full operand row counts.
+int gpp_gemm_batched(void* c, int64_t ldc, const void* a, int64_t lda, int64_t a_rows, int a_mn,
+                     const void* b, int64_t ldb, int64_t b_rows, int b_mn, int64_t M, int64_t N,
+                     int64_t K, float alpha, float beta, int out_f32, const int64_t* spec,
+                     void* stream) {
+  GPP_ARG_CHECK(c && a && b && spec, "null pointer");
+  BatchSpec bs;
+  bs.nbatch = static_cast<int>(spec[0]);
+  bs.nlo = static_cast<int>(spec[1]);
+  bs.a_m0 = static_cast<int>(spec[2]); bs.a_m_hi = static_cast<int>(spec[3]); bs.a_m_lo = static_cast<int>(spec[4]);
+  bs.a_k0 = static_cast<int>(spec[5]); bs.a_k_hi = static_cast<int>(spec[6]); bs.a_k_lo = static_cast<int>(spec[7]);
+  bs.b_n0 = static_cast<int>(spec[8]); bs.b_n_hi = static_cast<int>(spec[9]); bs.b_n_lo = static_cast<int>(spec[10]);
+  bs.b_k0 = static_cast<int>(spec[11]); bs.b_k_hi = static_cast<int>(spec[12]); bs.b_k_lo = static_cast<int>(spec[13]);
+  bs.c0 = spec[14]; bs.c_hi = spec[15]; bs.c_lo = spec[16];
+  EpiParams ep{c, ldc, nullptr, nullptr, 0, nullptr, 0, alpha, beta, 0, 0.f, nullptr, 0, 0, 0};
+  return tc_gemm_batched(out_f32 ? EPI_F32 : EPI_BF16, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, ep,
+                         bs, M, N, K, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

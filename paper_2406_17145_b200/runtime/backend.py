@@ -77,3 +77,27 @@ class CudaBackend:
 
     def interaction_bwd(self, dz, dout, z, F, mask_first):
         lib.interaction_bwd(dz, dout, z, F, mask_first)
+
+    # MMT -------------------------------------------------------------------
+    def layernorm_fwd(self, y, mean, rstd, x, g, b, eps=1e-5):
+        lib.layernorm_fwd(y, mean, rstd, x, g, b, eps)
+
+    def layernorm_bwd(self, dx, dg, db, dy, x, mean, rstd, g, dres=None, accumulate=False):
+        lib.layernorm_bwd(dx, dg, db, dy, x, mean, rstd, g, dres=dres, accumulate=accumulate)
+
+    def softmax_fwd(self, p, scores):
+        lib.softmax_fwd(p, scores)
+
+    def softmax_bwd(self, ds, p, dp, scale):
+        lib.softmax_bwd(ds, p, dp, scale)
+
+    def meanpool_fwd(self, out, x, M, S, D):
+        lib.meanpool_fwd(out, x, M, S, D)
+
+    def meanpool_bwd(self, dx, dout, M, S, D):
+        lib.meanpool_bwd(dx, dout, M, S, D)
+
+    def gemm_batched(self, c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, spec, alpha=1.0,
+                     out_f32=False):
+        lib.gemm_batched(c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, spec, alpha=alpha,
+                         out_f32=out_f32)

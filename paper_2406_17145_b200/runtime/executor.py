@@ -98,6 +98,9 @@ def init_params(spec: LayerSpec, op_id: int, seed: int) -> list[tuple[str, torch
         return [("w", w), ("b", b)]
     if spec.kind == "embbag":
         return [("table", torch.randn(spec.in_dim, spec.out_dim, generator=g) * 0.05)]
+    if spec.kind == "mmt_layer":
+        from .mmt import mmt_params
+        return mmt_params(spec, op_id, seed)
     return []
 
 
@@ -247,7 +250,9 @@ class Executor:
                 total += -(-t.numel() // _ALIGN) * _ALIGN
         # dense weights first: with the fused optimizer they are updated by their wgrad
         # epilogues and the flat SGD kernel only walks the remainder [rest_off:]
-        fusable = lambda o, name: self.layers[o].kind == "dense" and name == "w"
+        from .mmt import WEIGHTS as MMT_WEIGHTS
+        fusable = lambda o, name: (self.layers[o].kind == "dense" and name == "w") or (
+            self.layers[o].kind == "mmt_layer" and name in MMT_WEIGHTS)
         specs.sort(key=lambda t: 0 if fusable(t[0], t[1]) else 1)
         total = max(total, _ALIGN)
         self.master = torch.zeros(total, dtype=torch.float32, device=self.dev)
@@ -286,6 +291,7 @@ class Executor:
         self.out, self.recv, self.gbuf, self.grecv, self.gsend, self.pre = {}, {}, {}, {}, {}, {}
         self.pred, self.dpred = {}, {}
         self.emb_grad, self.zbuf, self.dzbuf = {}, {}, {}
+        self.mmt = {}
         for o in self.ops:
             spec = self.layers[o]
             if spec.kind in ("dense", "concat"):
@@ -310,6 +316,14 @@ class Executor:
                     self.gbuf[o] = self._ring((m, spec.out_dim))
                 # pooled-output gradients of the whole iteration -> one sparse SGD scatter
                 self.emb_grad[o] = torch.zeros((self.n * m, spec.out_dim), dtype=self.dtype, device=self.dev)
+            elif spec.kind == "mmt_layer":
+                from .mmt import MMTLayer
+                self.out[o] = self._ring((m, spec.out_dim))
+                if o in self.out_remote:
+                    self.grecv[o] = self._ring((m, spec.out_dim))
+                elif g.successors(o):
+                    self.gbuf[o] = self._ring((m, spec.out_dim))
+                self.mmt[o] = MMTLayer(self, o, spec)
             elif spec.kind == "interaction":
                 F = spec.in_dim
                 self.out[o] = self._ring((m, spec.out_dim))
@@ -409,6 +423,10 @@ class Executor:
                 y = batch[spec.label_key][j * self.m:(j + 1) * self.m]
                 loss = be.mse_loss if spec.kind == "mse_head" else be.bce_loss
                 loss(self.loss_acc, self.dpred[o][slot], self.pred[o][slot], y, scale)
+            elif spec.kind == "mmt_layer":
+                x = self._input(o, j, slot, batch)
+                lay = self.mmt[o]
+                lay.forward(x.reshape(lay.T, lay.d), self.out[o][slot], slot)
             elif spec.kind == "embbag":
                 idx = batch[spec.data_key][j * self.m:(j + 1) * self.m]
                 be.embbag_fwd(self.out[o][slot], self.tables[o], idx)
@@ -464,6 +482,12 @@ class Executor:
                     be.colsum(self.G[(o, "b")], dz, accumulate)
                 else:
                     be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
+            elif spec.kind == "mmt_layer":
+                lay = self.mmt[o]
+                x = self._input(o, j, slot, batch)
+                dx = self._dx_target(preds[0], slot).reshape(lay.T, lay.d) if needs_dx else None
+                lay.backward(self._dz_of(o, slot), x.reshape(lay.T, lay.d), dx, slot, accumulate,
+                             j == self.last_bw)
             elif spec.kind == "embbag":
                 be.copy_rows(self.emb_grad[o][j * self.m:(j + 1) * self.m], self._dz_of(o, slot))
             elif spec.kind == "interaction":

@@ -51,10 +51,13 @@ _SIGS = {
     "gpp_allgather": ([_vp, _vp, _vp, _i64, _vp], _i32),
     "gpp_group_start": ([], _i32),
     "gpp_group_end": ([], _i32),
-    "gpp_layernorm_fwd": ([_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _vp], _i32),
-    "gpp_layernorm_bwd": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp], _i32),
-    "gpp_attention_fwd": ([_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
-    "gpp_attention_bwd": ([_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
+    "gpp_layernorm_fwd": ([_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp], _i32),
+    "gpp_layernorm_bwd": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _vp], _i32),
+    "gpp_softmax_fwd": ([_vp, _vp, _i64, _i64, _vp], _i32),
+    "gpp_softmax_bwd": ([_vp, _vp, _vp, _i64, _i64, _f32, _vp], _i32),
+    "gpp_meanpool_fwd": ([_vp, _i64, _vp, _i64, _i64, _i64, _vp], _i32),
+    "gpp_meanpool_bwd": ([_vp, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
+    "gpp_gemm_batched": ([_vp, _i64, _vp, _i64, _i64, _i32, _vp, _i64, _i64, _i32, _i64, _i64, _i64, _f32, _f32, _i32, _vp, _vp], _i32),
     "gpp_embbag_fwd": ([_vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp], _i32),
     "gpp_embbag_sgd": ([_vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_interaction_fwd": ([_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
@@ -237,3 +240,42 @@ def interaction_bwd(dz, dout, z, F, mask_first, stream=None):
     M = z.shape[0]
     call("gpp_interaction_bwd", _ptr(dz), _ld(dz), _ptr(dout), _ld(dout), _ptr(z), _ld(z), M, F, 64,
          int(bool(mask_first)), _stream(stream))
+
+
+def layernorm_fwd(y, mean, rstd, x, gamma, beta, eps=1e-5, stream=None):
+    T, D = x.shape
+    call("gpp_layernorm_fwd", _ptr(y), _ptr(mean), _ptr(rstd), _ptr(x), _ptr(gamma), _ptr(beta), T, D,
+         float(eps), _stream(stream))
+
+
+def layernorm_bwd(dx, dgamma, dbeta, dy, x, mean, rstd, gamma, dres=None, accumulate=False, stream=None):
+    T, D = x.shape
+    call("gpp_layernorm_bwd", _ptr(dx), _ptr(dgamma), _ptr(dbeta), _ptr(dy), _ptr(x), _ptr(mean), _ptr(rstd),
+         _ptr(gamma), _ptr(dres), T, D, int(bool(accumulate)), _stream(stream))
+
+
+def softmax_fwd(p, scores, stream=None):
+    R, L = scores.shape
+    call("gpp_softmax_fwd", _ptr(p), _ptr(scores), R, L, _stream(stream))
+
+
+def softmax_bwd(ds, p, dp, scale, stream=None):
+    R, L = dp.shape
+    call("gpp_softmax_bwd", _ptr(ds), _ptr(p), _ptr(dp), R, L, float(scale), _stream(stream))
+
+
+def meanpool_fwd(out, x, M, S, D, stream=None):
+    call("gpp_meanpool_fwd", _ptr(out), _ld(out), _ptr(x), M, S, D, _stream(stream))
+
+
+def meanpool_bwd(dx, dout, M, S, D, stream=None):
+    call("gpp_meanpool_bwd", _ptr(dx), _ptr(dout), _ld(dout), M, S, D, _stream(stream))
+
+
+def gemm_batched(c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, spec, alpha=1.0, beta=0.0,
+                 out_f32=False, stream=None):
+    """Batched GEMM on flat buffers; ``spec`` = 17 ints (see include/gpp_b200.h)."""
+    assert len(spec) == 17
+    arr = (ctypes.c_int64 * 17)(*[int(v) for v in spec])
+    call("gpp_gemm_batched", _ptr(c), ldc, _ptr(a), lda, a_rows, int(a_mn), _ptr(b), ldb, b_rows, int(b_mn),
+         M, N, K, float(alpha), float(beta), int(bool(out_f32)), ctypes.cast(arr, ctypes.c_void_p), _stream(stream))

@@ -266,7 +266,55 @@ def dlrm(B: int = 512, tables: int = 26, rows: int = 1_000_000, bag: int = 100, 
                     flops_per_sample=flops, bytes_per_sample=float(byts))
 
 
-PRESETS = {"toy": toy, "candle": candle, "dlrm": dlrm}
+def mmt_layer_flops(S: int, d: int, ffn: int) -> float:
+    """Forward FLOPs per sample of one encoder layer: 4 projections + QK^T and PV."""
+    return 2.0 * S * d * (3 * d) + 2.0 * S * d * d + 2.0 * 2 * S * d * ffn + 2.0 * 2 * S * S * d
+
+
+def mmt(B: int = 32, branches: int = 4, layers: int = 12, S: int = 512, d: int = 1024, H: int = 16,
+        ffn: int = 4096, classes: int = 1000) -> Workload:
+    """BASELINE configs[2]/[4]: Multi-Modal Transformer — `branches` x `layers` pre-LN encoder
+    layers (d=1024, 16 heads, FFN 4096 GELU, seq 512, non-causal), the last
+    layer of each branch mean-pools its tokens, concat [B, branches*d] -> Linear(., classes) CE
+    (SURVEY.md §8(d) config 3).  One operator per layer (layer granularity)."""
+    ops, specs, edges, data = [], {}, [], {}
+    oid = 0
+    ends = []
+    f_fwd = mmt_layer_flops(S, d, ffn)
+    for t in range(branches):
+        prev = None
+        for l in range(layers):
+            pool = l == layers - 1
+            out_dim = d if pool else S * d
+            params = 4.0 * (4 * d * d + 2 * d * ffn + 9 * d + ffn)
+            acts = 2.0 * S * (10 * d + 2 * ffn) + 2.0 * H * S * S
+            ops.append(Operator(oid, f"b{t}_layer{l}", param_bytes=params, act_bytes_per_sample=acts,
+                                out_bytes_per_sample=2.0 * out_dim,
+                                fwd_cost=_gemm_curve(f_fwd, 10), bwd_cost=_gemm_curve(2 * f_fwd, 24)))
+            specs[oid] = LayerSpec("mmt_layer", S * d, out_dim, data_key=f"x{t}" if l == 0 else None,
+                                   extra=(S, d, H, ffn, pool))
+            if prev is not None:
+                edges.append((prev, oid))
+            prev = oid
+            oid += 1
+        ends.append(prev)
+        data[f"x{t}"] = ((S * d,), "normal")
+    cat = oid
+    op, spec = _concat(cat, "concat", branches * d, 2)
+    ops.append(op)
+    specs[cat] = spec
+    edges += [(e, cat) for e in ends]
+    oid += 1
+    op, spec = _head(oid, "head_ce", "ce_head", branches * d, classes, 2, "label")
+    ops.append(op)
+    specs[oid] = spec
+    edges.append((cat, oid))
+    data["label"] = ((), f"label:{classes}")
+    flops = branches * layers * 3 * f_fwd + 6.0 * branches * d * classes
+    return Workload("mmt", ComputationGraph(ops, edges), specs, data, B, "bf16", flops_per_sample=flops)
+
+
+PRESETS = {"toy": toy, "candle": candle, "dlrm": dlrm, "mmt": mmt}
 
 
 def make(name: str, **kw) -> Workload:

@@ -239,3 +239,87 @@ def test_embbag_and_interaction_kernels(cuda_lib):
     gref[:, 0] *= (zz[:, 0] > 0).float()
     torch.cuda.synchronize()
     assert _rel(dz.float().reshape(M, F, 64), gref) < 1e-2
+
+
+@pytest.mark.parametrize("D", [128, 1024])
+def test_layernorm_kernels(cuda_lib, D):
+    g = torch.Generator(device="cuda").manual_seed(D)
+    T = 777
+    x = torch.randn(T, D, device="cuda", generator=g).bfloat16()
+    gam = 1 + 0.1 * torch.randn(D, device="cuda", generator=g)
+    bet = 0.1 * torch.randn(D, device="cuda", generator=g)
+    y = torch.empty_like(x)
+    mean = torch.empty(T, device="cuda")
+    rstd = torch.empty(T, device="cuda")
+    cuda_lib.layernorm_fwd(y, mean, rstd, x, gam, bet)
+    xt = x.float().clone().requires_grad_(True)
+    gt = gam.clone().requires_grad_(True)
+    bt = bet.clone().requires_grad_(True)
+    ref = torch.nn.functional.layer_norm(xt, (D,), gt, bt, eps=1e-5)
+    torch.cuda.synchronize()
+    assert _rel(y, ref) < 1e-2
+    dy = torch.randn(T, D, device="cuda", generator=g).bfloat16()
+    dres = torch.randn(T, D, device="cuda", generator=g).bfloat16()
+    ref.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.empty(D, device="cuda")
+    db = torch.empty(D, device="cuda")
+    cuda_lib.layernorm_bwd(dx, dg, db, dy, x, mean, rstd, gam, dres=dres)
+    torch.cuda.synchronize()
+    assert _rel(dx, xt.grad + dres.float()) < 1e-2
+    assert _rel(dg, gt.grad) < 1e-3
+    assert _rel(db, bt.grad) < 1e-3
+
+
+def test_softmax_kernels(cuda_lib):
+    g = torch.Generator(device="cuda").manual_seed(4)
+    R, L = 1000, 512
+    s = 3 * torch.randn(R, L, device="cuda", generator=g)
+    p = torch.empty(R, L, device="cuda", dtype=torch.bfloat16)
+    cuda_lib.softmax_fwd(p, s)
+    torch.cuda.synchronize()
+    assert _rel(p, torch.softmax(s, 1)) < 1e-2
+    dp = torch.randn(R, L, device="cuda", generator=g)
+    ds = torch.empty_like(p)
+    cuda_lib.softmax_bwd(ds, p, dp, 0.125)
+    pf = p.float()
+    torch.cuda.synchronize()
+    assert _rel(ds, 0.125 * pf * (dp - (dp * pf).sum(1, keepdim=True))) < 1e-2
+
+
+def test_batched_attention_gemms_match_emulation(cuda_lib):
+    """The seven attention GEMM specs of runtime/mmt.py, GPU vs the torch emulation."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle.torch_backend import TorchBackend
+    from paper_2406_17145_b200.runtime.mmt import _spec
+    g = torch.Generator(device="cuda").manual_seed(8)
+    m, S, d, H = 3, 256, 256, 4
+    dh, T, Z = d // H, m * S, m * H
+    qkv = torch.randn(T, 3 * d, device="cuda", generator=g).bfloat16()
+    P = torch.softmax(torch.randn(Z * S, S, device="cuda", generator=g), 1).bfloat16()
+    do = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    cases = [
+        ("scores", (Z * S, S), torch.float32, S, qkv, 3 * d, T, False, qkv, 3 * d, T, False, S, S, dh,
+         _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S)),
+        ("pv", (T, d), torch.bfloat16, d, P, S, Z * S, False, qkv, 3 * d, T, True, S, dh, S,
+         _spec(Z, H, a_m_hi=H * S, a_m_lo=S, b_n0=2 * d, b_n_lo=dh, b_k_hi=S, c_hi=S * d, c_lo=dh)),
+        ("dv", (T, 3 * d), torch.bfloat16, 3 * d, P, S, Z * S, True, do, d, T, True, S, dh, S,
+         _spec(Z, H, a_k_hi=H * S, a_k_lo=S, b_n_lo=dh, b_k_hi=S, c0=2 * d, c_hi=S * 3 * d, c_lo=dh)),
+        ("dp", (Z * S, S), torch.float32, S, do, d, T, False, qkv, 3 * d, T, False, S, S, dh,
+         _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=2 * d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S)),
+        ("dq", (T, 3 * d), torch.bfloat16, 3 * d, P, S, Z * S, False, qkv, 3 * d, T, True, S, dh, S,
+         _spec(Z, H, a_m_hi=H * S, a_m_lo=S, b_n0=d, b_n_lo=dh, b_k_hi=S, c_hi=S * 3 * d, c_lo=dh)),
+        ("dk", (T, 3 * d), torch.bfloat16, 3 * d, P, S, Z * S, True, qkv, 3 * d, T, True, S, dh, S,
+         _spec(Z, H, a_k_hi=H * S, a_k_lo=S, b_n_lo=dh, b_k_hi=S, c0=d, c_hi=S * 3 * d, c_lo=dh)),
+    ]
+    tb = TorchBackend("cpu")
+    for name, shape, dt, ldc, a, lda, ar, amn, b, ldb, br, bmn, M, N, K, spec in cases:
+        c = torch.zeros(shape, device="cuda", dtype=dt)
+        cuda_lib.gemm_batched(c, ldc, a, lda, ar, amn, b, ldb, br, bmn, M, N, K, spec, alpha=0.5,
+                              out_f32=dt == torch.float32)
+        ref = torch.zeros(shape, dtype=dt)
+        tb.gemm_batched(ref, ldc, a.cpu(), lda, ar, amn, b.cpu(), ldb, br, bmn, M, N, K, spec, alpha=0.5,
+                        out_f32=dt == torch.float32)
+        torch.cuda.synchronize()
+        assert _rel(c.cpu(), ref) < 1e-2, name

@@ -138,3 +138,16 @@ def test_dlrm_bf16_matches_oracle(cuda_lib):
             err = _relerr(got, g, False)
             cos = torch.nn.functional.cosine_similarity(got.double().flatten(), g.double().flatten(), dim=0)
             assert err < 6e-2 and cos > 0.998, (step, k, err, cos.item())
+
+
+def test_mmt_small_bf16_matches_oracle(cuda_lib):
+    """Multi-Modal Transformer (pre-LN layers, batched-GEMM attention, mean-pool, concat,
+    CE head) on the GPU executor vs the oracle (GELU FFN -> smooth -> strict rtol)."""
+    wl = W.mmt(B=8, branches=2, layers=2, S=128, d=128, H=2, ffn=256, classes=64)
+    _check(wl, 4, 2e-2, steps=2)
+
+
+def test_mmt_full_width_layer(cuda_lib):
+    """One full-size MMT layer (S=512, d=1024, 16 heads, FFN 4096) per branch, B=2."""
+    wl = W.mmt(B=2, branches=2, layers=1, S=512, d=1024, H=16, ffn=4096, classes=1000)
+    _check(wl, 1, 2e-2, steps=1)
