@@ -63,6 +63,11 @@ const char* gpp_last_error(void);
 /* Number of kernels this library has launched since load (evidence counter). */
 uint64_t gpp_launch_count(void);
 
+/* One-shot hint: the next GEMM launched from this thread also prefetches
+ * [ptr, ptr + bytes) into L2 (spread over its CTAs, overlapping its main loop) — the
+ * executor points it at the weights / fp32 master the following kernel will read. */
+int gpp_gemm_prefetch_hint(const void* ptr, int64_t bytes);
+
 /* ---- dense operator (Operator fw/bw work, model.py:100-114) ------------- */
 
 /* y[M,N] = act(x[M,K] · w[N,K]^T + bias[N]) (+ residual[M,N] if non-null).

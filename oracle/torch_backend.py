@@ -36,6 +36,9 @@ class TorchBackend:
     def __init__(self, device="cpu"):
         self.device = torch.device(device)
 
+    def prefetch_hint(self, t):
+        pass
+
     def linear_fwd(self, y, x, w, bias, act, residual=None, pre=None):
         z = x.float() @ w.float().t()
         if bias is not None:

@@ -29,7 +29,12 @@ struct EpiParams {
   int64_t ldgrad;
   int store_grad;
   int64_t split_stride;  // split-K: partial s is written at (float*)out + s * split_stride
+  const void* pf_ptr;    // L2 prefetch hint: bytes another kernel will read next (or null)
+  int64_t pf_bytes;
 };
+
+// One-shot L2 prefetch hint consumed by the next GEMM launched on this host thread.
+void take_prefetch_hint(EpiParams& ep);
 
 // Batched GEMM (attention): batch z = hi * nlo + lo.  Each batch multiplies logical
 // sub-matrices of the SAME 2-D operands, offset in (m, k) / (n, k) coordinates, and

@@ -32,6 +32,21 @@ constexpr int NUM_THREADS = 192;
 constexpr int PAIR_EPI_WARPS = 8;                          // two epilogue warpgroups
 constexpr int PAIR_THREADS = 64 + 32 * PAIR_EPI_WARPS;     // + TMA warp + MMA warp
 
+// L2 prefetch of this CTA's share of the hinted buffer (64 KB bulk pieces), issued by an
+// otherwise idle lane so it overlaps the tensor-bound main loop.
+__device__ __forceinline__ void l2_prefetch_share(const EpiParams& ep, int cta, int ncta) {
+  if (ep.pf_ptr == nullptr || ep.pf_bytes <= 0) return;
+  const int64_t total = ep.pf_bytes & ~static_cast<int64_t>(15);
+  const int64_t share = ((total / ncta) + 65535) & ~static_cast<int64_t>(65535);
+  const int64_t beg = static_cast<int64_t>(cta) * share;
+  const int64_t end = beg + share < total ? beg + share : total;
+  const char* base = static_cast<const char*>(ep.pf_ptr);
+  for (int64_t off = beg; off < end; off += 65536) {
+    const uint32_t n = static_cast<uint32_t>(end - off < 65536 ? end - off : 65536);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off), "r"(n) : "memory");
+  }
+}
+
 // 32 bf16 from global (16-byte vector loads when aligned and in bounds).
 __device__ __forceinline__ void load_bf16x32(const bf16* p, bool vec, int n_valid, float (&o)[32]) {
   if (vec) {
@@ -398,6 +413,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
+    if (lane == 1) l2_prefetch_share(ep, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
       for (int kb = 0; kb < num_kb; ++kb) {
@@ -550,6 +566,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       }
     }
   } else if (warp == 1) {
+    if (lane == 1) l2_prefetch_share(ep, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
     if (leader && lane == 0) {
       // ---------------- MMA issuer (leader CTA only) ----------------
       uint32_t it = 0, lt = 0;
@@ -1006,9 +1023,11 @@ int tc_gemm_batched(int epi, const void* a, int64_t lda, int64_t a_rows, int a_m
 
 // Entry points used by capi.cu.
 int tc_gemm(int epi, const void* a, int64_t lda, int a_mn, const void* b, int64_t ldb, int b_mn,
-            const EpiParams& ep, int64_t M, int64_t N, int64_t K, cudaStream_t stream) {
+            const EpiParams& ep_in, int64_t M, int64_t N, int64_t K, cudaStream_t stream) {
   int rc = tc::check_operands(a, lda, a_mn, b, ldb, b_mn, M, N, K);
   if (rc) return rc;
+  EpiParams ep = ep_in;
+  take_prefetch_hint(ep);
   switch (epi) {
     case EPI_FWD:
       return tc::dispatch_layout<EPI_FWD>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);

@@ -373,7 +373,7 @@ int gpp_gemm_batched(void* c, int64_t ldc, const void* a, int64_t lda, int64_t a
   bs.b_n0 = static_cast<int>(spec[8]); bs.b_n_hi = static_cast<int>(spec[9]); bs.b_n_lo = static_cast<int>(spec[10]);
   bs.b_k0 = static_cast<int>(spec[11]); bs.b_k_hi = static_cast<int>(spec[12]); bs.b_k_lo = static_cast<int>(spec[13]);
   bs.c0 = spec[14]; bs.c_hi = spec[15]; bs.c_lo = spec[16];
-  EpiParams ep{c, ldc, nullptr, nullptr, 0, nullptr, 0, alpha, beta, 0, 0.f, nullptr, 0, 0, 0};
+  EpiParams ep{c, ldc, nullptr, nullptr, 0, nullptr, 0, alpha, beta, 0, 0.f, nullptr, 0, 0, 0, nullptr, 0};
   return tc_gemm_batched(out_f32 ? EPI_F32 : EPI_BF16, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, ep,
                          bs, M, N, K, static_cast<cudaStream_t>(stream));
 }

@@ -12,6 +12,15 @@ static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+static thread_local const void* g_pf_ptr = nullptr;
+static thread_local int64_t g_pf_bytes = 0;
+void take_prefetch_hint(EpiParams& ep) {
+  ep.pf_ptr = g_pf_ptr;
+  ep.pf_bytes = g_pf_bytes;
+  g_pf_ptr = nullptr;
+  g_pf_bytes = 0;
+}
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
@@ -314,6 +323,12 @@ using namespace gpp;
 extern "C" {
 
 int gpp_version(void) { return 1; }
+
+int gpp_gemm_prefetch_hint(const void* ptr, int64_t bytes) {
+  g_pf_ptr = ptr;
+  g_pf_bytes = ptr ? bytes : 0;
+  return GPP_OK;
+}
 const char* gpp_last_error(void) { return g_last_error.c_str(); }
 uint64_t gpp_launch_count(void) { return g_launches.load(); }
 
@@ -332,7 +347,7 @@ int gpp_linear_fwd(void* y, int64_t ldy, const void* x, int64_t ldx, const void*
                    int64_t ldpre, int64_t M, int64_t N, int64_t K, int act, int dtype,
                    void* stream) {
   GPP_ARG_CHECK(y && x && w, "null pointer");
-  EpiParams ep{y, ldy, bias, residual, ldres, pre_out, ldpre, 1.f, 0.f, act, 0.f, nullptr, 0, 0, 0};
+  EpiParams ep{y, ldy, bias, residual, ldres, pre_out, ldpre, 1.f, 0.f, act, 0.f, nullptr, 0, 0, 0, nullptr, 0};
   return gemm_any(EPI_FWD, x, ldx, 0, w, ldw, 0, ep, M, N, K, dtype, stream);
 }
 
@@ -341,7 +356,7 @@ int gpp_linear_dgrad(void* dx, int64_t lddx, const void* dy, int64_t lddy, const
                      int64_t K, int act, int dtype, void* stream) {
   GPP_ARG_CHECK(dx && dy && w, "null pointer");
   GPP_ARG_CHECK(act == GPP_ACT_NONE || saved, "act' needs the saved tensor");
-  EpiParams ep{dx, lddx, nullptr, saved, ldsaved, nullptr, 0, 1.f, 0.f, act, 0.f, nullptr, 0, 0, 0};
+  EpiParams ep{dx, lddx, nullptr, saved, ldsaved, nullptr, 0, 1.f, 0.f, act, 0.f, nullptr, 0, 0, 0, nullptr, 0};
   // dx[M,K] = dy[M,N] . w[N,K]: GEMM (M, K, N); B(n=k_in, k=n_out) = w[n_out][k_in] is MN-major.
   return gemm_any(EPI_DGRAD, dy, lddy, 0, w, ldw, 1, ep, M, K, N, dtype, stream);
 }
@@ -350,7 +365,7 @@ int gpp_linear_wgrad(float* dw, int64_t lddw, float* dbias, const void* dy, int6
                      const void* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
                      int accumulate, int dtype, void* stream) {
   GPP_ARG_CHECK(dw && dy && x, "null pointer");
-  EpiParams ep{dw, lddw, nullptr, nullptr, 0, nullptr, 0, 1.f, accumulate ? 1.f : 0.f, 0, 0.f, nullptr, 0, 0, 0};
+  EpiParams ep{dw, lddw, nullptr, nullptr, 0, nullptr, 0, 1.f, accumulate ? 1.f : 0.f, 0, 0.f, nullptr, 0, 0, 0, nullptr, 0};
   // dw[N,K] = sum_m dy[m,n] x[m,k]: GEMM (N, K, M) with both operands MN-major.
   int rc = gemm_any(EPI_F32, dy, lddy, 1, x, ldx, 1, ep, N, K, M, dtype, stream);
   if (rc || !dbias) return rc;
@@ -364,7 +379,7 @@ int gpp_linear_wgrad_sgd(float* master, int64_t ldm, void* shadow, int64_t lds, 
   GPP_ARG_CHECK(master && grad && dy && x, "null pointer");
   GPP_ARG_CHECK(dtype == GPP_F32 || shadow, "bf16 path needs the shadow weights");
   EpiParams ep{master, ldm, nullptr, nullptr, 0, shadow, lds, 1.f, accumulate ? 1.f : 0.f, 0,
-               lr, grad, ldg, store_grad, 0};
+               lr, grad, ldg, store_grad, 0, nullptr, 0};
   return gemm_any(EPI_SGD, dy, lddy, 1, x, ldx, 1, ep, N, K, M, dtype, stream);
 }
 
@@ -372,7 +387,7 @@ int gpp_gemm(void* c, int64_t ldc, const void* a, int64_t lda, int a_mn, const v
              int64_t ldb, int b_mn, int64_t M, int64_t N, int64_t K, float alpha, float beta,
              int out_f32, int dtype, void* stream) {
   GPP_ARG_CHECK(c && a && b, "null pointer");
-  EpiParams ep{c, ldc, nullptr, nullptr, 0, nullptr, 0, alpha, beta, 0, 0.f, nullptr, 0, 0, 0};
+  EpiParams ep{c, ldc, nullptr, nullptr, 0, nullptr, 0, alpha, beta, 0, 0.f, nullptr, 0, 0, 0, nullptr, 0};
   const int epi = (dtype == GPP_F32 || out_f32) ? EPI_F32 : EPI_BF16;
   return gemm_any(epi, a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, dtype, stream);
 }

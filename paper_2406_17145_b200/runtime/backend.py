@@ -26,6 +26,9 @@ class CudaBackend:
     def current_stream(self):
         return torch.cuda.current_stream(self.device)
 
+    def prefetch_hint(self, t):
+        lib.prefetch_hint(t)
+
     # dense operator --------------------------------------------------------
     def linear_fwd(self, y, x, w, bias, act, residual=None, pre=None):
         lib.linear_fwd(y, x, w, bias=bias, act=act, residual=residual, pre=pre)

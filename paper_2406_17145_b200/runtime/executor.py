@@ -223,6 +223,9 @@ class Executor:
             self.recv_fw[j] = _order(self.recv_fw[j])
             self.send_fw[j] = _order(self.send_fw[j])
         self.first_bw = next(t.index for t in st.schedule if t.direction == "bw")
+        dense = [o for o in self.ops if self.wl.layers[o].kind == "dense"]
+        self._next_dense = {a: b for a, b in zip(dense, dense[1:])}
+        self._prev_dense = {b: a for a, b in zip(dense, dense[1:])}
         self.last_bw = [t.index for t in st.schedule if t.direction == "bw"][-1]
 
     def eff_act(self, u: int) -> str:
@@ -470,6 +473,7 @@ class Executor:
                     u = preds[0]
                     saved, act = self._saved_for(u, x, slot)
                     be.linear_dgrad(self._dx_target(u, slot), dz, self.W[(o, "w")], saved, act)
+
                 if self.d > 1 and j == self.last_bw:
                     # DP stage: this weight's gradient is final -> overlap its all-reduce
                     # with the rest of the backward pass (bucket = one layer's weight)

@@ -31,6 +31,7 @@ _SIGS = {
     "gpp_linear_dgrad": ([_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_linear_wgrad": ([_vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_linear_wgrad_sgd": ([_vp, _i64, _vp, _i64, _vp, _i64, _f32, _i32, _i32, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _vp], _i32),
+    "gpp_gemm_prefetch_hint": ([_vp, _i64], _i32),
     "gpp_gemm": ([_vp, _i64, _vp, _i64, _i32, _vp, _i64, _i32, _i64, _i64, _i64, _f32, _f32, _i32, _i32, _vp], _i32),
     "gpp_rowdot_fwd": ([_vp, _vp, _i64, _vp, _vp, _i64, _i64, _i32, _vp], _i32),
     "gpp_rowdot_bwd": ([_vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _i64, _i64, _i32, _i32, _vp], _i32),
@@ -279,3 +280,8 @@ def gemm_batched(c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, sp
     arr = (ctypes.c_int64 * 17)(*[int(v) for v in spec])
     call("gpp_gemm_batched", _ptr(c), ldc, _ptr(a), lda, a_rows, int(a_mn), _ptr(b), ldb, b_rows, int(b_mn),
          M, N, K, float(alpha), float(beta), int(bool(out_f32)), ctypes.cast(arr, ctypes.c_void_p), _stream(stream))
+
+
+def prefetch_hint(t):
+    """Next GEMM launched from this thread prefetches tensor ``t`` into L2."""
+    call("gpp_gemm_prefetch_hint", _ptr(t), 0 if t is None else t.numel() * t.element_size())
