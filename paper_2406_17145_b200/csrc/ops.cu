@@ -187,20 +187,116 @@ __global__ void colsum_final_kernel(float* out, const float* part, int splits, i
   out[c] = accumulate ? out[c] + t : t;
 }
 
-// Persistent per-device scratch for the partial sums (allocated on first use, outside
-// any graph capture: the first call happens in warm-up).
+// Single-launch column sums for aligned, unweighted inputs.  Block = 8 warps x 32 lanes,
+// each lane owning VEC adjacent columns (one 16-byte load per row), so a block covers
+// 32*VEC columns over one row split with 8 rows in flight per thread.  The block's
+// fixed-order partial goes to part[split][col]; the last block of a column range to
+// arrive (per-range arrival counter) sums the partials in split order and writes out,
+// then re-arms its counter -- deterministic, and graph-replay safe.
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_vec_kernel(float* out, float* part, unsigned* counters,
+                                                         const T* x, int64_t ldx, int64_t M,
+                                                         int64_t N, int64_t rows_per_split,
+                                                         int accumulate) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int CPB = 32 * VEC;
+  constexpr int UNROLL = 8;
+  __shared__ float red[8][CPB + 1];
+  __shared__ bool is_last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * CPB + lane * VEC;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_split;
+  const int64_t r1 = min(M, r0 + rows_per_split);
+  float acc[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
+  auto add = [&](const uint4& v) {
+    if constexpr (sizeof(T) == 2) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[2 * j] += __low2float(h[j]);
+        acc[2 * j + 1] += __high2float(h[j]);
+      }
+    } else {
+      const float* f = reinterpret_cast<const float*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] += f[j];
+    }
+  };
+  if (col < N) {
+    int64_t m = r0 + w;
+    for (; m + 8 * (UNROLL - 1) < r1; m += 8 * UNROLL) {
+      uint4 v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(reinterpret_cast<const uint4*>(x + (m + 8 * u) * ldx + col));
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) add(v[u]);
+    }
+    for (; m < r1; m += 8) add(__ldg(reinterpret_cast<const uint4*>(x + m * ldx + col)));
+  }
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) red[w][lane * VEC + j] = acc[j];
+  __syncthreads();
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * CPB + threadIdx.x;
+  if (threadIdx.x < CPB && c < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][threadIdx.x];
+    part[static_cast<int64_t>(blockIdx.y) * N + c] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(&counters[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (threadIdx.x < CPB && c < N) {
+    float t = 0.f;
+    for (unsigned s = 0; s < gridDim.y; ++s) t += __ldcg(part + static_cast<int64_t>(s) * N + c);
+    out[c] = accumulate ? out[c] + t : t;
+  }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0;
+}
+
+// Persistent per-device scratch for the partial sums and the arrival counters
+// (allocated on first use, outside any graph capture: the first call happens in warm-up).
 constexpr int64_t kScratchFloats = 4 << 20;
+constexpr int64_t kCounters = 1 << 16;
 float* colsum_scratch() {
   static float* bufs[64] = {nullptr};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!bufs[dev]) cudaMalloc(&bufs[dev], kScratchFloats * sizeof(float));
+  if (!bufs[dev]) {
+    if (cudaMalloc(&bufs[dev], kScratchFloats * sizeof(float) + kCounters * sizeof(unsigned)) != cudaSuccess) {
+      bufs[dev] = nullptr;
+      return nullptr;
+    }
+    cudaMemset(bufs[dev] + kScratchFloats, 0, kCounters * sizeof(unsigned));
+  }
   return bufs[dev];
 }
 
 template <typename T>
 int colsum_launch(float* out, const T* x, int64_t ldx, const float* wts, int64_t M, int64_t N,
                   int accumulate, cudaStream_t s) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int64_t vec_blocks = (N + 32 * VEC - 1) / (32 * VEC);
+  if (!wts && N % VEC == 0 && ldx % VEC == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      vec_blocks <= kCounters) {
+    // ~4 blocks per SM, >= 64 rows (8 per warp) per split
+    int64_t splits = (148 * 4 + vec_blocks - 1) / vec_blocks;
+    if (splits > (M + 63) / 64) splits = (M + 63) / 64;
+    if (splits < 1) splits = 1;
+    while (splits > 1 && splits * N > kScratchFloats) --splits;
+    float* part = colsum_scratch();
+    if (!part) { set_error("colsum scratch allocation failed"); return GPP_ERR_CUDA; }
+    const int64_t rps = (M + splits - 1) / splits;
+    colsum_vec_kernel<T><<<dim3(static_cast<unsigned>(vec_blocks), static_cast<unsigned>(splits)), 256, 0, s>>>(
+        out, part, reinterpret_cast<unsigned*>(part + kScratchFloats), x, ldx, M, N, rps, accumulate);
+    GPP_LAUNCH_CHECK();
+    return GPP_OK;
+  }
   const int64_t col_blocks = (N + 63) / 64;
   int splits = static_cast<int>((148 * 4 + col_blocks - 1) / col_blocks);
   splits = splits < 1 ? 1 : (splits > 64 ? 64 : splits);

@@ -182,6 +182,29 @@ def test_sgd_and_colsum(cuda_lib):
     assert _rel(out, x.sum(0)) < 1e-5
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("M,N,ld", [(1024, 4096, 4096), (1, 8, 8), (3000, 1000, 1000),
+                                    (513, 264, 272), (64, 65536, 65536), (100, 333, 333)])
+def test_colsum_paths(cuda_lib, dtype, M, N, ld):
+    """Vectorised single-launch path (aligned) and the generic two-pass path (ragged);
+    repeated calls must give bit-identical results (arrival counters re-armed)."""
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    x = torch.randn(M, ld, device="cuda", generator=g).to(dtype)[:, :N]
+    ref = x.float().sum(0, dtype=torch.float64).float()
+    out = torch.empty(N, device="cuda")
+    cuda_lib.colsum(out, x)
+    first = out.clone()
+    for _ in range(3):
+        cuda_lib.colsum(out, x)
+    assert torch.equal(out, first)
+    assert _rel(out, ref) < 1e-5
+    base = torch.randn(N, device="cuda", generator=g)
+    acc = base.clone()
+    cuda_lib.colsum(acc, x, accumulate=True)
+    torch.cuda.synchronize()
+    assert _rel(acc, base + ref) < 1e-5
+
+
 @pytest.mark.parametrize("M", [64, 1024])
 @pytest.mark.parametrize("accumulate", [False, True])
 def test_wgrad_sgd_fused(cuda_lib, M, accumulate):
