@@ -304,6 +304,71 @@ __device__ __forceinline__ void epilogue_f32_coalesced(const EpiParams& ep, cons
   __syncwarp();
 }
 
+// ---- fused-SGD fast path (beta == 0, no grad store, aligned rows, N % 4 == 0) ----
+// The master chunk does not depend on the accumulator, so it is copied global -> smem
+// with cp.async (no registers held) two chunks ahead -- for a tile's first two chunks
+// before the accumulator is even ready.  Lane = row then updates its row in place
+// (m -= lr * alpha * acc), and the warp writes master + bf16 shadow back coalesced.
+__device__ __forceinline__ bool sgd_fast_ok(const EpiParams& ep, int N) {
+  const uintptr_t mo = reinterpret_cast<uintptr_t>(ep.out), so = reinterpret_cast<uintptr_t>(ep.pre);
+  return ep.beta == 0.f && !ep.store_grad && (N & 3) == 0 && (mo & 15) == 0 && (ep.ldo & 3) == 0 &&
+         (so & 7) == 0 && (ep.ldpre & 3) == 0;
+}
+
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Issue the copy of a 32 x 32 fp32 master chunk (rows row0.., columns col0..) into buf.
+__device__ __forceinline__ void sgd_fast_issue(const EpiParams& ep, float* buf, int row0, int col0,
+                                               int M, int N, int lane) {
+  const int sub = lane >> 3, c4 = (lane & 7) * 4;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 4 * i + sub, grow = row0 + r;
+    if (grow < M && col0 + c4 < N)
+      cp_async16(buf + r * STAGE_LD + c4,
+                 reinterpret_cast<const float*>(ep.out) + static_cast<int64_t>(grow) * ep.ldo + col0 + c4);
+  }
+  cp_async_commit();
+}
+
+// buf holds the chunk's master (copy complete for this lane); update and write back.
+__device__ __forceinline__ void sgd_fast_update(const EpiParams& ep, const uint32_t (&v)[32], float* buf,
+                                                int row0, int col0, int M, int N, int lane) {
+  __syncwarp();  // every lane's cp.async data visible warp-wide
+  const float s = -ep.lr * ep.alpha;
+  float* mine = buf + lane * STAGE_LD;
+#pragma unroll
+  for (int j = 0; j < 32; j += 4) {
+    float4 m = *reinterpret_cast<float4*>(mine + j);
+    m.x = fmaf(s, __uint_as_float(v[j]), m.x);
+    m.y = fmaf(s, __uint_as_float(v[j + 1]), m.y);
+    m.z = fmaf(s, __uint_as_float(v[j + 2]), m.z);
+    m.w = fmaf(s, __uint_as_float(v[j + 3]), m.w);
+    *reinterpret_cast<float4*>(mine + j) = m;
+  }
+  __syncwarp();
+  const int sub = lane >> 3, c4 = (lane & 7) * 4, col = col0 + c4;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 4 * i + sub, grow = row0 + r;
+    if (grow >= M || col >= N) continue;
+    const float4 nm = *reinterpret_cast<const float4*>(buf + r * STAGE_LD + c4);
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.out) + static_cast<int64_t>(grow) * ep.ldo + col) = nm;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(nm.x, nm.y);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(nm.z, nm.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(static_cast<bf16*>(ep.pre) + static_cast<int64_t>(grow) * ep.ldpre + col) = pk;
+  }
+  __syncwarp();  // buf may be refilled next
+}
+
 // Prefetch the chunk's aux operand (residual for EPI_FWD, act'-saved for EPI_DGRAD).
 template <int EPI>
 __device__ __forceinline__ void epilogue_aux(const EpiParams& ep, int row, int col0, int M, int N,
@@ -492,7 +557,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;       // [2]
   uint64_t* tempty_bar = tfull_bar + 2;           // [2] (leader's copy is the live one)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);  // 4 warps x 32 x 36
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);  // per warp 32 x 36 (x2 SGD)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -608,13 +673,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       if (k_splits > 1) epu.out = reinterpret_cast<float*>(ep.out) + (u % k_splits) * ep.split_stride;
       const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
       const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
-      mbar_wait(&tfull_bar[acc], aph);
-      tc_fence_after();
       const int row0 = m_blk * 2 * BM + static_cast<int>(rank) * BM + q * 32;
       const int row = row0 + lane;
       const int group = (warp - 2) / 4;  // epilogue warpgroup: takes every other 32-col chunk
+      constexpr int GSTEP = PAIR_EPI_WARPS / 4;
+      constexpr int CH = BN / 32 / GSTEP;  // chunks per warp per tile (even)
+      if constexpr (EPI == EPI_SGD) {
+        if (sgd_fast_ok(epu, N) && k_splits == 1) {
+          float* b0 = epi_stage + (warp - 2) * 2 * 32 * STAGE_LD;
+          float* b1 = b0 + 32 * STAGE_LD;
+          auto col_of = [&](int p) { return n_blk * BN + (group + p * GSTEP) * 32; };
+          sgd_fast_issue(epu, b0, row0, col_of(0), M, N, lane);
+          sgd_fast_issue(epu, b1, row0, col_of(1), M, N, lane);
+          mbar_wait(&tfull_bar[acc], aph);
+          tc_fence_after();
+#pragma unroll
+          for (int p = 0; p < CH; ++p) {
+            float* buf = (p & 1) ? b1 : b0;
+            uint32_t v[32];
+            tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + (group + p * GSTEP) * 32, v);
+            if (p + 1 < CH) cp_async_wait<1>(); else cp_async_wait<0>();
+            sgd_fast_update(epu, v, buf, row0, col_of(p), M, N, lane);
+            if (p + 2 < CH) sgd_fast_issue(epu, buf, row0, col_of(p + 2), M, N, lane);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+          continue;
+        }
+      }
+      mbar_wait(&tfull_bar[acc], aph);
+      tc_fence_after();
 #pragma unroll 1
-      for (int c = group; c < BN / 32; c += PAIR_EPI_WARPS / 4) {
+      for (int c = group; c < BN / 32; c += GSTEP) {
         uint32_t v[32];
         if constexpr (EPI == EPI_F32 || EPI == EPI_SGD) {
           tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
@@ -802,7 +893,8 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   else rc = make_map(&mb, b, N, K, ldb, 64, BK);
   if (rc) return rc;
   constexpr int STAGE_BYTES = (BM + BN / 2) * BK * 2;
-  constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + PAIR_EPI_WARPS * 32 * STAGE_LD * 4;
+  // fused SGD double-buffers its per-warp master chunks
+  constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + PAIR_EPI_WARPS * 32 * STAGE_LD * 4 * (EPI == EPI_SGD ? 2 : 1);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI>,
@@ -930,8 +1022,10 @@ static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
   auto run = [&](auto epi_tag, const EpiParams& e, int ks) -> int {
     constexpr int E = decltype(epi_tag)::value;
     if (pair) {
-      if (bn == 256) return launch_tc_pair<256, 5, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
-      return launch_tc_pair<128, 7, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
+      // EPI_SGD gives one smem stage to its double-buffered master chunks
+      constexpr int S256 = E == EPI_SGD ? 4 : 5, S128 = E == EPI_SGD ? 6 : 7;
+      if (bn == 256) return launch_tc_pair<256, S256, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
+      return launch_tc_pair<128, S128, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
     }
     if (bn == 256) return launch_tc<256, 4, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
     return launch_tc<128, 6, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);

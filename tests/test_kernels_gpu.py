@@ -224,6 +224,23 @@ def test_wgrad_sgd_fused(cuda_lib, M, accumulate):
     assert torch.equal(shadow, master.bfloat16())
 
 
+@pytest.mark.parametrize("N,K,M", [(4096, 4096, 1024), (1000, 520, 300), (264, 4104, 64), (1024, 28672, 1024)])
+def test_wgrad_sgd_fast_path(cuda_lib, N, K, M):
+    """Production fused update (no grad store, beta = 0): cp.async-staged master chunks."""
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    dy = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    master = torch.randn(N, K, device="cuda", generator=g)
+    shadow = torch.empty(N, K, device="cuda", dtype=torch.bfloat16)
+    grad = torch.zeros(N, K, device="cuda")  # not touched (store_grad off)
+    master0 = master.clone()
+    cuda_lib.linear_wgrad_sgd(master, shadow, grad, dy, x, 0.01)
+    torch.cuda.synchronize()
+    gref = dy.float().t() @ x.float()
+    assert torch.allclose(master, master0 - 0.01 * gref, rtol=1e-5, atol=2e-5)
+    assert torch.equal(shadow, master.bfloat16())
+
+
 def test_embbag_and_interaction_kernels(cuda_lib):
     g = torch.Generator(device="cuda").manual_seed(21)
     rows, M, bag, F = 5000, 300, 100, 27
