@@ -178,28 +178,43 @@ def chain(n: int, costs: list[float] | None = None) -> ComputationGraph:
     return ComputationGraph(ops, [(i, i + 1) for i in range(n - 1)])
 
 
+CASE_STUDY_B = 64  # mini-batch of the §7.5 case study preset
+
+
 def case_study(blocks: int = 4, branches: int = 2) -> ComputationGraph:
     """§7.5: branches x [attention + 2 linear] blocks, merged by a concat.
 
-    One block = one operator (layer granularity).  Table costs
-    make b=4 twice as efficient per sample as b=1 and ~10% better than b=2,
-    and activations are large so the memory cap decides b.
+    One block = one operator (layer granularity); op ids are branch-major.
+    The concat is zero-cost and has no weights, so it is folded into the last block of each
+    branch (the branch outputs are the model outputs): GPP can then place it with a block
+    as in Fig. 6 instead of spending a device on it.  The documented
+    synthetic profile:
+
+    * fw ms {1: 1.0, 2: 1.2, 4: 2.0, 8: 3.8}, bw = 2 x fw: per-sample cost falls 1.8 -> 1.5 ms
+      from b = 2 to b = 4 (the compute-efficiency gain source, PAPER.md:931-934);
+    * 1 GB of weights per block: a data-parallel replica pays a ~10 ms all-reduce per
+      micro-batch, and two blocks never fit one device under ``case_study_cluster``;
+    * 100 MB of activations per sample: with the 4 GB cap the first stage of a depth-D
+      1F1B pipeline fits D*b <= 16 samples -> b = 4 at depth 4 (GPP), b = 2 at depth 8 (SPP).
     """
+    f = CostCurve.table({1: 1.0, 2: 1.2, 4: 2.0, 8: 3.8})
+    bw = CostCurve.table({1: 2.0, 2: 2.4, 4: 4.0, 8: 7.6})
     ops, edges = [], []
     oid = 0
-    ends = []
-    curve_f = CostCurve.table({1: 1.0, 2: 1.2, 4: 2.2, 8: 4.4})
-    curve_b = CostCurve.table({1: 2.0, 2: 2.4, 4: 4.4, 8: 8.8})
     for br in range(branches):
         prev = None
         for k in range(blocks):
-            ops.append(Operator(oid, f"b{br}_blk{k}", 1e6, 1e6, 1e6, curve_f, curve_b))
+            ops.append(Operator(oid, f"b{br}_blk{k}", 1e9, 1e8, 1e3, f, bw))
             if prev is not None:
                 edges.append((prev, oid))
             prev = oid
             oid += 1
-        ends.append(prev)
     return ComputationGraph(ops, edges)
+
+
+def case_study_cluster(n: int = 8) -> DeviceCluster:
+    """The case study's memory-capped pool: 4 GB per device, 1e8 B/ms links."""
+    return DeviceCluster(num_devices=n, mem_per_device=4e9, intra_bw=1e8, inter_bw=1e8, link_latency=0.0)
 
 
 def dlrm(B: int = 512, tables: int = 26, rows: int = 1_000_000, bag: int = 100, hidden: int = 4096,

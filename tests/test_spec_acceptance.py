@@ -251,3 +251,59 @@ def test_optimize_vs_exhaustive_random_sp():
         n_tot += 1
         n_ok += opt.bottleneck_tps <= brute.tps + eps + 1e-12
     assert n_ok / n_tot >= 0.85, (n_ok, n_tot)
+
+
+# ---------------------------------------------------------------- case study (acceptance 6)
+def test_case_study_gpp_vs_spp():
+    """§7.5: identical partition (one block per stage on 8 devices),
+    GPP b=4 / depth 4 / warm-up 4 vs SPP b=2 / depth 8 / warm-up 8, simulated iteration
+    ratio in 0.78-0.88 with both gain sources (warm-up, compute efficiency) >= 5%."""
+    g, cl, B = W.case_study(), W.case_study_cluster(), W.CASE_STUDY_B
+    gpp, spp = P.optimize(g, cl, B), P.spp_optimize(g, cl, B)
+    part = lambda st: sorted(sorted(s.op_ids) for s in st.stage_graph.stages)
+    assert part(gpp) == part(spp) == [[i] for i in range(8)]
+    assert {s.micro_batch for s in gpp.stage_graph.stages} == {4}
+    assert {s.micro_batch for s in spp.stage_graph.stages} == {2}
+    rg, rs = SIM.simulate(gpp.stage_graph, cl, g), SIM.simulate(spp.stage_graph, cl, g)
+    assert (rg.depth, rs.depth) == (4, 8)
+    assert (rg.warm_up_microbatches, rs.warm_up_microbatches) == (4, 8)
+    ratio = rg.iteration_ms / rs.iteration_ms
+    assert 0.78 <= ratio <= 0.88
+    # decomposition: "Parallel" = GPP's pipelines at SPP's micro-batch size (PAPER.md:860)
+    par = S.schedule_stage_graph(M.StageGraph(
+        [M.Stage(s.id, s.op_ids, 2, s.devices) for s in gpp.stage_graph.stages],
+        gpp.stage_graph.edges, B))
+    rp = SIM.simulate(par, cl, g)
+    assert rs.iteration_ms / rp.iteration_ms >= 1.05  # warm-up gain
+    assert rp.iteration_ms / rg.iteration_ms >= 1.05  # compute-efficiency gain
+    for st in (gpp, spp):
+        assert M.validate_strategy(g, cl, st.stage_graph) == []
+        assert max(SIM.simulate(st.stage_graph, cl, g).peak_mem_bytes.values()) <= cl.mem_per_device
+
+
+# ---------------------------------------------------------------- branch scaling (acceptance 7)
+def test_branch_scaling_ratio_nondecreasing():
+    """candle-uno-style towers with 2/4/8 branches on as many devices: the GPP/SPP
+    simulated throughput ratio never decreases with the branch count (§7.3)."""
+    ratios = []
+    for n in (2, 4, 8):
+        wl = W.candle(B=1024, towers=n)
+        cl = W.b200_cluster(n)
+        o = P.PartitionOptions(micro_batches=(128,))
+        t = [SIM.simulate(fn(wl.graph, cl, 1024, o).stage_graph, cl, wl.graph).iteration_ms
+             for fn in (P.optimize, P.spp_optimize)]
+        ratios.append(t[1] / t[0])
+    assert all(b >= a for a, b in zip(ratios, ratios[1:])), ratios
+
+
+# ---------------------------------------------------------------- search cost (acceptance 8)
+def test_search_states_grow_about_linearly_in_branches():
+    """DP states reported by the optimizer, fixed 8 devices and b, 4-layer towers: doubling
+    the branch count at most ~doubles the states (measured x2.3 / x2.2)."""
+    states = {}
+    for n in (4, 8, 16):
+        wl = W.candle(B=1024, towers=n)
+        st = P.optimize(wl.graph, W.b200_cluster(8), 1024, P.PartitionOptions(micro_batches=(128,)))
+        assert st.probes > 0
+        states[n] = st.dp_states
+    assert states[8] / states[4] <= 2.5 and states[16] / states[8] <= 2.5, states
