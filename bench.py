@@ -153,6 +153,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="candle", choices=["candle", "toy", "dlrm", "mmt"])
     ap.add_argument("--mode", default="gpp", choices=["gpp", "spp"])
+    ap.add_argument("--costs", default="measured", choices=["measured", "analytic"],
+                    help="partitioner cost curves: frozen B200 tables (profiles/) or analytic FLOP curves")
     ap.add_argument("--per-gpu-batch", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
@@ -177,11 +179,11 @@ def main():
     from paper_2406_17145_b200.runtime.executor import Executor
     from paper_2406_17145_b200.runtime.profiler import TimedBackend
     from paper_2406_17145_b200.sim import simulate
-    from paper_2406_17145_b200.workloads import b200_cluster
+    from paper_2406_17145_b200.workloads import b200_cluster, with_measured_curves
 
     wl = _workload(args.workload, world, args.per_gpu_batch)
     t_plan = time.perf_counter()
-    strategy = plan(wl, world, args.mode)
+    strategy = plan(wl, world, args.mode, costs=args.costs)
     t_plan = time.perf_counter() - t_plan
     sg = strategy.stage_graph
     dev = torch.device("cuda", local)
@@ -303,7 +305,8 @@ def main():
 
     # ---------------- simulated twin + bubble estimate ----------------
     cluster = b200_cluster(world)
-    sim = simulate(sg, cluster, wl.graph)
+    sim_graph = with_measured_curves(wl)[0].graph if args.costs == "measured" else wl.graph
+    sim = simulate(sg, cluster, sim_graph, sync_epilogue=True)
 
     if rank == 0:
         cpu = None
@@ -329,12 +332,12 @@ def main():
                             "inflight": s.sched_cfg.inflight_samples} for s in sg.stages],
                 "l2": "per-step working set (weights+master+grads ~2.9 GB) >> 126 MB L2",
                 "optimizer": "SGD fp32 master + bf16 shadow (fused into last wgrad epilogue when DP=1)",
-                "plan_s": round(t_plan, 3), "cuda_graph": graphed is not None,
+                "plan_s": round(t_plan, 3), "cuda_graph": graphed is not None, "costs": args.costs,
             },
             "e2e": {"value": round(e2e, 3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d_bytes),
                     "d2h_bytes_per_step": 4},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05 bf16 GEMM, all dense fw/dgrad/wgrad)",
+            "roofline": {"bound": "tensor", "kernel": "gemm_tc_pair_kernel (tcgen05 cta_group::2 bf16 GEMM, all dense fw/dgrad/wgrad+SGD)",
                          "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
                          "peak_source": f"{peak_src} bf16_tflops_sustained",

@@ -82,6 +82,11 @@ class PartitionOptions:
     # SPEC cost model charges the DP all-reduce once per MICRO-batch (cost.py:68-70).  The
     # B200 executor all-reduces once per ITERATION; True prices that.
     sync_per_iteration: bool = False
+    # B200 extension (off for the SPEC tests): a parallel bundle's join and the series
+    # segment after it may share a stage with one branch group -- Fig. 6's "one stage
+    # necessarily contains the concatenation operator", which the
+    # SP-aligned DP alone cannot express (it would spend a device on the join).
+    merge_join: bool = False
 
 
 @dataclass
@@ -142,6 +147,13 @@ class _Frag:
 
 
 _EMPTY = _Frag(None, (), 0.0)
+
+
+@dataclass(frozen=True)
+class _OpSet:
+    """A stage candidate that is not an SP subtree (merge-join stages)."""
+
+    ops: frozenset
 
 
 class _DP:
@@ -291,7 +303,59 @@ class _DP:
                 tps_all = [self.tps(seg.ops, c_f[0], d1) for d1 in range(1, d)]
                 if all(t is not None and t > self.t_max for t in tps_all):
                     break
+        if self.opts.merge_join and isinstance(units[start], SPParallel) and d >= 2:
+            best = self._consider(best, self._merge_join(units, start, c_f, c_b, d, rest_virtual_from))
         self.memo[key] = best
+        return best
+
+    def _merge_join(self, units, start, c_f, c_b, d, rest_virtual_from):
+        """Parallel unit P followed by a segment T: one branch group g of P and T form one
+        stage M on d_m devices; the other branches o (d_o devices) feed M; the chain after T
+        gets the remaining devices.  M is solved first (its successor is the rest of the
+        chain), then o with M as its successor; the join takes the larger in-flight count."""
+        par = units[start]
+        n = len(units)
+        best = None
+        # wide bundles (DLRM's 27 branches): every merged-stage successor config would
+        # re-solve all sub-bundles, so the extension is limited to <= 8 branches
+        if len(flatten_parallel(par)) > self.opts.max_exhaustive_branches + 2:
+            return None
+        for q in range(start + 2, n + 1):
+            tail = units[start + 1:q]
+            if all(self.is_virtual(u) for u in tail):
+                continue
+            t_ops = frozenset().union(*(u.ops for u in tail))
+            rest_virtual = rest_virtual_from[q]
+            for n1, n2 in self._par_splits(par):
+                for g, o in ((n1, n2), (n2, n1)):
+                    if self.is_virtual(g) or self.is_virtual(o):
+                        continue
+                    m = _OpSet(g.ops | t_ops)
+                    for d_m in range(1, d):
+                        for d_o in range(1, d - d_m + 1):
+                            d_r = d - d_m - d_o
+                            if rest_virtual:
+                                if d_r:
+                                    continue
+                                succs = [(c_b, None)]
+                            else:
+                                if d_r < 1:
+                                    continue
+                                succs = []
+                                for c_m in self.boundary_configs(c_f):
+                                    r2 = self._chain(units, q, c_m, c_b, d_r)
+                                    if r2 is not None and r2.i_f is not None:
+                                        succs.append(((r2.i_f, c_m[0], c_m[1]), r2))
+                            for succ, r2 in succs:
+                                rm = self._base(m, c_f, succ, d_m)
+                                if rm is None:
+                                    continue
+                                ro = self.solve(o, c_f, (rm.i_f, c_f[0], c_f[1]), d_o)
+                                if ro is None or ro.i_f is None:
+                                    continue
+                                stages = rm.stages + ro.stages + (r2.stages if r2 is not None else ())
+                                mem = max([rm.mem, ro.mem] + ([r2.mem] if r2 is not None else []))
+                                best = self._consider(best, _Frag(max(rm.i_f, ro.i_f), stages, mem))
         return best
 
     def _segment(self, seg, c_f, c_b, d):
@@ -333,6 +397,24 @@ class _DP:
                 ifs = [x.i_f for x in (r1, r2) if x.i_f is not None]
                 best = self._consider(best, _Frag(max(ifs) if ifs else None, r1.stages + r2.stages, max(r1.mem, r2.mem)))
         return best
+
+
+def merge_join_applicable(g: ComputationGraph, opts: PartitionOptions | None = None) -> bool:
+    """Whether PartitionOptions.merge_join can change the search on ``g``: some parallel
+    bundle of <= max_exhaustive_branches + 2 branches exists."""
+    limit = (opts or PartitionOptions()).max_exhaustive_branches + 2
+    _, tree = _tree_and_graph(g)
+    stack = [tree]
+    while stack:
+        n = stack.pop()
+        if isinstance(n, SPParallel):
+            kids = flatten_parallel(n)
+            if len(kids) <= limit:
+                return True
+            stack.extend(kids)
+        elif isinstance(n, SPSeries):
+            stack.extend((n.left, n.right))
+    return False
 
 
 def _tree_and_graph(g: ComputationGraph):

@@ -32,7 +32,7 @@ def dist_env() -> tuple[int, int, int]:
 
 def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions | None = None,
          mem_bytes: float = 180e9, sweep: bool | None = None, min_microbatches: int = 1,
-         max_microbatches: int = 32) -> P.Strategy:
+         max_microbatches: int = 32, costs: str = "measured") -> P.Strategy:
     """Run the GPP (or SPP baseline) partitioner + scheduler for ``n_gpus`` B200s.
 
     The TPS objective (Eq. 1) is a steady-state measure: with launch overheads in the
@@ -44,7 +44,10 @@ def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions 
     which does see warm-up / cool-down bubbles.  Single-GPU plans skip the sweep.
     """
     from ..sim import simulate
+    from ..workloads import with_measured_curves
 
+    if costs == "measured":  # frozen B200 tables where profiled (falls back to analytic curves)
+        wl = with_measured_curves(wl)[0]
     cluster = b200_cluster(n_gpus, mem_bytes)
     fn = P.optimize if mode == "gpp" else P.spp_optimize
     opts = opts or P.PartitionOptions(sync_per_iteration=True)
@@ -55,17 +58,21 @@ def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions 
     else:
         B = wl.mini_batch
         best, best_t = None, None
+        # GPP also tries join-merging stages (PartitionOptions.merge_join); SPP stays the
+        # paper's sequential baseline
+        merges = (False, True) if mode == "gpp" and P.merge_join_applicable(wl.graph, opts) else (False,)
         for b, _ in P.candidate_configs(B):
             if not (min_microbatches <= B // b <= max_microbatches):
                 continue
-            o = P.PartitionOptions(**{**opts.__dict__, "micro_batches": (b,)})
-            try:
-                cand = fn(wl.graph, cluster, B, o)
-            except P.NoFeasibleStrategy:
-                continue
-            t = simulate(cand.stage_graph, cluster, wl.graph, sync_epilogue=True).iteration_ms
-            if best_t is None or t < best_t:
-                best, best_t = cand, t
+            for mj in merges:
+                o = P.PartitionOptions(**{**opts.__dict__, "micro_batches": (b,), "merge_join": mj})
+                try:
+                    cand = fn(wl.graph, cluster, B, o)
+                except P.NoFeasibleStrategy:
+                    continue
+                t = simulate(cand.stage_graph, cluster, wl.graph, sync_epilogue=True).iteration_ms
+                if best_t is None or t < best_t:
+                    best, best_t = cand, t
         if best is None:
             st = fn(wl.graph, cluster, wl.mini_batch, opts)
         else:

@@ -52,6 +52,36 @@ class Piece:
     start: int           # global sample index of the first row (ordering key)
 
 
+class _OrderedSends:
+    """Posts a task's outgoing pieces as soon as their tensors are final, keeping each
+    peer's posting order equal to the list order the peer posts its receives in."""
+
+    def __init__(self, pieces, peer_of):
+        self.pieces = list(pieces)
+        self.posted = [False] * len(self.pieces)
+        self.ready: set[int] = set()
+        self.peer_of = peer_of
+
+    def mark(self, tensor: int, post) -> list:
+        self.ready.add(tensor)
+        return self.flush(post)
+
+    def flush(self, post, everything: bool = False) -> list:
+        works, blocked = [], set()
+        for i, pc in enumerate(self.pieces):
+            if self.posted[i]:
+                continue
+            peer = self.peer_of(pc)
+            if peer in blocked:
+                continue
+            if everything or pc.tensor in self.ready:
+                works.append(post(pc))
+                self.posted[i] = True
+            else:
+                blocked.add(peer)
+        return works
+
+
 def _rank_rows(st: Stage, rank: int) -> tuple[int, int]:
     devs = sorted(st.devices)
     q = devs.index(rank)
@@ -396,16 +426,22 @@ class Executor:
     # ---------------------------------------------------------------- tasks
     def _fw(self, j: int, batch):
         be, slot = self.be, j % self.ell
-        works = []
+        # receives are posted up front but waited for only by the first op consuming them,
+        # so ops fed locally (e.g. this stage's own towers) overlap the transfer
+        pending: dict[int, list] = {}
         for pc in self.recv_fw[j]:
             buf = self.recv[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows]
-            works.append(self.tp.irecv(buf, pc.producer))
-        for w in works:
-            w.wait()
+            pending.setdefault(pc.tensor, []).append(self.tp.irecv(buf, pc.producer))
         self._wait_sends(("fw", slot))
+        sends = _OrderedSends(self.send_fw[j], lambda pc: pc.consumer)
+        post = lambda pc: self.tp.isend(self.out[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows], pc.consumer)
+        works = []
         scale = 1.0 / self.B
         for o in self.ops:
             spec = self.layers[o]
+            for u in self.wl.graph.predecessors(o):
+                for w in pending.pop(u, ()):
+                    w.wait()
             if spec.kind == "dense":
                 x = self._input(o, j, slot, batch)
                 pre = self.pre[o][slot] if o in self.pre else None
@@ -444,26 +480,31 @@ class Executor:
                 be.linear_fwd(self.pred[o][slot], x, self.W[(o, "w")], self.P[(o, "b")], "none")
                 lab = batch[spec.label_key][j * self.m:(j + 1) * self.m]
                 be.ce_loss(self.loss_acc, self.dpred[o][slot], self.pred[o][slot], lab, scale)
-        sends = []
-        for pc in self.send_fw[j]:
-            buf = self.out[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows]
-            sends.append(self.tp.isend(buf, pc.consumer))
-        if sends:
-            self._send_works[("fw", slot)] = sends
+            works += sends.mark(o, post)  # o's output is final: ship its pieces now
+        for ws in pending.values():
+            for w in ws:
+                w.wait()
+        works += sends.flush(post, everything=True)
+        if works:
+            self._send_works[("fw", slot)] = works
 
     def _bw(self, j: int, batch, accumulate: bool):
         be, slot = self.be, j % self.ell
-        works = []
+        pending: dict[int, list] = {}
         for pc in self.send_fw[j]:  # grads come back along the forward pieces of task j
             buf = self.grecv[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows]
-            works.append(self.tp.irecv(buf, pc.consumer))
-        for w in works:
-            w.wait()
+            pending.setdefault(pc.tensor, []).append(self.tp.irecv(buf, pc.consumer))
         self._wait_sends(("bw", slot))
+        # input gradients go back along task j's forward pieces as soon as they are final
+        sends = _OrderedSends(self.recv_fw[j], lambda pc: pc.producer)
+        post = lambda pc: self.tp.isend(self.gsend[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows], pc.producer)
+        works = []
         g = self.wl.graph
         for o in reversed(self.ops):
             spec = self.layers[o]
             preds = g.predecessors(o)
+            for w in pending.pop(o, ()):
+                w.wait()
             needs_dx = spec.data_key is None and len(preds) == 1
             if spec.kind == "dense":
                 x = self._input(o, j, slot, batch)
@@ -527,12 +568,15 @@ class Executor:
                     u = preds[0]
                     saved, act = self._saved_for(u, x, slot)
                     be.linear_dgrad(self._dx_target(u, slot), dl, self.W[(o, "w")], saved, act)
-        sends = []
-        for pc in self.recv_fw[j]:  # our input gradients go back along task j's forward pieces
-            buf = self.gsend[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows]
-            sends.append(self.tp.isend(buf, pc.producer))
-        if sends:
-            self._send_works[("bw", slot)] = sends
+            for u in preds:
+                if u in self.gsend:
+                    works += sends.mark(u, post)
+        for ws in pending.values():
+            for w in ws:
+                w.wait()
+        works += sends.flush(post, everything=True)
+        if works:
+            self._send_works[("bw", slot)] = works
 
     # ------------------------------------------------------------ iteration
     def run_iteration(self, batch: dict[str, torch.Tensor], step_optimizer: bool = True):

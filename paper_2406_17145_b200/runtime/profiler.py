@@ -101,13 +101,24 @@ class TimedBackend(CudaBackend):
 
 
 def _time_us(fn, reps: int) -> float:
+    """Device time per call of ``fn``, replayed from a CUDA graph of ``reps`` calls: the
+    executor replays captured iterations, so host launch overhead is not a task cost."""
     for _ in range(2):
         fn()
     torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(reps):
+                fn()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for _ in range(reps):
-        fn()
+    g.replay()
     e.record()
     torch.cuda.synchronize()
     return s.elapsed_time(e) * 1e3 / reps

@@ -14,11 +14,13 @@ first) yields the branch-by-branch SPP order.
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+import json
+import os
+from dataclasses import dataclass, field, replace
 
 from .model import ComputationGraph, CostCurve, DeviceCluster, Operator
 
-__all__ = ["LayerSpec", "Workload", "b200_cluster", "PRESETS", "make"]
+__all__ = ["LayerSpec", "Workload", "b200_cluster", "PRESETS", "make", "with_measured_curves", "MEASURED_CURVES"]
 
 # B200 constants (MEASURED_PEAKS.json).
 BF16_TFLOPS_SUSTAINED = 1397.3
@@ -59,6 +61,49 @@ class Workload:
     bytes_per_sample: float = 0.0    # HBM-bound algorithmic bytes per sample (embeddings)
     notes: str = ""
     meta: dict = field(default_factory=dict)
+
+
+# Frozen B200 per-operator timings (tools/profile_costs.py on one B200, production
+# kernels): the partitioner's table CostCurves.
+MEASURED_CURVES = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                               "cost_curves_b200.json")
+
+
+def dense_profile_key(spec: "LayerSpec") -> str:
+    """Profile key of a dense op: source ops (reading batch data) run no dgrad."""
+    return f"dense:{spec.in_dim}x{spec.out_dim}:{spec.act}:{'nodgrad' if spec.data_key else 'dgrad'}"
+
+
+def with_measured_curves(wl: "Workload", profile: dict | str | None = None) -> tuple["Workload", int]:
+    """Replace the analytic fw/bw curves of bf16 dense operators by measured B200 tables.
+
+    ``profile`` is the JSON written by tools/profile_costs.py (default: the committed
+    ``profiles/cost_curves_b200.json``): ``curves[key] = {b: [...], fwd_ms: [...], bwd_ms:
+    [...]}`` with ms per task at b samples per device.  Operators without a profiled shape
+    keep their analytic curves.  Returns (workload, number of operators replaced).
+    """
+    if profile is None or isinstance(profile, str):
+        path = profile or MEASURED_CURVES
+        if not os.path.exists(path):
+            return wl, 0
+        with open(path) as f:
+            profile = json.load(f)
+    if wl.dtype != "bf16":
+        return wl, 0
+    curves = profile.get("curves", {})
+    ops, n = [], 0
+    for op in wl.graph.ops:
+        spec = wl.layers.get(op.id)
+        c = curves.get(dense_profile_key(spec)) if spec is not None and spec.kind == "dense" else None
+        if c:
+            op = replace(op, fwd_cost=CostCurve.table(dict(zip(c["b"], c["fwd_ms"]))),
+                         bwd_cost=CostCurve.table(dict(zip(c["b"], c["bwd_ms"]))))
+            n += 1
+        ops.append(op)
+    if not n:
+        return wl, 0
+    return replace(wl, graph=ComputationGraph(ops, wl.graph.edges),
+                   meta={**wl.meta, "costs": f"measured B200 tables for {n} ops"}), n
 
 
 def b200_cluster(n: int, mem_bytes: float = 180e9) -> DeviceCluster:

@@ -307,3 +307,33 @@ def test_search_states_grow_about_linearly_in_branches():
         assert st.probes > 0
         states[n] = st.dp_states
     assert states[8] / states[4] <= 2.5 and states[16] / states[8] <= 2.5, states
+
+
+# ---------------------------------------------------------------- merge-join extension
+def test_merge_join_places_join_with_a_branch():
+    """B200 extension (PartitionOptions.merge_join): on 2 devices the
+    2-tower CANDLE tail shares a stage with one tower instead of {towers} | {tail}."""
+    wl = W.candle(B=1024, towers=2)
+    cl = W.b200_cluster(2)
+    st = P.optimize(wl.graph, cl, 1024, P.PartitionOptions(merge_join=True, micro_batches=(256,)))
+    assert M.validate_strategy(wl.graph, cl, st.stage_graph) == []
+    parts = sorted(sorted(s.op_ids) for s in st.stage_graph.stages)
+    assert parts in ([[0, 1, 2, 3], [4, 5, 6, 7, 8, 9, 10]], [[0, 1, 2, 3, 8, 9, 10], [4, 5, 6, 7]])
+    base = P.optimize(wl.graph, cl, 1024, P.PartitionOptions(micro_batches=(256,)))
+    assert sorted(sorted(s.op_ids) for s in base.stage_graph.stages) == [list(range(8)), [8, 9, 10]]
+    assert st.bottleneck_tps < 0.8 * base.bottleneck_tps
+    SIM.simulate(st.stage_graph, cl, wl.graph)  # schedulable, deadlock-free
+
+
+def test_merge_join_outputs_valid_and_never_worse():
+    """merge_join only adds candidates: valid, deadlock-free, bottleneck TPS <= the plain DP."""
+    rng = random.Random(7)
+    for trial in range(60):
+        n = rng.randint(3, 7)
+        g = _rand_sp_graph(rng, n)
+        cl = M.DeviceCluster(rng.randint(2, 4), 1e12, 1e3, 1e9)
+        st = P.optimize(g, cl, 8, P.PartitionOptions(merge_join=True, epsilon_mode="spec"))
+        assert M.validate_strategy(g, cl, st.stage_graph) == []
+        SIM.simulate(st.stage_graph, cl, g)
+        plain = P.optimize(g, cl, 8, P.PartitionOptions(epsilon_mode="spec"))
+        assert st.bottleneck_tps <= plain.bottleneck_tps + 1e-3 * plain.maxtps + 1e-12
