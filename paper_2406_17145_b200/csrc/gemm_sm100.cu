@@ -17,6 +17,7 @@
 //                        bias / activation / residual / act'-mask -> global
 // Operand tiles are 128B-swizzled (TMA SWIZZLE_128B == UMMA SWIZZLE_128B).
 #include <cuda.h>
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <type_traits>
@@ -542,7 +543,7 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
                         const __grid_constant__ CUtensorMap tma_b, EpiParams ep, int M, int N,
-                        int K, int k_splits) {
+                        int K, int k_splits, int m_fast) {
   constexpr int A_BYTES = BM * BK * 2;            // 16 KB: this CTA's 128 rows of A
   constexpr int B_BYTES = (BN / 2) * BK * 2;      // this CTA's BN/2 rows of B
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -603,7 +604,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       for (int u = cluster_id; u < num_units; u += num_clusters) {
         const int tile = u / k_splits, kb0 = (u % k_splits) * kb_per;
         const int num_kb = min(kb_total, kb0 + kb_per) - kb0;
-        const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
+        // raster: concurrently running pairs share the larger operand's tiles through L2
+        const int m_blk = m_fast ? tile % m_tiles : tile / n_tiles;
+        const int n_blk = m_fast ? tile / m_tiles : tile % n_tiles;
         const int a_row = m_blk * 2 * BM + static_cast<int>(rank) * BM;
         const int b_row = n_blk * BN + static_cast<int>(rank) * (BN / 2);
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
@@ -672,7 +675,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       EpiParams epu = ep;
       if (k_splits > 1) epu.out = reinterpret_cast<float*>(ep.out) + (u % k_splits) * ep.split_stride;
       const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
-      const int m_blk = tile / n_tiles, n_blk = tile % n_tiles;
+      const int m_blk = m_fast ? tile % m_tiles : tile / n_tiles;
+      const int n_blk = m_fast ? tile / m_tiles : tile % n_tiles;
       const int row0 = m_blk * 2 * BM + static_cast<int>(rank) * BM + q * 32;
       const int row = row0 + lane;
       const int group = (warp - 2) / 4;  // epilogue warpgroup: takes every other 32-col chunk
@@ -906,7 +910,7 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   if (units < clusters) clusters = units;
   gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(2 * clusters),
                                                      PAIR_THREADS, SMEM, stream>>>(
-      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits);
+      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits, M < N ? 1 : 0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("gemm_tc_pair launch: ") + cudaGetErrorString(e));
@@ -1009,6 +1013,9 @@ static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
     // CTA-pair 256 x BN tiles; BN=128 when 256-wide tiles leave most pairs idle.
     const int64_t pairs256 = ((M + 255) / 256) * ((N + 255) / 256);
     bn = (N > 128 && pairs256 >= 48) ? 256 : 128;
+    // small output, long K: split-K fills the GPU anyway, and 256-wide tiles cut the
+    // L2 -> SM operand traffic per FLOP by a third (the CANDLE tail: 1024 x 1024 x 28672)
+    if (bn == 128 && N > 128 && pairs256 * std::min<int64_t>(max_splits_env(), num_kb / 2) >= 48) bn = 256;
     tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
     slots = num_sms() / 2;
   } else {

@@ -48,24 +48,26 @@ def main():
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--batch", type=int, default=1024)
-    ap.add_argument("--width", type=int, default=4096)
+    ap.add_argument("--width", type=int, default=4096, help="in features (and out unless --out-width)")
+    ap.add_argument("--out-width", type=int, default=None)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     B, W, L = args.batch, args.width, args.layers
-    master = [torch.randn(W, W, device=dev) / 64 for _ in range(L)]
+    O = args.out_width or W
+    master = [torch.randn(O, W, device=dev) / 64 for _ in range(L)]
     shadow = [m.bfloat16() for m in master]
-    grad = [torch.zeros(W, W, device=dev) for _ in range(L)]
-    dy = [torch.randn(B, W, device=dev).bfloat16() for _ in range(L)]
+    grad = [torch.zeros(O, W, device=dev) for _ in range(L)]
+    dy = [torch.randn(B, O, device=dev).bfloat16() for _ in range(L)]
     x = [torch.randn(B, W, device=dev).bfloat16() for _ in range(L)]
-    db = torch.zeros(W, device=dev)
-    r = {"shape": [W, W, B], "layers": L, "timing": "CUDA-graph replay"}
+    db = torch.zeros(O, device=dev)
+    r = {"shape": [O, W, B], "layers": L, "timing": "CUDA-graph replay"}
     r["wgrad_sgd_us"] = timeit(lambda i: lib.linear_wgrad_sgd(master[i], shadow[i], grad[i], dy[i], x[i], 1e-6), L, args.reps)
     r["wgrad_sgd_acc_us"] = timeit(
         lambda i: lib.linear_wgrad_sgd(master[i], shadow[i], grad[i], dy[i], x[i], 1e-6, accumulate=True), L, args.reps)
     r["wgrad_f32_us"] = timeit(lambda i: lib.linear_wgrad(grad[i], None, dy[i], x[i]), L, args.reps)
     r["colsum_us"] = timeit(lambda i: lib.colsum(db, dy[i]), L, args.reps)
-    flops = 2.0 * W * W * B
-    hbm = 2 * B * W * 2 + W * W * (4 + 4 + 2)
+    flops = 2.0 * O * W * B
+    hbm = B * (O + W) * 2 + O * W * (4 + 4 + 2)
     r["wgrad_sgd_tflops"] = round(flops / r["wgrad_sgd_us"] / 1e6, 1)
     r["wgrad_sgd_algo_GBs"] = round(hbm / r["wgrad_sgd_us"] / 1e3, 1)
     r["floor_us"] = {"tensor@1.5PF": round(flops / 1.5e9, 1), "hbm@7.0TB/s": round(hbm / 7.0e6, 1)}
