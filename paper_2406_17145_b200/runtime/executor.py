@@ -62,12 +62,13 @@ class _OrderedSends:
         self.ready: set[int] = set()
         self.peer_of = peer_of
 
-    def mark(self, tensor: int, post) -> list:
+    def mark(self, tensor: int) -> None:
         self.ready.add(tensor)
-        return self.flush(post)
 
-    def flush(self, post, everything: bool = False) -> list:
-        works, blocked = [], set()
+    def flush(self, post_many, everything: bool = False) -> list:
+        """Post every piece that is ready and not held back by an earlier piece to the same
+        peer, as ONE grouped transfer (``post_many(pieces) -> works``)."""
+        todo, blocked = [], set()
         for i, pc in enumerate(self.pieces):
             if self.posted[i]:
                 continue
@@ -75,11 +76,11 @@ class _OrderedSends:
             if peer in blocked:
                 continue
             if everything or pc.tensor in self.ready:
-                works.append(post(pc))
+                todo.append(pc)
                 self.posted[i] = True
             else:
                 blocked.add(peer)
-        return works
+        return post_many(todo) if todo else []
 
 
 def _rank_rows(st: Stage, rank: int) -> tuple[int, int]:
@@ -419,6 +420,12 @@ class Executor:
         return self.grecv[o][slot] if o in self.grecv else self.gbuf[o][slot]
 
     # ------------------------------------------------------------- transport
+    def _irecv_many(self, items):
+        return self.tp.irecv_many(items) if items else []
+
+    def _isend_many(self, items):
+        return self.tp.isend_many(items) if items else []
+
     def _wait_sends(self, key):
         for w in self._send_works.pop(key, []):
             w.wait()
@@ -429,12 +436,14 @@ class Executor:
         # receives are posted up front but waited for only by the first op consuming them,
         # so ops fed locally (e.g. this stage's own towers) overlap the transfer
         pending: dict[int, list] = {}
-        for pc in self.recv_fw[j]:
-            buf = self.recv[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows]
-            pending.setdefault(pc.tensor, []).append(self.tp.irecv(buf, pc.producer))
+        rws = self._irecv_many([(self.recv[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows], pc.producer)
+                                  for pc in self.recv_fw[j]])
+        for pc, w in zip(self.recv_fw[j], rws):
+            pending.setdefault(pc.tensor, []).append(w)
         self._wait_sends(("fw", slot))
         sends = _OrderedSends(self.send_fw[j], lambda pc: pc.consumer)
-        post = lambda pc: self.tp.isend(self.out[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows], pc.consumer)
+        post = lambda pcs: self._isend_many([(self.out[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows],
+                                                pc.consumer) for pc in pcs])
         works = []
         scale = 1.0 / self.B
         for o in self.ops:
@@ -480,7 +489,9 @@ class Executor:
                 be.linear_fwd(self.pred[o][slot], x, self.W[(o, "w")], self.P[(o, "b")], "none")
                 lab = batch[spec.label_key][j * self.m:(j + 1) * self.m]
                 be.ce_loss(self.loss_acc, self.dpred[o][slot], self.pred[o][slot], lab, scale)
-            works += sends.mark(o, post)  # o's output is final: ship its pieces now
+            sends.mark(o)  # o's output is final: ship its pieces now (cheap embedding bags
+            if spec.kind != "embbag":  # batch up into one grouped transfer)
+                works += sends.flush(post)
         for ws in pending.values():
             for w in ws:
                 w.wait()
@@ -491,13 +502,16 @@ class Executor:
     def _bw(self, j: int, batch, accumulate: bool):
         be, slot = self.be, j % self.ell
         pending: dict[int, list] = {}
-        for pc in self.send_fw[j]:  # grads come back along the forward pieces of task j
-            buf = self.grecv[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows]
-            pending.setdefault(pc.tensor, []).append(self.tp.irecv(buf, pc.consumer))
+        # grads come back along the forward pieces of task j
+        rws = self._irecv_many([(self.grecv[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows], pc.consumer)
+                                  for pc in self.send_fw[j]])
+        for pc, w in zip(self.send_fw[j], rws):
+            pending.setdefault(pc.tensor, []).append(w)
         self._wait_sends(("bw", slot))
         # input gradients go back along task j's forward pieces as soon as they are final
         sends = _OrderedSends(self.recv_fw[j], lambda pc: pc.producer)
-        post = lambda pc: self.tp.isend(self.gsend[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows], pc.producer)
+        post = lambda pcs: self._isend_many([(self.gsend[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows],
+                                                pc.producer) for pc in pcs])
         works = []
         g = self.wl.graph
         for o in reversed(self.ops):
@@ -568,9 +582,13 @@ class Executor:
                     u = preds[0]
                     saved, act = self._saved_for(u, x, slot)
                     be.linear_dgrad(self._dx_target(u, slot), dl, self.W[(o, "w")], saved, act)
+            marked = False
             for u in preds:
                 if u in self.gsend:
-                    works += sends.mark(u, post)
+                    sends.mark(u)
+                    marked = True
+            if marked:
+                works += sends.flush(post)
         for ws in pending.values():
             for w in ws:
                 w.wait()

@@ -48,6 +48,12 @@ class TorchTransport:
     def isend(self, buf, dst):
         return dist.isend(buf, dst=dst, group=self.p2p[(self.rank, dst)])
 
+    def irecv_many(self, items):
+        return [self.irecv(b, src) for b, src in items]
+
+    def isend_many(self, items):
+        return [self.isend(b, dst) for b, dst in items]
+
     def allreduce(self, t):
         dist.all_reduce(t, group=self.dp)
 
@@ -135,6 +141,34 @@ class NcclTransport:
         done = torch.cuda.Event()
         done.record(s)
         return _Done(done)
+
+    def _many(self, items, send: bool):
+        """Several transfers in ONE NCCL group: one fork per pair stream, one kernel per
+        communicator -- DLRM ships 26 embedding pieces per task to the same peer."""
+        if len(items) == 1:
+            b, peer = items[0]
+            return [self.isend(b, peer) if send else self.irecv(b, peer)]
+        keys = [((self.rank, peer) if send else (peer, self.rank)) for _, peer in items]
+        streams = {k: self._fork(k) for k in dict.fromkeys(keys)}
+        fn = "gpp_send" if send else "gpp_recv"
+        self._lib.call("gpp_group_start")
+        try:
+            for (b, peer), k in zip(items, keys):
+                self._lib.call(fn, self.comms[k], b.data_ptr(), b.numel() * b.element_size(),
+                               self._peer(*k, peer), streams[k].cuda_stream)
+        finally:
+            self._lib.call("gpp_group_end")
+        done = {}
+        for k, st in streams.items():
+            done[k] = torch.cuda.Event()
+            done[k].record(st)
+        return [_Done(done[k]) for k in keys]
+
+    def irecv_many(self, items):
+        return self._many(items, send=False) if items else []
+
+    def isend_many(self, items):
+        return self._many(items, send=True) if items else []
 
     def allreduce(self, t):
         self._lib.call("gpp_allreduce_f32", self.dp_comm, t.data_ptr(), t.numel(),
