@@ -998,7 +998,11 @@ static int choose_splits(int64_t tiles, int64_t slots, int64_t num_kb) {
   int64_t s = slots / tiles;
   if (s > num_kb / 2) s = num_kb / 2;
   if (s > max_splits_env()) s = max_splits_env();
-  return s < 1 ? 1 : static_cast<int>(s);
+  if (s < 1) s = 1;
+  // every split must own >= 1 k-block: kernels split K as ceil(num_kb / s) blocks each, so
+  // e.g. 64 blocks over 9 splits would leave the 9th empty (an uncommitted accumulator)
+  const int64_t per = (num_kb + s - 1) / s;
+  return static_cast<int>((num_kb + per - 1) / per);
 }
 
 template <bool A_MN, bool B_MN, int EPI>
@@ -1091,6 +1095,14 @@ static int batched_bn(const void* a, int64_t lda, int64_t a_rows, const void* b,
                       int64_t K, cudaStream_t stream) {
   // full operand extents: K-major -> (inner = ld, outer = rows); MN-major -> (inner = ld, outer = rows)
   const int64_t ai = lda, ao = a_rows, bi = ldb, bo = b_rows;
+  if (K <= 2 * BK) {
+    // attention scores / dP (K = head dim): one or two k-blocks, so a deep ring buys
+    // nothing; 2 stages (97 KB smem, BN TMEM columns) let two CTAs share an SM and
+    // overlap one tile's fp32 epilogue with the next tile's loads and MMA
+    if (N > 128)
+      return launch_tc<256, 2, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, 1, stream, bs, ai, ao, bi, bo);
+    return launch_tc<128, 2, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, 1, stream, bs, ai, ao, bi, bo);
+  }
   if (N > 128)
     return launch_tc<256, 4, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, 1, stream, bs, ai, ao, bi, bo);
   return launch_tc<128, 6, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, 1, stream, bs, ai, ao, bi, bo);

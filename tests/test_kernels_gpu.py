@@ -10,7 +10,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 SHAPES = [(128, 256, 64), (256, 512, 128), (1000, 520, 200), (384, 128, 4096), (1024, 4096, 1024),
-          (16, 4096, 4096), (1024, 1024, 28672), (96, 136, 2000)]  # last 3: split-K paths
+          (16, 4096, 4096), (1024, 1024, 28672), (96, 136, 2000),  # split-K paths
+          (512, 1024, 4096), (256, 512, 3136)]  # split counts that do not divide the k-blocks
 
 
 def _rel(a, b):
@@ -327,14 +328,15 @@ def test_softmax_kernels(cuda_lib):
     assert _rel(ds, 0.125 * pf * (dp - (dp * pf).sum(1, keepdim=True))) < 1e-2
 
 
-def test_batched_attention_gemms_match_emulation(cuda_lib):
-    """The seven attention GEMM specs of runtime/mmt.py, GPU vs the torch emulation."""
+@pytest.mark.parametrize("m,S,d,H", [(3, 256, 256, 4), (4, 512, 1024, 16)])
+def test_batched_attention_gemms_match_emulation(cuda_lib, m, S, d, H):
+    """The seven attention GEMM specs of runtime/mmt.py, GPU vs the torch emulation
+    (the second shape is the MMT layer: many tiles, two CTAs per SM)."""
     import sys, os
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from oracle.torch_backend import TorchBackend
     from paper_2406_17145_b200.runtime.mmt import _spec
     g = torch.Generator(device="cuda").manual_seed(8)
-    m, S, d, H = 3, 256, 256, 4
     dh, T, Z = d // H, m * S, m * H
     qkv = torch.randn(T, 3 * d, device="cuda", generator=g).bfloat16()
     P = torch.softmax(torch.randn(Z * S, S, device="cuda", generator=g), 1).bfloat16()
