@@ -897,8 +897,10 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   else rc = make_map(&mb, b, N, K, ldb, 64, BK);
   if (rc) return rc;
   constexpr int STAGE_BYTES = (BM + BN / 2) * BK * 2;
-  // fused SGD double-buffers its per-warp master chunks
-  constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + PAIR_EPI_WARPS * 32 * STAGE_LD * 4 * (EPI == EPI_SGD ? 2 : 1);
+  // fp32 epilogues stage through smem (fused SGD double-buffers its master chunks);
+  // the bf16 epilogues write straight from registers and give that space to the ring
+  constexpr int EPI_BUFS = EPI == EPI_SGD ? 2 : (EPI == EPI_F32 ? 1 : 0);
+  constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + PAIR_EPI_WARPS * 32 * STAGE_LD * 4 * EPI_BUFS;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI>,
@@ -1034,7 +1036,8 @@ static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
     constexpr int E = decltype(epi_tag)::value;
     if (pair) {
       // EPI_SGD gives one smem stage to its double-buffered master chunks
-      constexpr int S256 = E == EPI_SGD ? 4 : 5, S128 = E == EPI_SGD ? 6 : 7;
+      constexpr int S256 = E == EPI_SGD ? 4 : (E == EPI_F32 ? 5 : 6);
+      constexpr int S128 = E == EPI_SGD ? 6 : (E == EPI_F32 ? 7 : 8);
       if (bn == 256) return launch_tc_pair<256, S256, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
       return launch_tc_pair<128, S128, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
     }

@@ -365,3 +365,35 @@ def test_batched_attention_gemms_match_emulation(cuda_lib, m, S, d, H):
                         out_f32=dt == torch.float32)
         torch.cuda.synchronize()
         assert _rel(c.cpu(), ref) < 1e-2, name
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 4096, 4096), (1024, 2560, 4096), (768, 4096, 1024)])
+@pytest.mark.parametrize("act", ["relu", "gelu"])
+def test_pair_epilogues_partial_wave(cuda_lib, M, N, K, act):
+    """Pair GEMMs whose tiles do not fill the 74 pairs (64 / 40 / 48 tiles): fw with bias /
+    act / pre-activation / residual and dgrad with the act' mask, twice in a row, against
+    fp32 torch."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(N, K, device="cuda", generator=g) / K**0.5).bfloat16()
+    b = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    fa = {"relu": torch.relu, "gelu": torch.nn.functional.gelu}[act]
+    z = x.float() @ w.float().t() + b
+    for _ in range(2):
+        y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        pre = torch.empty_like(y)
+        cuda_lib.linear_fwd(y, x, w, bias=b, act=act, residual=res, pre=pre)
+        torch.cuda.synchronize()
+        assert _rel(pre, z) < 1e-2
+        assert _rel(y, fa(z) + res.float()) < 2e-2
+    dy = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    saved = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    s = saved.float().clone().requires_grad_(True)
+    fa(s).backward(torch.ones_like(s))
+    ref = (dy.float() @ w.float()) * s.grad
+    for _ in range(2):
+        dx = torch.empty(M, K, device="cuda", dtype=torch.bfloat16)
+        cuda_lib.linear_dgrad(dx, dy, w, saved=saved, act=act)
+        torch.cuda.synchronize()
+        assert _rel(dx, ref) < 2e-2
