@@ -22,6 +22,8 @@
  *   gpp_sgd_step                fused optimizer over a stage's parameters
  *   gpp_layernorm_fwd / _bwd, gpp_softmax_fwd / _bwd, gpp_meanpool_fwd / _bwd,
  *   gpp_gemm_batched            MMT pre-LN transformer layer (attention as batched GEMMs)
+ *   gpp_attn_softmax / gpp_attn_softmax_bwd  attention scores with the softmax (or its
+ *                               backward) fused into the tcgen05 epilogue (S <= 512)
  *   gpp_embbag_fwd / gpp_embbag_sgd        DLRM embedding-bag and its sparse SGD scatter
  *   gpp_interaction_fwd / _bwd  DLRM dot interaction
  *   gpp_copy_rows               strided row-block copy (concat slices, DP re-shard,
@@ -175,6 +177,19 @@ int gpp_gemm_batched(void* c, int64_t ldc, const void* a, int64_t lda, int64_t a
                      const void* b, int64_t ldb, int64_t b_rows, int b_mn, int64_t M, int64_t N,
                      int64_t K, float alpha, float beta, int out_f32, const int64_t* spec,
                      void* stream);
+/* Fused attention softmax over the same batch spec (both operands K-major, keys N <= 512,
+ * N % 32 == 0, head dim K % 64 == 0, K <= 256):
+ *   gpp_attn_softmax:      p[z] = softmax_rows(scale * q[z] k[z]^T)            (bf16 out)
+ *   gpp_attn_softmax_bwd:  ds[z] = scale * p[z] o (g[z] - rowsum(p[z] o g[z])),
+ *                          g[z] = dout[z] v[z]^T                              (bf16 out)
+ * p / ds rows at c0 + hi*c_hi + lo*c_lo with leading dims ldp / ldc.  Replaces the scores
+ * GEMM + softmax (+ backward) pair of the MMT attention without the fp32 scores in HBM. */
+int gpp_attn_softmax(void* p, int64_t ldp, const void* q, int64_t ldq, int64_t q_rows, const void* k,
+                     int64_t ldk, int64_t k_rows, int64_t M, int64_t N, int64_t K, float scale,
+                     const int64_t* spec, void* stream);
+int gpp_attn_softmax_bwd(void* ds, int64_t ldc, const void* p, int64_t ldp, const void* dout, int64_t ldo,
+                         int64_t o_rows, const void* v, int64_t ldv, int64_t v_rows, int64_t M, int64_t N,
+                         int64_t K, float scale, const int64_t* spec, void* stream);
 
 /* ---- DLRM: embedding bags and the dot interaction ------------- */
 /* pooled[m, :D] = sum_b table[idx[m*ldi + b], :D]; fp32 table [rows, D], bf16 pooled, D = 64. */

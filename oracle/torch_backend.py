@@ -205,6 +205,41 @@ class TorchBackend:
     def meanpool_bwd(self, dx, dout, M, S, D):
         dx.copy_((dout.float()[:, None, :] / S).expand(M, S, D).reshape(M * S, D))
 
+    def attn_softmax(self, p, ldp, q, ldq, q_rows, k, ldk, k_rows, M, N, K, scale, spec):
+        """Emulates gpp_attn_softmax: scores GEMM (fp32) then row softmax, per batch."""
+        nb = spec[0]
+        sc = torch.zeros(nb * M * N, dtype=torch.float32)
+        self.gemm_batched(sc, N, q, ldq, q_rows, False, k, ldk, k_rows, False, M, N, K,
+                          tuple(spec[:14]) + (0, _hi_stride(spec, M, N), M * N), alpha=scale,
+                          out_f32=True)
+        self._scatter_rows(p, ldp, spec, M, N, torch.softmax(sc.reshape(nb * M, N), dim=1))
+
+    def attn_softmax_bwd(self, ds, ldc, p, ldp, dout, ldo, o_rows, v, ldv, v_rows, M, N, K, scale, spec):
+        """Emulates gpp_attn_softmax_bwd: dP = dout v^T (fp32), ds = scale p (dP - rowsum(p dP))."""
+        nb = spec[0]
+        dp = torch.zeros(nb * M * N, dtype=torch.float32)
+        self.gemm_batched(dp, N, dout, ldo, o_rows, False, v, ldv, v_rows, False, M, N, K,
+                          tuple(spec[:14]) + (0, _hi_stride(spec, M, N), M * N), out_f32=True)
+        dp = dp.reshape(nb * M, N)
+        pf = self._gather_rows(p, ldp, spec, M, N)
+        self._scatter_rows(ds, ldc, spec, M, N, scale * pf * (dp - (dp * pf).sum(1, keepdim=True)))
+
+    @staticmethod
+    def _row_index(ld, spec, M, N):
+        nb, nlo, c0, chi, clo = spec[0], spec[1], spec[14], spec[15], spec[16]
+        idx = []
+        for z in range(nb):
+            hi, lo = divmod(z, nlo)
+            off = c0 + hi * chi + lo * clo
+            idx.append(off + torch.arange(M)[:, None] * ld + torch.arange(N)[None, :])
+        return torch.cat(idx).reshape(-1)
+
+    def _scatter_rows(self, out, ld, spec, M, N, vals):
+        out.reshape(-1)[self._row_index(ld, spec, M, N)] = vals.reshape(-1).to(out.dtype)
+
+    def _gather_rows(self, t, ld, spec, M, N):
+        return t.reshape(-1)[self._row_index(ld, spec, M, N)].float().reshape(-1, N)
+
     def gemm_batched(self, c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, spec, alpha=1.0,
                      out_f32=False):
         (nb, nlo, am0, amh, aml, ak0, akh, akl, bn0, bnh, bnl, bk0, bkh, bkl, c0, chi, clo) = spec
@@ -221,3 +256,8 @@ class TorchBackend:
             off = c0 + hi * chi + lo * clo
             idx = off + torch.arange(M)[:, None] * ldc + torch.arange(N)[None, :]
             cf[idx.reshape(-1)] = Cz.reshape(-1).to(cf.dtype)
+
+
+def _hi_stride(spec, M, N):
+    """Contiguous per-batch [M, N] scratch: batch z = hi*nlo + lo sits at z*M*N."""
+    return spec[1] * M * N

@@ -48,6 +48,13 @@ struct BatchSpec {
 };
 
 // Batched bf16 GEMM (1-CTA tcgen05 kernel over batch x tiles).
+// Attention scores + fused softmax (bwd = 0: P = softmax(alpha Q K^T)) or fused softmax
+// backward (bwd = 1: dS = alpha P o (dO V^T - rowsum(P o dO V^T))); both operands K-major,
+// keys N <= 512.  P / out share the BatchSpec C offsets.
+int tc_attn_softmax(int bwd, void* out, int64_t ldc, const void* P, int64_t ldp, const void* a, int64_t lda,
+                    int64_t a_rows, const void* b, int64_t ldb, int64_t b_rows, const BatchSpec& bs, int64_t M,
+                    int64_t N, int64_t K, float alpha, cudaStream_t stream);
+
 int tc_gemm_batched(int epi, const void* a, int64_t lda, int64_t a_rows, int a_mn, const void* b,
                     int64_t ldb, int64_t b_rows, int b_mn, const EpiParams& ep, const BatchSpec& bs,
                     int64_t M, int64_t N, int64_t K, cudaStream_t stream);

@@ -1121,6 +1121,227 @@ static int batched_layout(const void* a, int64_t lda, int64_t a_rows, int a_mn, 
   return batched_bn<true, true, EPI>(a, lda, a_rows, b, ldb, b_rows, ep, bs, M, N, K, s);
 }
 
+
+// ------------------------------------------------------------------------
+// Attention scores with the softmax fused into the epilogue (MMT, S <= 512 keys).
+//
+// One CTA per (batch = sample x head, 128 query rows): the whole 128 x S score block
+// lives in TMEM (512 fp32 columns, two N=256 UMMAs per k-step), so the epilogue thread
+// that owns a query row sees every key of it and writes the probabilities directly:
+//   fw : P  = softmax(alpha * Q K^T)                 (3 TMEM passes: max, sum, write)
+//   bw : dS = alpha * P o (dP - rowsum(P o dP)),  dP = dO V^T   (2 passes, P from HBM)
+// The fp32 score / dP matrices never reach HBM (the unfused path wrote and re-read
+// 2 x Z S^2 x 4 bytes per layer and direction).
+// ------------------------------------------------------------------------
+constexpr int ATT_N = 512;
+constexpr int ATT_STAGES = 2;
+
+template <bool BWD>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    attn_softmax_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                        bf16* __restrict__ out, int64_t ldc, const bf16* __restrict__ P, int64_t ldp,
+                        float alpha, int M, int N, int K, BatchSpec bs) {
+  constexpr int A_BYTES = BM * BK * 2;
+  constexpr int B_HALF = 256 * BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + 2 * B_HALF;
+  constexpr uint32_t IDESC = idesc_bf16<256, false, false>();
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + ATT_STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + ATT_STAGES;
+  uint64_t* accum_bar = empty_bar + ATT_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m_blocks = (M + BM - 1) / BM;
+  const int z = static_cast<int>(blockIdx.x) / m_blocks;
+  const int m_blk = static_cast<int>(blockIdx.x) % m_blocks;
+  const int z_hi = z / bs.nlo, z_lo = z % bs.nlo;
+  const int am_off = bs.a_m0 + z_hi * bs.a_m_hi + z_lo * bs.a_m_lo;
+  const int ak_off = bs.a_k0 + z_hi * bs.a_k_hi + z_lo * bs.a_k_lo;
+  const int bn_off = bs.b_n0 + z_hi * bs.b_n_hi + z_lo * bs.b_n_lo;
+  const int bk_off = bs.b_k0 + z_hi * bs.b_k_hi + z_lo * bs.b_k_lo;
+  const int64_t c_off = bs.c0 + z_hi * bs.c_hi + z_lo * bs.c_lo;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+    for (int s = 0; s < ATT_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(accum_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(ATT_N)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % ATT_STAGES;
+        mbar_wait(&empty_bar[s], ((kb / ATT_STAGES) & 1) ^ 1);
+        uint8_t* a_dst = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+        tma_load_2d(a_dst, &tma_a, &full_bar[s], kb * BK + ak_off, m_blk * BM + am_off);
+        tma_load_2d(a_dst + A_BYTES, &tma_b, &full_bar[s], kb * BK + bk_off, bn_off);
+        tma_load_2d(a_dst + A_BYTES + B_HALF, &tma_b, &full_bar[s], kb * BK + bk_off, bn_off + 256);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % ATT_STAGES;
+        mbar_wait(&full_bar[s], (kb / ATT_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t adesc = sdesc_sw128(a_base + k * 32, 16, 1024);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint64_t bdesc = sdesc_sw128(a_base + A_BYTES + h * B_HALF + k * 32, 16, 1024);
+            umma_bf16(tmem_base + h * 256, adesc, bdesc, IDESC, (kb | k) != 0 ? 1u : 0u);
+          }
+        }
+        umma_commit(&empty_bar[s]);
+      }
+      umma_commit(accum_bar);
+    }
+  } else {
+    mbar_wait(accum_bar, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int row = m_blk * BM + q * 32 + lane;
+    const bool live = row < M;
+    const int nch = N / 32;
+    const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    bf16* orow = out + c_off + static_cast<int64_t>(live ? row : 0) * ldc;
+    if constexpr (!BWD) {
+      float mx = -INFINITY;
+      for (int c = 0; c < nch; ++c) {
+        uint32_t v[32];
+        tmem_ld32(trow + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
+      }
+      const float sl2 = alpha * 1.4426950408889634f;  // alpha * log2(e); alpha > 0
+      const float mb = mx * sl2;
+      float sum = 0.f;
+      for (int c = 0; c < nch; ++c) {
+        uint32_t v[32];
+        tmem_ld32(trow + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum += exp2f(fmaf(__uint_as_float(v[j]), sl2, -mb));
+      }
+      const float inv = 1.f / sum;
+      for (int c = 0; c < nch; ++c) {
+        uint32_t v[32];
+        tmem_ld32(trow + c * 32, v);
+        uint4 pk[4];
+        uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(exp2f(fmaf(__uint_as_float(v[j]), sl2, -mb)) * inv,
+                                                          exp2f(fmaf(__uint_as_float(v[j + 1]), sl2, -mb)) * inv);
+          w[j / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        if (live) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) reinterpret_cast<uint4*>(orow + c * 32)[i] = pk[i];
+        }
+      }
+    } else {
+      const bf16* prow = P + c_off + static_cast<int64_t>(live ? row : 0) * ldp;
+      auto load_p = [&](int c, float (&pf)[32]) {
+        uint4 r[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r[i] = __ldg(reinterpret_cast<const uint4*>(prow + c * 32) + i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r[i]);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            pf[i * 8 + 2 * t] = __low2float(h[t]);
+            pf[i * 8 + 2 * t + 1] = __high2float(h[t]);
+          }
+        }
+      };
+      float D = 0.f;
+      for (int c = 0; c < nch; ++c) {
+        uint32_t v[32];
+        float pf[32];
+        load_p(c, pf);
+        tmem_ld32(trow + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) D = fmaf(pf[j], __uint_as_float(v[j]), D);
+      }
+      for (int c = 0; c < nch; ++c) {
+        uint32_t v[32];
+        float pf[32];
+        load_p(c, pf);
+        tmem_ld32(trow + c * 32, v);
+        uint4 pk[4];
+        uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(alpha * pf[j] * (__uint_as_float(v[j]) - D),
+                                                          alpha * pf[j + 1] * (__uint_as_float(v[j + 1]) - D));
+          w[j / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        if (live) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) reinterpret_cast<uint4*>(orow + c * 32)[i] = pk[i];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ATT_N) : "memory");
+  }
+}
+
+template <bool BWD>
+static int launch_attn_softmax(bf16* out, int64_t ldc, const bf16* P, int64_t ldp, const void* a, int64_t lda,
+                               int64_t a_rows, const void* b, int64_t ldb, int64_t b_rows, const BatchSpec& bs,
+                               int64_t M, int64_t N, int64_t K, float alpha, cudaStream_t stream) {
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, a, lda, a_rows, lda, BK, BM);
+  if (rc) return rc;
+  rc = make_map(&mb, b, ldb, b_rows, ldb, BK, 256);
+  if (rc) return rc;
+  constexpr int SMEM = ATT_STAGES * (BM * BK * 2 + 2 * 256 * BK * 2) + 1024 + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_softmax_kernel<BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr_set = true;
+  }
+  const int64_t grid = static_cast<int64_t>(bs.nbatch) * ((M + BM - 1) / BM);
+  attn_softmax_kernel<BWD><<<static_cast<unsigned>(grid), NUM_THREADS, SMEM, stream>>>(
+      ma, mb, out, ldc, P, ldp, alpha, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), bs);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("attn_softmax launch: ") + cudaGetErrorString(e));
+    return GPP_ERR_CUDA;
+  }
+  count_launch();
+  return GPP_OK;
+}
+
 }  // namespace tc
 
 int tc_gemm_batched(int epi, const void* a, int64_t lda, int64_t a_rows, int a_mn, const void* b,
@@ -1156,6 +1377,26 @@ int tc_gemm(int epi, const void* a, int64_t lda, int a_mn, const void* b, int64_
     default:
       return tc::dispatch_layout<EPI_BF16>(a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, stream);
   }
+}
+
+int tc_attn_softmax(int bwd, void* out, int64_t ldc, const void* P, int64_t ldp, const void* a, int64_t lda,
+                    int64_t a_rows, const void* b, int64_t ldb, int64_t b_rows, const BatchSpec& bs, int64_t M,
+                    int64_t N, int64_t K, float alpha, cudaStream_t stream) {
+  GPP_ARG_CHECK(M > 0 && N > 0 && K > 0 && bs.nbatch >= 1 && bs.nlo >= 1, "bad shape");
+  GPP_ARG_CHECK(N <= tc::ATT_N && N % 32 == 0, "fused attention softmax needs 32 | keys <= 512");
+  GPP_ARG_CHECK(K % tc::BK == 0 && K <= 4 * tc::BK, "head dim must be a multiple of 64, <= 256 (no k-tile may straddle heads)");
+  GPP_ARG_CHECK(alpha > 0.f, "softmax scale must be positive");
+  GPP_ARG_CHECK((reinterpret_cast<uintptr_t>(a) & 15) == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0 &&
+                    lda % 8 == 0 && ldb % 8 == 0, "TMA alignment");
+  GPP_ARG_CHECK((reinterpret_cast<uintptr_t>(out) & 15) == 0 && ldc % 8 == 0 && bs.c0 % 8 == 0 &&
+                    bs.c_hi % 8 == 0 && bs.c_lo % 8 == 0, "16-byte aligned output rows");
+  if (bwd) {
+    GPP_ARG_CHECK(P && (reinterpret_cast<uintptr_t>(P) & 15) == 0 && ldp % 8 == 0, "16-byte aligned P rows");
+    return tc::launch_attn_softmax<true>(static_cast<bf16*>(out), ldc, static_cast<const bf16*>(P), ldp, a, lda,
+                                         a_rows, b, ldb, b_rows, bs, M, N, K, alpha, stream);
+  }
+  return tc::launch_attn_softmax<false>(static_cast<bf16*>(out), ldc, nullptr, 0, a, lda, a_rows, b, ldb, b_rows,
+                                        bs, M, N, K, alpha, stream);
 }
 
 }  // namespace gpp

@@ -378,4 +378,32 @@ int gpp_gemm_batched(void* c, int64_t ldc, const void* a, int64_t lda, int64_t a
                          bs, M, N, K, static_cast<cudaStream_t>(stream));
 }
 
+static BatchSpec batch_spec(const int64_t* spec) {
+  BatchSpec bs;
+  bs.nbatch = static_cast<int>(spec[0]);
+  bs.nlo = static_cast<int>(spec[1]);
+  bs.a_m0 = static_cast<int>(spec[2]); bs.a_m_hi = static_cast<int>(spec[3]); bs.a_m_lo = static_cast<int>(spec[4]);
+  bs.a_k0 = static_cast<int>(spec[5]); bs.a_k_hi = static_cast<int>(spec[6]); bs.a_k_lo = static_cast<int>(spec[7]);
+  bs.b_n0 = static_cast<int>(spec[8]); bs.b_n_hi = static_cast<int>(spec[9]); bs.b_n_lo = static_cast<int>(spec[10]);
+  bs.b_k0 = static_cast<int>(spec[11]); bs.b_k_hi = static_cast<int>(spec[12]); bs.b_k_lo = static_cast<int>(spec[13]);
+  bs.c0 = spec[14]; bs.c_hi = spec[15]; bs.c_lo = spec[16];
+  return bs;
+}
+
+int gpp_attn_softmax(void* p, int64_t ldp, const void* q, int64_t ldq, int64_t q_rows, const void* k,
+                     int64_t ldk, int64_t k_rows, int64_t M, int64_t N, int64_t K, float scale,
+                     const int64_t* spec, void* stream) {
+  GPP_ARG_CHECK(p && q && k && spec, "null pointer");
+  return tc_attn_softmax(0, p, ldp, nullptr, 0, q, ldq, q_rows, k, ldk, k_rows, batch_spec(spec), M, N, K, scale,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int gpp_attn_softmax_bwd(void* ds, int64_t ldc, const void* p, int64_t ldp, const void* dout, int64_t ldo,
+                         int64_t o_rows, const void* v, int64_t ldv, int64_t v_rows, int64_t M, int64_t N,
+                         int64_t K, float scale, const int64_t* spec, void* stream) {
+  GPP_ARG_CHECK(ds && p && dout && v && spec, "null pointer");
+  return tc_attn_softmax(1, ds, ldc, p, ldp, dout, ldo, o_rows, v, ldv, v_rows, batch_spec(spec), M, N, K, scale,
+                         static_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

@@ -100,6 +100,12 @@ class CudaBackend:
     def meanpool_bwd(self, dx, dout, M, S, D):
         lib.meanpool_bwd(dx, dout, M, S, D)
 
+    def attn_softmax(self, p, ldp, q, ldq, q_rows, k, ldk, k_rows, M, N, K, scale, spec):
+        lib.attn_softmax(p, ldp, q, ldq, q_rows, k, ldk, k_rows, M, N, K, scale, spec)
+
+    def attn_softmax_bwd(self, ds, ldc, p, ldp, dout, ldo, o_rows, v, ldv, v_rows, M, N, K, scale, spec):
+        lib.attn_softmax_bwd(ds, ldc, p, ldp, dout, ldo, o_rows, v, ldv, v_rows, M, N, K, scale, spec)
+
     def gemm_batched(self, c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, spec, alpha=1.0,
                      out_f32=False):
         lib.gemm_batched(c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, spec, alpha=alpha,

@@ -59,6 +59,8 @@ _SIGS = {
     "gpp_meanpool_fwd": ([_vp, _i64, _vp, _i64, _i64, _i64, _vp], _i32),
     "gpp_meanpool_bwd": ([_vp, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
     "gpp_gemm_batched": ([_vp, _i64, _vp, _i64, _i64, _i32, _vp, _i64, _i64, _i32, _i64, _i64, _i64, _f32, _f32, _i32, _vp, _vp], _i32),
+    "gpp_attn_softmax": ([_vp, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp, _vp], _i32),
+    "gpp_attn_softmax_bwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp, _vp], _i32),
     "gpp_embbag_fwd": ([_vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp], _i32),
     "gpp_embbag_sgd": ([_vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_interaction_fwd": ([_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
@@ -280,6 +282,20 @@ def gemm_batched(c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, sp
     arr = (ctypes.c_int64 * 17)(*[int(v) for v in spec])
     call("gpp_gemm_batched", _ptr(c), ldc, _ptr(a), lda, a_rows, int(a_mn), _ptr(b), ldb, b_rows, int(b_mn),
          M, N, K, float(alpha), float(beta), int(bool(out_f32)), ctypes.cast(arr, ctypes.c_void_p), _stream(stream))
+
+
+def attn_softmax(p, ldp, q, ldq, q_rows, k, ldk, k_rows, M, N, K, scale, spec, stream=None):
+    """p[z] = softmax(scale * q[z] k[z]^T) per batch (fused tcgen05 epilogue, keys <= 512)."""
+    arr = (ctypes.c_int64 * 17)(*[int(v) for v in spec])
+    call("gpp_attn_softmax", _ptr(p), ldp, _ptr(q), ldq, q_rows, _ptr(k), ldk, k_rows, M, N, K, float(scale),
+         ctypes.cast(arr, ctypes.c_void_p), _stream(stream))
+
+
+def attn_softmax_bwd(ds, ldc, p, ldp, dout, ldo, o_rows, v, ldv, v_rows, M, N, K, scale, spec, stream=None):
+    """ds[z] = scale * p o (dout v^T - rowsum(p o dout v^T)) per batch (fused epilogue)."""
+    arr = (ctypes.c_int64 * 17)(*[int(x) for x in spec])
+    call("gpp_attn_softmax_bwd", _ptr(ds), ldc, _ptr(p), ldp, _ptr(dout), ldo, o_rows, _ptr(v), ldv, v_rows, M, N,
+         K, float(scale), ctypes.cast(arr, ctypes.c_void_p), _stream(stream))
 
 
 def prefetch_hint(t):

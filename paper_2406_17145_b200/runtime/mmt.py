@@ -7,9 +7,10 @@
 Every matrix product is a libgpp_b200 tcgen05 GEMM: the four projections with fused
 bias / GELU (+ pre-activation) / residual epilogues, attention scores / P.V and the
 five backward attention products as ONE batched GEMM each (batch = sample x head,
-expressed as coordinate offsets into the packed QKV buffer).  LayerNorm, softmax and
-mean-pool are warp-per-row kernels.  Rows of the executor's [m, S*d] buffers are
-viewed as [m*S, d] token matrices.
+expressed as coordinate offsets into the packed QKV buffer).  For S <= 512 the scores
+GEMM carries the softmax in its epilogue (and dO.V^T the softmax backward), so the
+fp32 score / dP matrices never reach HBM.  LayerNorm and mean-pool are warp-per-row
+kernels.  Rows of the executor's [m, S*d] buffers are viewed as [m*S, d] token matrices.
 """
 
 from __future__ import annotations
@@ -60,8 +61,10 @@ class MMTLayer:
         st = lambda: [torch.zeros(T, dtype=torch.float32, device=dev) for _ in range(ex.ell)]
         self.mean1, self.rstd1, self.mean2, self.rstd2 = st(), st(), st(), st()
         z = lambda shape, t=dt: torch.zeros(shape, dtype=t, device=dev)
-        self.scores = z((Z * S, S), torch.float32)
-        self.dP = z((Z * S, S), torch.float32)
+        # fused attention softmax (tcgen05 epilogue) when the key row fits TMEM
+        self.fused = S <= 512 and S % 32 == 0 and self.dh % 64 == 0 and dt == torch.bfloat16
+        self.scores = None if self.fused else z((Z * S, S), torch.float32)
+        self.dP = None if self.fused else z((Z * S, S), torch.float32)
         self.dS = z((Z * S, S))
         self.dy2 = z((T, d)) if self.pool else None
         self.df, self.dh2, self.dy1, self.do = z((T, f)), z((T, d)), z((T, d)), z((T, d))
@@ -80,11 +83,14 @@ class MMTLayer:
         h1, qkv, P, o_ = self.h1[slot], self.qkv[slot], self.P[slot], self.o_[slot]
         be.layernorm_fwd(h1, self.mean1[slot], self.rstd1[slot], x2d, self._p("ln1_g"), self._p("ln1_b"))
         be.linear_fwd(qkv, h1, self._w("wqkv"), self._p("bqkv"), "none")
-        # scores[z] = Q_z K_z^T * scale  (fp32, z = sample * H + head)
-        be.gemm_batched(self.scores, S, qkv, 3 * d, T, False, qkv, 3 * d, T, False, S, S, dh,
-                        _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S),
-                        alpha=self.scale, out_f32=True)
-        be.softmax_fwd(P, self.scores)
+        # P[z] = softmax(Q_z K_z^T * scale)  (z = sample * H + head)
+        spec = _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S)
+        if self.fused:
+            be.attn_softmax(P, S, qkv, 3 * d, T, qkv, 3 * d, T, S, S, dh, self.scale, spec)
+        else:
+            be.gemm_batched(self.scores, S, qkv, 3 * d, T, False, qkv, 3 * d, T, False, S, S, dh, spec,
+                            alpha=self.scale, out_f32=True)
+            be.softmax_fwd(P, self.scores)
         # o[z] = P_z V_z  -> head-interleaved columns of o
         be.gemm_batched(o_, d, P, S, Z * S, False, qkv, 3 * d, T, True, S, dh, S,
                         _spec(Z, H, a_m_hi=H * S, a_m_lo=S, b_n0=2 * d, b_n_lo=dh, b_k_hi=S, c_hi=S * d, c_lo=dh))
@@ -132,11 +138,13 @@ class MMTLayer:
         # dV[z] = P_z^T dO_z
         be.gemm_batched(self.dqkv, 3 * d, P, S, Z * S, True, self.do, d, T, True, S, dh, S,
                         _spec(Z, H, a_k_hi=H * S, a_k_lo=S, b_n_lo=dh, b_k_hi=S, c0=2 * d, c_hi=S * 3 * d, c_lo=dh))
-        # dP[z] = dO_z V_z^T
-        be.gemm_batched(self.dP, S, self.do, d, T, False, qkv, 3 * d, T, False, S, S, dh,
-                        _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=2 * d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S),
-                        out_f32=True)
-        be.softmax_bwd(self.dS, P, self.dP, self.scale)
+        # dP[z] = dO_z V_z^T ;  dS = scale * P o (dP - rowsum(P o dP))
+        spec = _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=2 * d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S)
+        if self.fused:
+            be.attn_softmax_bwd(self.dS, S, P, S, self.do, d, T, qkv, 3 * d, T, S, S, dh, self.scale, spec)
+        else:
+            be.gemm_batched(self.dP, S, self.do, d, T, False, qkv, 3 * d, T, False, S, S, dh, spec, out_f32=True)
+            be.softmax_bwd(self.dS, P, self.dP, self.scale)
         # dQ[z] = dS_z K_z ;  dK[z] = dS_z^T Q_z
         be.gemm_batched(self.dqkv, 3 * d, self.dS, S, Z * S, False, qkv, 3 * d, T, True, S, dh, S,
                         _spec(Z, H, a_m_hi=H * S, a_m_lo=S, b_n0=d, b_n_lo=dh, b_k_hi=S, c_hi=S * 3 * d, c_lo=dh))

@@ -397,3 +397,34 @@ def test_pair_epilogues_partial_wave(cuda_lib, M, N, K, act):
         cuda_lib.linear_dgrad(dx, dy, w, saved=saved, act=act)
         torch.cuda.synchronize()
         assert _rel(dx, ref) < 2e-2
+
+
+@pytest.mark.parametrize("m,S,d,H", [(3, 256, 256, 4), (2, 512, 1024, 16), (2, 96, 256, 4)])
+def test_fused_attention_softmax(cuda_lib, m, S, d, H):
+    """Scores GEMM with the softmax (and its backward) in the tcgen05 epilogue vs the
+    unfused emulation (fp32 scores, row softmax) on the MMT packed-QKV layout."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle.torch_backend import TorchBackend
+    from paper_2406_17145_b200.runtime.mmt import _spec
+    g = torch.Generator(device="cuda").manual_seed(S + d)
+    dh, T, Z = d // H, m * S, m * H
+    scale = dh ** -0.5
+    qkv = torch.randn(T, 3 * d, device="cuda", generator=g).bfloat16()
+    do = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    spec_f = _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S)
+    spec_b = _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=2 * d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S)
+    P = torch.empty(Z * S, S, device="cuda", dtype=torch.bfloat16)
+    cuda_lib.attn_softmax(P, S, qkv, 3 * d, T, qkv, 3 * d, T, S, S, dh, scale, spec_f)
+    tb = TorchBackend("cpu")
+    Pr = torch.zeros(Z * S, S, dtype=torch.bfloat16)
+    tb.attn_softmax(Pr, S, qkv.cpu(), 3 * d, T, qkv.cpu(), 3 * d, T, S, S, dh, scale, spec_f)
+    torch.cuda.synchronize()
+    assert _rel(P.cpu(), Pr) < 1e-2
+    assert torch.allclose(P.float().sum(1).cpu(), torch.ones(Z * S), atol=2e-2)
+    dS = torch.empty_like(P)
+    cuda_lib.attn_softmax_bwd(dS, S, P, S, do, d, T, qkv, 3 * d, T, S, S, dh, scale, spec_b)
+    dSr = torch.zeros(Z * S, S, dtype=torch.bfloat16)
+    tb.attn_softmax_bwd(dSr, S, P.cpu(), S, do.cpu(), d, T, qkv.cpu(), 3 * d, T, S, S, dh, scale, spec_b)
+    torch.cuda.synchronize()
+    assert _rel(dS.cpu(), dSr) < 2e-2
