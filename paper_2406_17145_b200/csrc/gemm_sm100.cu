@@ -1108,6 +1108,8 @@ static int batched_bn(const void* a, int64_t lda, int64_t a_rows, const void* b,
   }
   if (N > 128)
     return launch_tc<256, 4, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, 1, stream, bs, ai, ao, bi, bo);
+  if (N <= 64)  // head-dim outputs (P.V, dQ, dK, dV): 64-wide tiles, 96 KB smem -> 2 CTAs / SM
+    return launch_tc<64, 4, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, 1, stream, bs, ai, ao, bi, bo);
   return launch_tc<128, 6, A_MN, B_MN, EPI>(a, lda, b, ldb, ep, M, N, K, 1, stream, bs, ai, ao, bi, bo);
 }
 
