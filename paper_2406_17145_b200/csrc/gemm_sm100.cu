@@ -1136,10 +1136,12 @@ static int batched_layout(const void* a, int64_t lda, int64_t a_rows, int a_mn, 
 // 2 x Z S^2 x 4 bytes per layer and direction).
 // ------------------------------------------------------------------------
 constexpr int ATT_N = 512;
-constexpr int ATT_STAGES = 2;
+constexpr int ATT_STAGES = 1;  // ~82 KB smem: two CTAs per SM (one computing, one loading)
+constexpr int ATT_EPI_WARPS = 8;                        // two per TMEM lane quarter
+constexpr int ATT_THREADS = 64 + 32 * ATT_EPI_WARPS;    // + TMA warp + MMA warp
 
 template <bool BWD>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(ATT_THREADS, 1)
     attn_softmax_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                         bf16* __restrict__ out, int64_t ldc, const bf16* __restrict__ P, int64_t ldp,
                         float alpha, int M, int N, int K, BatchSpec bs) {
@@ -1154,6 +1156,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty_bar = full_bar + ATT_STAGES;
   uint64_t* accum_bar = empty_bar + ATT_STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+  float* red = reinterpret_cast<float*>(smem + ATT_STAGES * STAGE_BYTES + 256);  // [2 halves][128 rows]
+  // per epilogue warp: a 32-row x 32-key bf16 chunk staged for coalesced row stores
+  constexpr int ATT_STG_LD = 80;  // bytes per staged row (64 + pad)
+  uint8_t* stg_all = smem + ATT_STAGES * STAGE_BYTES + 256 + 2 * BM * 4;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1178,17 +1184,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(accum_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(ATT_N)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  __syncthreads();  // barriers initialised
 
+  // The whole TMEM (512 columns) is one CTA's score block, so a second resident CTA
+  // blocks in tcgen05.alloc until this one frees it -- its TMA loads are issued BEFORE
+  // the allocation and overlap this CTA's epilogue.
   if (warp == 0) {
     if (lane == 0) {
       for (int kb = 0; kb < num_kb; ++kb) {
@@ -1201,6 +1201,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_load_2d(a_dst + A_BYTES + B_HALF, &tma_b, &full_bar[s], kb * BK + bk_off, bn_off + 256);
       }
     }
+  } else {
+    if (warp == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(ATT_N)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    asm volatile("bar.sync 2, %0;" ::"n"(32 + 32 * ATT_EPI_WARPS) : "memory");  // warps 1..9
+    tc_fence_after();
+  }
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
   } else if (warp == 1) {
     if (lane == 0) {
       for (int kb = 0; kb < num_kb; ++kb) {
@@ -1222,47 +1236,75 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       umma_commit(accum_bar);
     }
   } else {
+    // epilogue: warp w handles TMEM lane quarter w % 4 (its 32 query rows) and key half
+    // hf = (w - 2) / 4; the two halves of a row combine max / sums through smem
     mbar_wait(accum_bar, 0);
     tc_fence_after();
     const int q = warp & 3;
-    const int row = m_blk * BM + q * 32 + lane;
+    const int hf = (warp - 2) / 4;
+    const int lr = q * 32 + lane;
+    const int row = m_blk * BM + lr;
     const bool live = row < M;
-    const int nch = N / 32;
+    const int c_lo = hf * 8, c_hi = min(N / 32, hf * 8 + 8);  // this half's 32-key chunks
     const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    bf16* orow = out + c_off + static_cast<int64_t>(live ? row : 0) * ldc;
+    uint8_t* stg = stg_all + (warp - 2) * 32 * ATT_STG_LD;
+    const int row_base = m_blk * BM + q * 32;
+    // this thread's 32 outputs (64 B of its row) -> smem -> 4 lanes per row, 16 B each
+    auto store_chunk = [&](int c, const uint4 (&pk)[4]) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) *reinterpret_cast<uint4*>(stg + lane * ATT_STG_LD + i * 16) = pk[i];
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = (lane >> 2) + 8 * i, seg = lane & 3;
+        const uint4 val = *reinterpret_cast<const uint4*>(stg + r * ATT_STG_LD + seg * 16);
+        if (row_base + r < M)
+          *reinterpret_cast<uint4*>(out + c_off + static_cast<int64_t>(row_base + r) * ldc + c * 32 + seg * 8) = val;
+      }
+      __syncwarp();
+    };
+    auto combine = [&](float v, bool is_max) {
+      red[hf * BM + lr] = v;
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * ATT_EPI_WARPS) : "memory");
+      const float o = red[(1 - hf) * BM + lr];
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * ATT_EPI_WARPS) : "memory");  // red reusable
+      return is_max ? fmaxf(v, o) : v + o;
+    };
     if constexpr (!BWD) {
       float mx = -INFINITY;
-      for (int c = 0; c < nch; ++c) {
+      for (int c = c_lo; c < c_hi; ++c) {
         uint32_t v[32];
         tmem_ld32(trow + c * 32, v);
 #pragma unroll
         for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
       }
+      mx = combine(mx, true);
       const float sl2 = alpha * 1.4426950408889634f;  // alpha * log2(e); alpha > 0
       const float mb = mx * sl2;
       float sum = 0.f;
-      for (int c = 0; c < nch; ++c) {
+      for (int c = c_lo; c < c_hi; ++c) {  // one exp per score, parked back in TMEM
         uint32_t v[32];
         tmem_ld32(trow + c * 32, v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) sum += exp2f(fmaf(__uint_as_float(v[j]), sl2, -mb));
+        for (int j = 0; j < 32; ++j) {
+          const float e = exp2f(fmaf(__uint_as_float(v[j]), sl2, -mb));
+          sum += e;
+          v[j] = __float_as_uint(e);
+        }
+        tmem_st32(trow + c * 32, v);
       }
-      const float inv = 1.f / sum;
-      for (int c = 0; c < nch; ++c) {
+      const float inv = 1.f / combine(sum, false);
+      for (int c = c_lo; c < c_hi; ++c) {
         uint32_t v[32];
         tmem_ld32(trow + c * 32, v);
         uint4 pk[4];
         uint32_t* w = reinterpret_cast<uint32_t*>(pk);
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
-          const __nv_bfloat162 h2 = __floats2bfloat162_rn(exp2f(fmaf(__uint_as_float(v[j]), sl2, -mb)) * inv,
-                                                          exp2f(fmaf(__uint_as_float(v[j + 1]), sl2, -mb)) * inv);
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(v[j]) * inv, __uint_as_float(v[j + 1]) * inv);
           w[j / 2] = *reinterpret_cast<const uint32_t*>(&h2);
         }
-        if (live) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) reinterpret_cast<uint4*>(orow + c * 32)[i] = pk[i];
-        }
+        store_chunk(c, pk);
       }
     } else {
       const bf16* prow = P + c_off + static_cast<int64_t>(live ? row : 0) * ldp;
@@ -1281,7 +1323,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       };
       float D = 0.f;
-      for (int c = 0; c < nch; ++c) {
+      for (int c = c_lo; c < c_hi; ++c) {
         uint32_t v[32];
         float pf[32];
         load_p(c, pf);
@@ -1289,7 +1331,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) D = fmaf(pf[j], __uint_as_float(v[j]), D);
       }
-      for (int c = 0; c < nch; ++c) {
+      D = combine(D, false);
+      for (int c = c_lo; c < c_hi; ++c) {
         uint32_t v[32];
         float pf[32];
         load_p(c, pf);
@@ -1302,10 +1345,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                                           alpha * pf[j + 1] * (__uint_as_float(v[j + 1]) - D));
           w[j / 2] = *reinterpret_cast<const uint32_t*>(&h2);
         }
-        if (live) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) reinterpret_cast<uint4*>(orow + c * 32)[i] = pk[i];
-        }
+        store_chunk(c, pk);
       }
     }
   }
@@ -1326,14 +1366,15 @@ static int launch_attn_softmax(bf16* out, int64_t ldc, const bf16* P, int64_t ld
   if (rc) return rc;
   rc = make_map(&mb, b, ldb, b_rows, ldb, BK, 256);
   if (rc) return rc;
-  constexpr int SMEM = ATT_STAGES * (BM * BK * 2 + 2 * 256 * BK * 2) + 1024 + 256;
+  constexpr int SMEM = ATT_STAGES * (BM * BK * 2 + 2 * 256 * BK * 2) + 1024 + 256 + 2 * BM * 4 +
+                       ATT_EPI_WARPS * 32 * 80;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(attn_softmax_kernel<BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr_set = true;
   }
   const int64_t grid = static_cast<int64_t>(bs.nbatch) * ((M + BM - 1) / BM);
-  attn_softmax_kernel<BWD><<<static_cast<unsigned>(grid), NUM_THREADS, SMEM, stream>>>(
+  attn_softmax_kernel<BWD><<<static_cast<unsigned>(grid), ATT_THREADS, SMEM, stream>>>(
       ma, mb, out, ldc, P, ldp, alpha, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), bs);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
