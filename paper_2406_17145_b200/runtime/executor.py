@@ -608,12 +608,25 @@ class Executor:
         self.loss_acc.zero_()
         self._ar_handles = []
         seen_bw = False
+        # Sparse table updates (non-DP stages): a micro-batch's rows may be written only once
+        # no forward of this iteration will read the table again, i.e. after the stage's
+        # last fw -- from then on each finished bw's scatter overlaps the cool-down instead
+        # of all of them piling up after the last task (exact: the same per-row sums).
+        eager_sparse = step_optimizer and bool(self.tables) and self.d == 1
+        fw_left = sum(1 for t in self.stage.schedule if t.direction == "fw")
+        bw_done: list[int] = []
         for t in self.stage.schedule:
             if t.direction == "fw":
                 self._fw(t.index, batch)
+                fw_left -= 1
             else:
                 self._bw(t.index, batch, accumulate=seen_bw)
                 seen_bw = True
+                bw_done.append(t.index)
+            if eager_sparse and fw_left == 0:
+                for j in bw_done:
+                    self._sparse_update(batch, j)
+                bw_done = []
         for key in list(self._send_works):
             self._wait_sends(key)
         if self.d > 1:
@@ -623,7 +636,7 @@ class Executor:
             self.tp.join(self._ar_handles)
             self._ar_handles = []
         if step_optimizer:
-            for o, table in self.tables.items():
+            for o, table in self.tables.items() if not eager_sparse else ():
                 idx = batch[self.layers[o].data_key]
                 g_o = self.emb_grad[o]
                 if self.d > 1:  # every replica applies every replica's sparse updates
@@ -640,6 +653,13 @@ class Executor:
             else:
                 self.be.sgd_step(self.master, self.shadow, self.grad, self.lr)
         return self.loss_acc
+
+    def _sparse_update(self, batch, j: int) -> None:
+        """Embedding-bag SGD for micro-batch j's rows of every table on this stage."""
+        rows = slice(j * self.m, (j + 1) * self.m)
+        for o, table in self.tables.items():
+            idx = batch[self.layers[o].data_key][rows]
+            self.be.embbag_sgd(table, self.emb_grad[o][rows], idx, self.lr)
 
     def stage_loss(self, loss: torch.Tensor) -> float:
         """Loss of the whole mini-batch on a head rank (sums the DP replicas' shares)."""
