@@ -145,6 +145,39 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _gemm_traffic(workload: str) -> dict:
+    """DRAM bytes per GEMM launch from the committed ncu --set full capture of one CANDLE
+    step (profiles/ncu_step_gemms_r1d_summary.csv), averaged over the step's launch mix
+    (28 tower fw, 21 tower dgrad, 28 tower wgrad+SGD, one of each tail GEMM), beside the
+    algorithmic bytes of the same mix (operands + outputs + fp32 master read/write + bf16
+    shadow).  Only the CANDLE step was captured; other workloads report null."""
+    if workload != "candle":
+        return {"traffic": None}
+    import csv
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_step_gemms_r1d_summary.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+    except OSError:
+        return {"traffic": None}
+    h = rows[0]
+    mb = {r[0]: float(r[h.index("dram__bytes_read.sum")]) + float(r[h.index("dram__bytes_write.sum")]) for r in rows[2:]}
+    mix = {"fw tower": (28, 48.0), "fw tail": (1, 119.4), "dgrad tail": (1, 178.2), "wgrad+SGD tail": (1, 353.3),
+           "dgrad tower": (21, 56.0), "wgrad+SGD tower": (28, 176.0)}
+    tot = alg = n = 0.0
+    for role, v in mb.items():
+        key = next((k for k in mix if role.startswith(k + " ")), None)
+        if key is None:
+            continue
+        c, a = mix[key]
+        tot, alg, n = tot + c * v, alg + c * a, n + c
+    if not n:
+        return {"traffic": None}
+    return {"traffic": round(tot / n, 1), "traffic_unit": "MB per GEMM launch (ncu dram read+write, step mix)",
+            "algorithmic_MB_per_launch": round(alg / n, 1),
+            "traffic_source": "profiles/ncu_step_gemms_r1d_summary.csv"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -330,7 +363,10 @@ def main():
                 "parallelism": f"{args.mode} stages={len(sg.stages)} depth={sim.depth}",
                 "stages": [{"ops": len(s.op_ids), "b": s.micro_batch, "d": s.dp_degree,
                             "inflight": s.sched_cfg.inflight_samples} for s in sg.stages],
-                "l2": "per-step working set (weights+master+grads ~2.9 GB) >> 126 MB L2",
+                "l2": {"candle": "per-step working set (weights+master+grads ~2.9 GB) >> 126 MB L2",
+                       "dlrm": "per-step working set (26 x 256 MB fp32 tables + MLP master/grads) >> 126 MB L2",
+                       "mmt": "per-step working set (48 layers x ~150 MB master/grad/shadow + activations) >> 126 MB L2",
+                       "toy": "toy model fits in L2 (launch-bound; no roofline claim)"}.get(args.workload),
                 "optimizer": "SGD fp32 master + bf16 shadow (fused into last wgrad epilogue when DP=1)",
                 "plan_s": round(t_plan, 3), "cuda_graph": graphed is not None, "costs": args.costs,
             },
@@ -339,7 +375,8 @@ def main():
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "kernel": "gemm_tc_pair_kernel (tcgen05 cta_group::2 bf16 GEMM, all dense fw/dgrad/wgrad+SGD)",
                          "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
-                         "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
+                         "frac": round(achieved / peak, 4) if peak else None,
+                         **_gemm_traffic(args.workload),
                          "peak_source": f"{peak_src} bf16_tflops_sustained",
                          "share_of_step": round(gemm_share, 4),
                          "by_kind": summ.get("by_kind", {})},
