@@ -178,6 +178,74 @@ def _gemm_traffic(workload: str) -> dict:
             "traffic_source": "profiles/ncu_step_gemms_r1d_summary.csv"}
 
 
+def _time_arm(wl, world, rank, dev, mode, args, clocks=True):
+    """Plan ``mode`` (gpp | spp) for ``world`` GPUs, build this rank's executor, capture its
+    iteration in a CUDA graph and time ``args.steps`` replays (max over ranks)."""
+    from paper_2406_17145_b200.runtime import lib
+    from paper_2406_17145_b200.runtime.api import plan
+    from paper_2406_17145_b200.runtime.data import make_batch, to_device_rows
+    from paper_2406_17145_b200.runtime.executor import Executor
+    from paper_2406_17145_b200.runtime.profiler import TimedBackend
+
+    t_plan = time.perf_counter()
+    strategy = plan(wl, world, mode, costs=args.costs)
+    t_plan = time.perf_counter() - t_plan
+    sg = strategy.stage_graph
+    be = TimedBackend(dev)
+    be.enabled = False
+    ex = Executor(wl, sg, rank, world, be, lr=1e-4)
+    keys = set(ex.data_keys()) if ex.stage else set()
+    full = make_batch(wl, 0, keys=keys)
+    dev_batch = to_device_rows(ex, full, ex.dtype, dev) if ex.stage else {}
+    graphed = None
+    graphed_launches = 0
+    if not args.no_graph and (ex.stage is not None or world > 1):
+        from paper_2406_17145_b200.runtime.graph import GraphedIteration
+
+        n_before = lib.launch_count()
+        ex.run_iteration(dev_batch)
+        graphed_launches = lib.launch_count() - n_before  # libgpp kernels per iteration
+        graphed = GraphedIteration(ex, dev_batch)
+        for b in graphed.bufs:
+            for k in b:
+                b[k].copy_(dev_batch[k])
+
+    def step(i=0):
+        return graphed.replay(i) if graphed is not None else ex.run_iteration(dev_batch)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(dev.index) if clocks else None
+    if sampler:
+        sampler.start()
+    launches0 = lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    launches = lib.launch_count() - launches0
+    if graphed is not None:  # replays launch the captured kernels without host calls
+        launches = graphed_launches * args.steps
+    ms = e0.elapsed_time(e1)
+    clk = sampler.stop() if sampler else None
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        lt = torch.tensor([float(launches)], device=dev)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+    return {"ex": ex, "sg": sg, "graphed": graphed, "dev_batch": dev_batch, "ms": ms, "launches": launches,
+            "clocks": clk, "plan_s": t_plan, "be": be}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -191,6 +259,7 @@ def main():
     ap.add_argument("--per-gpu-batch", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
+    ap.add_argument("--no-spp", action="store_true", help="skip the SPP comparison arm (N > 1)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -205,72 +274,17 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_2406_17145_b200 import model as M
-    from paper_2406_17145_b200.runtime import lib
-    from paper_2406_17145_b200.runtime.api import plan
-    from paper_2406_17145_b200.runtime.data import make_batch, to_device_rows
-    from paper_2406_17145_b200.runtime.executor import Executor
-    from paper_2406_17145_b200.runtime.profiler import TimedBackend
-    from paper_2406_17145_b200.sim import simulate
+    from paper_2406_17145_b200.runtime.data import make_batch
+    from paper_2406_17145_b200.runtime.api import twin
     from paper_2406_17145_b200.workloads import b200_cluster, with_measured_curves
 
     wl = _workload(args.workload, world, args.per_gpu_batch)
-    t_plan = time.perf_counter()
-    strategy = plan(wl, world, args.mode, costs=args.costs)
-    t_plan = time.perf_counter() - t_plan
-    sg = strategy.stage_graph
     dev = torch.device("cuda", local)
-    be = TimedBackend(dev)
-    be.enabled = False
-    ex = Executor(wl, sg, rank, world, be, lr=1e-4)
+    arm = _time_arm(wl, world, rank, dev, args.mode, args)
+    ex, sg, graphed, dev_batch, ms, launches, clk, t_plan, be = (
+        arm["ex"], arm["sg"], arm["graphed"], arm["dev_batch"], arm["ms"], arm["launches"], arm["clocks"],
+        arm["plan_s"], arm["be"])
     keys = set(ex.data_keys()) if ex.stage else set()
-
-    # ---------------- value: inputs resident in HBM ----------------
-    full = make_batch(wl, 0, keys=keys)
-    dev_batch = to_device_rows(ex, full, ex.dtype, dev) if ex.stage else {}
-    graphed = None
-    if not args.no_graph and (ex.stage is not None or world > 1):
-        from paper_2406_17145_b200.runtime.graph import GraphedIteration
-
-        n_before = lib.launch_count()
-        ex.run_iteration(dev_batch)
-        graphed_launches = lib.launch_count() - n_before  # libgpp kernels per iteration
-        graphed = GraphedIteration(ex, dev_batch)
-        for b in graphed.bufs:
-            for k in b:
-                b[k].copy_(dev_batch[k])
-
-    def step(i=0):
-        return graphed.replay(i) if graphed is not None else ex.run_iteration(dev_batch if graphed is None else None)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
-    launches0 = lib.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(args.steps):
-        step()
-    e1.record()
-    torch.cuda.synchronize()
-    launches = lib.launch_count() - launches0
-    if graphed is not None:  # replays launch the captured kernels without host calls
-        launches = graphed_launches * args.steps
-    ms = e0.elapsed_time(e1)
-    clk = clocks.stop()
-    if world > 1:
-        dist.barrier()
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        lt = torch.tensor([float(launches)], device=dev)
-        dist.all_reduce(lt)
-        launches = int(lt.item())
     value = wl.mini_batch * args.steps / (ms / 1e3)
 
     # ---------------- e2e: host buffers through the public API ----------------
@@ -324,22 +338,86 @@ def main():
         e2e_ms = float(t.item())
     e2e = wl.mini_batch * args.steps / (e2e_ms / 1e3)
 
-    # ---------------- roofline: live GEMM timing (events around each launch) ----------------
-    be.enabled = True
-    be.reset()
-    prof_iters = 2
-    for _ in range(prof_iters):
-        ex.run_iteration(dev_batch)
+    # ---------------- roofline + busy time: events around every kernel call ----------------
+    # One iteration captured in a CUDA graph with an event-record node on each side of every
+    # kernel call (external events keep their timestamps across replays) and replayed: the
+    # durations are those of the graph-replayed step.  Fallback: eager iterations with the
+    # GPU queue kept ahead of the host (a sleep longer than the host's enqueue time).
+    prof_iters = 1
+    timing = "cuda-graph event nodes"
     torch.cuda.synchronize()
-    summ = be.summary() if ex.stage else {"flops": 0.0, "ms": 0.0, "tflops": 0.0, "launches": 0}
+    be.enabled = True
+    be.external = True
+    be.reset()
+    try:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        pg = torch.cuda.CUDAGraph()
+        if world > 1:
+            dist.barrier()
+        with torch.cuda.graph(pg):
+            ex.run_iteration(dev_batch)
+        be.enabled = False
+        for _ in range(3):
+            pg.replay()
+        torch.cuda.synchronize()
+    except Exception as exc:  # noqa: BLE001 - report and fall back to eager timing
+        timing = f"eager events, queue preloaded (graph capture failed: {type(exc).__name__})"
+        be.external = False
+        be.enabled = False
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        h0 = time.perf_counter()
+        ex.run_iteration(dev_batch)
+        host_s = time.perf_counter() - h0
+        torch.cuda.synchronize()
+        be.enabled = True
+        be.reset()
+        if world > 1:
+            dist.barrier()
+        be.preload(host_s)
+        ex.run_iteration(dev_batch)
+        torch.cuda.synchronize()
+    summ = be.summary() if ex.stage else {"flops": 0.0, "ms": 0.0, "busy_ms": 0.0, "tflops": 0.0, "launches": 0}
     be.enabled = False
     peaks, peak_src = _peaks()
-    gemm_share = (summ["ms"] / prof_iters) / (ms / args.steps) if ms > 0 else 0.0
+    t_iter = ms / args.steps
+    cuda_graph = graphed is not None
+    gemm_share = (summ["ms"] / prof_iters) / t_iter if ms > 0 else 0.0
+    busy = summ["busy_ms"] / prof_iters  # this rank's kernel time per iteration
+    busy_sum = busy
+    if world > 1:
+        bt = torch.tensor([busy], device=dev, dtype=torch.float64)
+        dist.all_reduce(bt)
+        busy_sum = float(bt.item())
+    bubble = max(0.0, 1.0 - busy_sum / (world * t_iter))
+    # summed stage-compute roofline: every sample's algorithmic FLOPs at the
+    # sustained tensor peak plus its HBM-bound bytes at the measured copy bandwidth, over N GPUs
+    t_roof = wl.mini_batch * (wl.flops_per_sample / (peaks["bf16_tflops_sustained"] * 1e12)
+                              + wl.bytes_per_sample / (peaks["hbm_gbs"] * 1e9)) / world * 1e3
+
+    # ---------------- GPP vs the sequential pipeline (SPP) on the same runtime ----------------
+    spp = None
+    if world > 1 and args.mode == "gpp" and not args.no_spp:
+        spp_sg_gpp = [(len(s.op_ids), s.micro_batch, s.dp_degree) for s in sg.stages]
+        del graphed, ex, dev_batch, arm
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        sp = _time_arm(wl, world, rank, dev, "spp", args, clocks=False)
+        spp_value = wl.mini_batch * args.steps / (sp["ms"] / 1e3)
+        spp = {"value": round(spp_value, 3), "ms_per_step": round(sp["ms"] / args.steps, 4),
+               "gpp_vs_spp_speedup": round(value / spp_value, 4), "plan_s": round(sp["plan_s"], 3),
+               "stages": [{"ops": len(s.op_ids), "b": s.micro_batch, "d": s.dp_degree} for s in sp["sg"].stages],
+               "gpp_stages": [{"ops": a, "b": b, "d": d} for a, b, d in spp_sg_gpp],
+               "note": "SPP = spp_optimize (SPEC.md:384-392) strategy on this same runtime, CUDA-graph replay"}
 
     # ---------------- simulated twin + bubble estimate ----------------
     cluster = b200_cluster(world)
     sim_graph = with_measured_curves(wl)[0].graph if args.costs == "measured" else wl.graph
-    sim = simulate(sg, cluster, sim_graph, sync_epilogue=True)
+    sim = twin(sg, cluster, sim_graph)
 
     if rank == 0:
         cpu = None
@@ -368,7 +446,7 @@ def main():
                        "mmt": "per-step working set (48 layers x ~150 MB master/grad/shadow + activations) >> 126 MB L2",
                        "toy": "toy model fits in L2 (launch-bound; no roofline claim)"}.get(args.workload),
                 "optimizer": "SGD fp32 master + bf16 shadow (fused into last wgrad epilogue when DP=1)",
-                "plan_s": round(t_plan, 3), "cuda_graph": graphed is not None, "costs": args.costs,
+                "plan_s": round(t_plan, 3), "cuda_graph": cuda_graph, "costs": args.costs,
             },
             "e2e": {"value": round(e2e, 3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d_bytes),
                     "d2h_bytes_per_step": 4},
@@ -378,10 +456,19 @@ def main():
                          "frac": round(achieved / peak, 4) if peak else None,
                          **_gemm_traffic(args.workload),
                          "peak_source": f"{peak_src} bf16_tflops_sustained",
-                         "share_of_step": round(gemm_share, 4),
-                         "by_kind": summ.get("by_kind", {})},
+                         "share_of_step": round(gemm_share, 4), "timing": timing,
+                         "by_kind": summ.get("by_kind", {}),
+                         "other_kernels_ms": summ.get("other_ms", {})},
             "clocks": clk,
+            "step_roofline": {"t_roof_ms": round(t_roof, 4), "frac": round(t_roof / t_iter, 4),
+                              "flops_per_sample": wl.flops_per_sample, "bytes_per_sample": wl.bytes_per_sample,
+                              "note": "summed stage-compute roofline: B*(F/P_sustained + bytes/BW_hbm)/N vs measured step"},
+            "bubble": {"measured": round(bubble, 4), "busy_ms_per_gpu": round(busy_sum / world, 4),
+                       "model": round(sim.bubble_fraction, 4),
+                       "note": "1 - sum over ranks of kernel busy time / (N * step time); busy from events around "
+                               "every kernel call in eager iterations"},
             "sim": {"iteration_ms_model": round(sim.iteration_ms, 4), "bubble_fraction_model": round(sim.bubble_fraction, 4)},
+            "spp": spp,
         }
         if cpu:
             line["cpu_baseline"] = cpu

@@ -22,6 +22,7 @@
  *   gpp_sgd_step                fused optimizer over a stage's parameters
  *   gpp_layernorm_fwd / _bwd, gpp_softmax_fwd / _bwd, gpp_meanpool_fwd / _bwd,
  *   gpp_gemm_batched            MMT pre-LN transformer layer (attention as batched GEMMs)
+ *   gpp_attn_fwd / gpp_attn_bwd       fused MMT attention (softmax + P.V / softmax-bwd + dS.K)
  *   gpp_attn_softmax / gpp_attn_softmax_bwd  attention scores with the softmax (or its
  *                               backward) fused into the tcgen05 epilogue (S <= 512)
  *   gpp_embbag_fwd / gpp_embbag_sgd        DLRM embedding-bag and its sparse SGD scatter
@@ -190,6 +191,19 @@ int gpp_attn_softmax(void* p, int64_t ldp, const void* q, int64_t ldq, int64_t q
 int gpp_attn_softmax_bwd(void* ds, int64_t ldc, const void* p, int64_t ldp, const void* dout, int64_t ldo,
                          int64_t o_rows, const void* v, int64_t ldv, int64_t v_rows, int64_t M, int64_t N,
                          int64_t K, float scale, const int64_t* spec, void* stream);
+
+/* Fused MMT attention (one launch per direction; attn_sm100.cu).  Packed QKV [m*S, 3d]
+ * (Q | K | V, head h in columns h*64 .. h*64+63), z = sample*H + head, P / ds [m*H*S, S]:
+ *   gpp_attn_fwd:  p[z] = softmax(scale q[z] k[z]^T)  (stored for the backward) and
+ *                  o[:, h*64..] = p[z] v[z]                                 (bf16)
+ *   gpp_attn_bwd:  ds[z] = scale p[z] o (dout[z] v[z]^T - D),  D = rowsum(dout o o),
+ *                  dqkv[:, h*64..] (the Q block) = ds[z] k[z]                 (bf16)
+ * Requires d == 64 H, S in {128, 256, 384, 512}.  Replaces gpp_attn_softmax + the P.V
+ * gpp_gemm_batched (fw) and gpp_attn_softmax_bwd + the dS.K gpp_gemm_batched (bw). */
+int gpp_attn_fwd(const void* qkv, void* p, void* o, int64_t ldo, int64_t m, int64_t S, int64_t d, int64_t H,
+                 float scale, void* stream);
+int gpp_attn_bwd(const void* qkv, const void* p, const void* o, int64_t ldo, const void* dout, int64_t lddo,
+                 void* ds, void* dqkv, int64_t m, int64_t S, int64_t d, int64_t H, float scale, void* stream);
 
 /* ---- DLRM: embedding bags and the dot interaction ------------- */
 /* pooled[m, :D] = sum_b table[idx[m*ldi + b], :D]; fp32 table [rows, D], bf16 pooled, D = 64. */

@@ -205,6 +205,33 @@ class TorchBackend:
     def meanpool_bwd(self, dx, dout, M, S, D):
         dx.copy_((dout.float()[:, None, :] / S).expand(M, S, D).reshape(M * S, D))
 
+    @staticmethod
+    def _heads(t, m, S, H, col0, dh):
+        """[m*S, >=col0+H*dh] head-interleaved columns -> [m*H, S, dh] fp32."""
+        return t[:, col0:col0 + H * dh].float().reshape(m, S, H, dh).permute(0, 2, 1, 3).reshape(m * H, S, dh)
+
+    def attn_fwd(self, qkv, p, o, m, S, d, H, scale):
+        """Emulates gpp_attn_fwd: P = softmax(scale Q K^T) (bf16, kept), O = bf16(P) V."""
+        dh = d // H
+        q, k, v = (self._heads(qkv, m, S, H, c, dh) for c in (0, d, 2 * d))
+        pr = torch.softmax(scale * (q @ k.transpose(1, 2)), dim=2).to(p.dtype)
+        p.copy_(pr.reshape(m * H * S, S))
+        oz = pr.float() @ v
+        o[:, :d].copy_(oz.reshape(m, H, S, dh).permute(0, 2, 1, 3).reshape(m * S, d))
+
+    def attn_bwd(self, qkv, p, o, dout, ds, dqkv, m, S, d, H, scale):
+        """Emulates gpp_attn_bwd: dP = dO V^T, D = rowsum(dO o O), dS = scale P (dP - D),
+        dQ = bf16(dS) K into the Q block of dqkv."""
+        dh = d // H
+        k, v = self._heads(qkv, m, S, H, d, dh), self._heads(qkv, m, S, H, 2 * d, dh)
+        g, oz = self._heads(dout, m, S, H, 0, dh), self._heads(o, m, S, H, 0, dh)
+        pz = p.float().reshape(m * H, S, S)
+        D = (g * oz).sum(2, keepdim=True)
+        dsz = (scale * pz * (g @ v.transpose(1, 2) - D)).to(ds.dtype)
+        ds.copy_(dsz.reshape(m * H * S, S))
+        dq = dsz.float() @ k
+        dqkv[:, :d].copy_(dq.reshape(m, H, S, dh).permute(0, 2, 1, 3).reshape(m * S, d))
+
     def attn_softmax(self, p, ldp, q, ldq, q_rows, k, ldk, k_rows, M, N, K, scale, spec):
         """Emulates gpp_attn_softmax: scores GEMM (fp32) then row softmax, per batch."""
         nb = spec[0]

@@ -58,6 +58,14 @@ int tc_attn_softmax(int bwd, void* out, int64_t ldc, const void* P, int64_t ldp,
 int tc_gemm_batched(int epi, const void* a, int64_t lda, int64_t a_rows, int a_mn, const void* b,
                     int64_t ldb, int64_t b_rows, int b_mn, const EpiParams& ep, const BatchSpec& bs,
                     int64_t M, int64_t N, int64_t K, cudaStream_t stream);
+// MMT attention, one CTA per (sample x head, 128 query rows), S % 128 == 0, S <= 512,
+// head dim 64, packed QKV [T, 3d] (attn_sm100.cu):
+//   fw : P = softmax(alpha Q K^T) -> HBM (for the backward), O = P V  -> o[:, head*64..]
+//   bw : dP = dO V^T, D = rowsum(dO o O), dS = alpha P o (dP - D) -> HBM, dQ = dS K -> dqkv
+int tc_attn_fwd(const void* qkv, void* P, void* o, int64_t ldo, int64_t m, int64_t S, int64_t d, int64_t H,
+                float alpha, cudaStream_t stream);
+int tc_attn_bwd(const void* qkv, const void* P, const void* o, int64_t ldo, const void* dout, int64_t lddo,
+                void* dS, void* dqkv, int64_t m, int64_t S, int64_t d, int64_t H, float alpha, cudaStream_t stream);
 // bf16 operands, tcgen05 + TMA (gemm_sm100.cu).
 int tc_gemm(int epi, const void* a, int64_t lda, int a_mn, const void* b, int64_t ldb, int b_mn,
             const EpiParams& ep, int64_t M, int64_t N, int64_t K, cudaStream_t stream);

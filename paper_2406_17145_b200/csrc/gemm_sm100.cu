@@ -815,6 +815,11 @@ static int make_map(CUtensorMap* out, const void* ptr, int64_t inner, int64_t ou
   return GPP_OK;
 }
 
+int make_map_bf16(CUtensorMap* out, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
+                  int box_outer) {
+  return make_map(out, ptr, inner, outer, ld, box_inner, box_outer);
+}
+
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 static int launch_tc(const void* a, int64_t lda, const void* b, int64_t ldb, const EpiParams& ep,
                      int64_t M, int64_t N, int64_t K, int k_splits, cudaStream_t stream,

@@ -21,13 +21,22 @@ from .backend import CudaBackend
 from .data import make_batch, to_device_rows
 from .executor import Executor
 
-__all__ = ["plan", "build", "RunReport", "execute", "dist_env"]
+__all__ = ["plan", "twin", "build", "RunReport", "execute", "dist_env"]
 
 
 def dist_env() -> tuple[int, int, int]:
     """(rank, world, local_rank) from torchrun's environment (1 process per GPU)."""
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def twin(sg: StageGraph, cluster, graph):
+    """The executor's simulated twin: op-granular sends/receives (what runtime.executor
+    does) and, for DP stages, the once-per-iteration all-reduce plus the unfused SGD pass
+    (14 B per parameter = 3.5 x the fp32 param_bytes) after the last task."""
+    from ..sim import simulate
+
+    return simulate(sg, cluster, graph, sync_epilogue=True, op_granular=True, optimizer_bytes_per_param_byte=3.5)
 
 
 def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions | None = None,
@@ -70,7 +79,7 @@ def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions 
                     cand = fn(wl.graph, cluster, B, o)
                 except P.NoFeasibleStrategy:
                     continue
-                t = simulate(cand.stage_graph, cluster, wl.graph, sync_epilogue=True).iteration_ms
+                t = twin(cand.stage_graph, cluster, wl.graph).iteration_ms
                 if best_t is None or t < best_t:
                     best, best_t = cand, t
         if best is None:

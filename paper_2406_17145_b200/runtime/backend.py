@@ -106,6 +106,12 @@ class CudaBackend:
     def attn_softmax_bwd(self, ds, ldc, p, ldp, dout, ldo, o_rows, v, ldv, v_rows, M, N, K, scale, spec):
         lib.attn_softmax_bwd(ds, ldc, p, ldp, dout, ldo, o_rows, v, ldv, v_rows, M, N, K, scale, spec)
 
+    def attn_fwd(self, qkv, p, o, m, S, d, H, scale):
+        lib.attn_fwd(qkv, p, o, m, S, d, H, scale)
+
+    def attn_bwd(self, qkv, p, o, dout, ds, dqkv, m, S, d, H, scale):
+        lib.attn_bwd(qkv, p, o, dout, ds, dqkv, m, S, d, H, scale)
+
     def gemm_batched(self, c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, spec, alpha=1.0,
                      out_f32=False):
         lib.gemm_batched(c, ldc, a, lda, a_rows, a_mn, b, ldb, b_rows, b_mn, M, N, K, spec, alpha=alpha,

@@ -253,6 +253,31 @@ class Executor:
         for j in range(self.n):
             self.recv_fw[j] = _order(self.recv_fw[j])
             self.send_fw[j] = _order(self.send_fw[j])
+        # Stage edges that carry no operator data (e.g. the chain edges of a sequential
+        # pipeline whose consecutive stages are independent branches) still order tasks in
+        # the simulator's semantics (fw(y, j) waits for fw(x, i), bw(x, j) for bw(y, i),
+        # SPEC.md:436-441): they are realised as 4-byte token messages, sent when the
+        # producing task ends and waited for before the consuming task's first op.
+        data_pairs = {(self.owner[u], self.owner[v]) for u, v in g.edges
+                      if u in self.owner and v in self.owner and self.owner[u] != self.owner[v]}
+        self.tok_in = {j: [] for j in range(self.n)}   # fw: wait at task start; bw: send at task end
+        self.tok_out = {j: [] for j in range(self.n)}  # fw: send at task end; bw: wait at task start
+        for (a, b) in sorted(self.sg.edges):
+            if (a, b) in data_pairs or st.id not in (a, b):
+                continue
+            seen = set()
+            for pc in build_pieces(self.sg.by_id[a], self.sg.by_id[b], [-1], self.B):
+                key = (pc.producer, pc.consumer, pc.p_task, pc.c_task)
+                if key in seen:
+                    continue
+                seen.add(key)
+                if b == st.id and pc.consumer == self.rank:
+                    self.tok_in[pc.c_task].append(pc)
+                if a == st.id and pc.producer == self.rank:
+                    self.tok_out[pc.p_task].append(pc)
+        for j in range(self.n):
+            self.tok_in[j] = _order(self.tok_in[j])
+            self.tok_out[j] = _order(self.tok_out[j])
         self.first_bw = next(t.index for t in st.schedule if t.direction == "bw")
         dense = [o for o in self.ops if self.wl.layers[o].kind == "dense"]
         self._next_dense = {a: b for a, b in zip(dense, dense[1:])}
@@ -375,6 +400,9 @@ class Executor:
             self.gsend[u] = self._ring((m, w))
         self.loss_acc = torch.zeros(1, dtype=torch.float32, device=self.dev)
         self._send_works: dict[tuple, list] = {}
+        # ordering tokens of data-less stage edges (content irrelevant)
+        self.tok_tx = torch.zeros(1, dtype=torch.float32, device=self.dev)
+        self.tok_rx = torch.zeros(1, dtype=torch.float32, device=self.dev)
 
     # ------------------------------------------------------------ data access
     def local_rows(self, key_tensor_full: torch.Tensor) -> torch.Tensor:
@@ -440,6 +468,8 @@ class Executor:
                                   for pc in self.recv_fw[j]])
         for pc, w in zip(self.recv_fw[j], rws):
             pending.setdefault(pc.tensor, []).append(w)
+        for w in self._irecv_many([(self.tok_rx, pc.producer) for pc in self.tok_in[j]]):
+            w.wait()
         self._wait_sends(("fw", slot))
         sends = _OrderedSends(self.send_fw[j], lambda pc: pc.consumer)
         post = lambda pcs: self._isend_many([(self.out[pc.tensor][slot][pc.p_row0:pc.p_row0 + pc.rows],
@@ -496,6 +526,7 @@ class Executor:
             for w in ws:
                 w.wait()
         works += sends.flush(post, everything=True)
+        works += self._isend_many([(self.tok_tx, pc.consumer) for pc in self.tok_out[j]])
         if works:
             self._send_works[("fw", slot)] = works
 
@@ -507,6 +538,8 @@ class Executor:
                                   for pc in self.send_fw[j]])
         for pc, w in zip(self.send_fw[j], rws):
             pending.setdefault(pc.tensor, []).append(w)
+        for w in self._irecv_many([(self.tok_rx, pc.consumer) for pc in self.tok_out[j]]):
+            w.wait()
         self._wait_sends(("bw", slot))
         # input gradients go back along task j's forward pieces as soon as they are final
         sends = _OrderedSends(self.recv_fw[j], lambda pc: pc.producer)
@@ -593,6 +626,7 @@ class Executor:
             for w in ws:
                 w.wait()
         works += sends.flush(post, everything=True)
+        works += self._isend_many([(self.tok_tx, pc.producer) for pc in self.tok_in[j]])
         if works:
             self._send_works[("bw", slot)] = works
 

@@ -59,6 +59,8 @@ _SIGS = {
     "gpp_meanpool_fwd": ([_vp, _i64, _vp, _i64, _i64, _i64, _vp], _i32),
     "gpp_meanpool_bwd": ([_vp, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
     "gpp_gemm_batched": ([_vp, _i64, _vp, _i64, _i64, _i32, _vp, _i64, _i64, _i32, _i64, _i64, _i64, _f32, _f32, _i32, _vp, _vp], _i32),
+    "gpp_attn_fwd": ([_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
+    "gpp_attn_bwd": ([_vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_attn_softmax": ([_vp, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp, _vp], _i32),
     "gpp_attn_softmax_bwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp, _vp], _i32),
     "gpp_embbag_fwd": ([_vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp], _i32),
@@ -296,6 +298,19 @@ def attn_softmax_bwd(ds, ldc, p, ldp, dout, ldo, o_rows, v, ldv, v_rows, M, N, K
     arr = (ctypes.c_int64 * 17)(*[int(x) for x in spec])
     call("gpp_attn_softmax_bwd", _ptr(ds), ldc, _ptr(p), ldp, _ptr(dout), ldo, o_rows, _ptr(v), ldv, v_rows, M, N,
          K, float(scale), ctypes.cast(arr, ctypes.c_void_p), _stream(stream))
+
+
+def attn_fwd(qkv, p, o, m, S, d, H, scale, stream=None):
+    """Fused MMT attention forward: p = softmax(scale q k^T) (kept for the backward),
+    o[:, h*64..] = p v (one tcgen05 kernel; packed qkv [m*S, 3d], p [m*H*S, S])."""
+    call("gpp_attn_fwd", _ptr(qkv), _ptr(p), _ptr(o), _ld(o), m, S, d, H, float(scale), _stream(stream))
+
+
+def attn_bwd(qkv, p, o, dout, ds, dqkv, m, S, d, H, scale, stream=None):
+    """Fused MMT attention backward: ds = scale p o (dout v^T - rowsum(dout o o)) and the
+    Q block of dqkv = ds k (one tcgen05 kernel)."""
+    call("gpp_attn_bwd", _ptr(qkv), _ptr(p), _ptr(o), _ld(o), _ptr(dout), _ld(dout), _ptr(ds), _ptr(dqkv), m, S, d,
+         H, float(scale), _stream(stream))
 
 
 def prefetch_hint(t):

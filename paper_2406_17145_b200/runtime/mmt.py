@@ -5,12 +5,13 @@
     [pool: out = mean over the S tokens of y2 — the branch output fed to the concat]
 
 Every matrix product is a libgpp_b200 tcgen05 GEMM: the four projections with fused
-bias / GELU (+ pre-activation) / residual epilogues, attention scores / P.V and the
-five backward attention products as ONE batched GEMM each (batch = sample x head,
-expressed as coordinate offsets into the packed QKV buffer).  For S <= 512 the scores
-GEMM carries the softmax in its epilogue (and dO.V^T the softmax backward), so the
-fp32 score / dP matrices never reach HBM.  LayerNorm and mean-pool are warp-per-row
-kernels.  Rows of the executor's [m, S*d] buffers are viewed as [m*S, d] token matrices.
+bias / GELU (+ pre-activation) / residual epilogues.  Attention with 64-wide heads and
+S in {128, ..., 512} is ONE kernel per direction (csrc/attn_sm100.cu): scores, softmax
+and P.V forward; dO.V^T, softmax backward and dS.K backward; the remaining dV = P^T dO
+and dK = dS^T Q are batched GEMMs (batch = sample x head, expressed as coordinate
+offsets into the packed QKV buffer).  Other shapes use the scores GEMM with the softmax
+in its epilogue plus batched GEMMs.  The fp32 score / dP matrices never reach HBM.
+LayerNorm and mean-pool are warp-per-row kernels.  Rows of the executor's [m, S*d] buffers are viewed as [m*S, d] token matrices.
 """
 
 from __future__ import annotations
@@ -61,7 +62,10 @@ class MMTLayer:
         st = lambda: [torch.zeros(T, dtype=torch.float32, device=dev) for _ in range(ex.ell)]
         self.mean1, self.rstd1, self.mean2, self.rstd2 = st(), st(), st(), st()
         z = lambda shape, t=dt: torch.zeros(shape, dtype=t, device=dev)
-        # fused attention softmax (tcgen05 epilogue) when the key row fits TMEM
+        # one-kernel attention (softmax + P.V / softmax-bwd + dS.K) for 64-wide heads and
+        # S in {128..512}; else the scores kernel with the softmax in its epilogue when the
+        # key row fits TMEM; else unfused GEMM + softmax kernels
+        self.flash = S % 128 == 0 and S <= 512 and self.dh == 64 and dt == torch.bfloat16
         self.fused = S <= 512 and S % 32 == 0 and self.dh % 64 == 0 and dt == torch.bfloat16
         self.scores = None if self.fused else z((Z * S, S), torch.float32)
         self.dP = None if self.fused else z((Z * S, S), torch.float32)
@@ -83,6 +87,22 @@ class MMTLayer:
         h1, qkv, P, o_ = self.h1[slot], self.qkv[slot], self.P[slot], self.o_[slot]
         be.layernorm_fwd(h1, self.mean1[slot], self.rstd1[slot], x2d, self._p("ln1_g"), self._p("ln1_b"))
         be.linear_fwd(qkv, h1, self._w("wqkv"), self._p("bqkv"), "none")
+        if self.flash:
+            be.attn_fwd(qkv, P, o_, self.ex.m, S, d, H, self.scale)
+        else:
+            self._attention_fwd(qkv, P, o_)
+        y1 = self.y1[slot]
+        be.linear_fwd(y1, o_, self._w("wo"), self._p("bo"), "none", residual=x2d)
+        h2 = self.h2[slot]
+        be.layernorm_fwd(h2, self.mean2[slot], self.rstd2[slot], y1, self._p("ln2_g"), self._p("ln2_b"))
+        be.linear_fwd(self.f[slot], h2, self._w("w1"), self._p("b1"), "gelu", pre=self.pre1[slot])
+        y2 = self.y2[slot] if self.pool else out.view(T, d)
+        be.linear_fwd(y2, self.f[slot], self._w("w2"), self._p("b2"), "none", residual=y1)
+        if self.pool:
+            be.meanpool_fwd(out, y2, self.ex.m, S, d)
+
+    def _attention_fwd(self, qkv, P, o_):
+        be, S, d, H, dh, T, Z = self.ex.be, self.S, self.d, self.H, self.dh, self.T, self.Z
         # P[z] = softmax(Q_z K_z^T * scale)  (z = sample * H + head)
         spec = _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S)
         if self.fused:
@@ -94,15 +114,6 @@ class MMTLayer:
         # o[z] = P_z V_z  -> head-interleaved columns of o
         be.gemm_batched(o_, d, P, S, Z * S, False, qkv, 3 * d, T, True, S, dh, S,
                         _spec(Z, H, a_m_hi=H * S, a_m_lo=S, b_n0=2 * d, b_n_lo=dh, b_k_hi=S, c_hi=S * d, c_lo=dh))
-        y1 = self.y1[slot]
-        be.linear_fwd(y1, o_, self._w("wo"), self._p("bo"), "none", residual=x2d)
-        h2 = self.h2[slot]
-        be.layernorm_fwd(h2, self.mean2[slot], self.rstd2[slot], y1, self._p("ln2_g"), self._p("ln2_b"))
-        be.linear_fwd(self.f[slot], h2, self._w("w1"), self._p("b1"), "gelu", pre=self.pre1[slot])
-        y2 = self.y2[slot] if self.pool else out.view(T, d)
-        be.linear_fwd(y2, self.f[slot], self._w("w2"), self._p("b2"), "none", residual=y1)
-        if self.pool:
-            be.meanpool_fwd(out, y2, self.ex.m, S, d)
 
     def _wgrad(self, name, bname, dz, xin, accumulate, last):
         ex, be = self.ex, self.ex.be
@@ -138,16 +149,22 @@ class MMTLayer:
         # dV[z] = P_z^T dO_z
         be.gemm_batched(self.dqkv, 3 * d, P, S, Z * S, True, self.do, d, T, True, S, dh, S,
                         _spec(Z, H, a_k_hi=H * S, a_k_lo=S, b_n_lo=dh, b_k_hi=S, c0=2 * d, c_hi=S * 3 * d, c_lo=dh))
-        # dP[z] = dO_z V_z^T ;  dS = scale * P o (dP - rowsum(P o dP))
-        spec = _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=2 * d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S)
-        if self.fused:
-            be.attn_softmax_bwd(self.dS, S, P, S, self.do, d, T, qkv, 3 * d, T, S, S, dh, self.scale, spec)
+        if self.flash:
+            # dS = scale * P o (dO V^T - rowsum(dO o O)) and dQ = dS K in one kernel
+            be.attn_bwd(qkv, P, self.o_[slot], self.do, self.dS, self.dqkv, ex.m, S, d, H, self.scale)
         else:
-            be.gemm_batched(self.dP, S, self.do, d, T, False, qkv, 3 * d, T, False, S, S, dh, spec, out_f32=True)
-            be.softmax_bwd(self.dS, P, self.dP, self.scale)
-        # dQ[z] = dS_z K_z ;  dK[z] = dS_z^T Q_z
-        be.gemm_batched(self.dqkv, 3 * d, self.dS, S, Z * S, False, qkv, 3 * d, T, True, S, dh, S,
-                        _spec(Z, H, a_m_hi=H * S, a_m_lo=S, b_n0=d, b_n_lo=dh, b_k_hi=S, c_hi=S * 3 * d, c_lo=dh))
+            # dP[z] = dO_z V_z^T ;  dS = scale * P o (dP - rowsum(P o dP))
+            spec = _spec(Z, H, a_m_hi=S, a_k_lo=dh, b_n_hi=S, b_k0=2 * d, b_k_lo=dh, c_hi=H * S * S, c_lo=S * S)
+            if self.fused:
+                be.attn_softmax_bwd(self.dS, S, P, S, self.do, d, T, qkv, 3 * d, T, S, S, dh, self.scale, spec)
+            else:
+                be.gemm_batched(self.dP, S, self.do, d, T, False, qkv, 3 * d, T, False, S, S, dh, spec, out_f32=True)
+                be.softmax_bwd(self.dS, P, self.dP, self.scale)
+            # dQ[z] = dS_z K_z
+            be.gemm_batched(self.dqkv, 3 * d, self.dS, S, Z * S, False, qkv, 3 * d, T, True, S, dh, S,
+                            _spec(Z, H, a_m_hi=H * S, a_m_lo=S, b_n0=d, b_n_lo=dh, b_k_hi=S, c_hi=S * 3 * d,
+                                  c_lo=dh))
+        # dK[z] = dS_z^T Q_z
         be.gemm_batched(self.dqkv, 3 * d, self.dS, S, Z * S, True, qkv, 3 * d, T, True, S, dh, S,
                         _spec(Z, H, a_k_hi=H * S, a_k_lo=S, b_n_lo=dh, b_k_hi=S, c0=d, c_hi=S * 3 * d, c_lo=dh))
         be.linear_dgrad(self.dh1, self.dqkv, self._w("wqkv"), None, "none")

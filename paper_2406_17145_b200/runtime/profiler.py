@@ -28,21 +28,48 @@ class _Rec:
     end: torch.cuda.Event
 
 
+GEMM_KINDS = ("fwd", "dgrad", "wgrad")
+# every other kernel-launching backend call, timed for the per-rank busy time
+_OTHER_CALLS = ("colsum", "rowdot_fwd", "rowdot_bwd", "mse_loss", "bce_loss", "ce_loss", "copy_rows",
+                "sgd_step", "embbag_fwd", "embbag_sgd", "interaction_fwd", "interaction_bwd",
+                "layernorm_fwd", "layernorm_bwd", "softmax_fwd", "softmax_bwd", "meanpool_fwd",
+                "meanpool_bwd", "attn_softmax", "attn_softmax_bwd", "gemm_batched", "attn_fwd", "attn_bwd")
+
+
 class TimedBackend(CudaBackend):
+    """CudaBackend with CUDA events around every kernel-launching call (when enabled).
+
+    Dense-operator GEMMs are recorded with their algorithmic FLOPs (the roofline's
+    tensor-bound kernel family); every other call is recorded with 0 FLOPs so that
+    ``summary()['busy_ms']`` is the rank's total kernel time (the pipeline-bubble
+    measure).  Events are recorded on the launching (current) stream.  Callers that
+    want undistorted durations keep the GPU queue ahead of the host (``preload``)."""
+
     def __init__(self, device):
         super().__init__(device)
         self.records: list[_Rec] = []
         self.enabled = True
+        self.external = False  # graph capture: event-record nodes that keep their timestamps
+        for name in _OTHER_CALLS:
+            base = getattr(CudaBackend, name, None)
+            if base is not None:
+                setattr(self, name, self._wrap(name, base))
+
+    def _wrap(self, name, base):
+        def call(*a, **kw):
+            return self._timed(name, 0, 0, 0, lambda: base(self, *a, **kw))
+        return call
 
     def _timed(self, kind, m, n, k, fn):
         if not self.enabled:
             return fn()
-        s = torch.cuda.Event(enable_timing=True)
-        e = torch.cuda.Event(enable_timing=True)
+        s = torch.cuda.Event(enable_timing=True, external=self.external)
+        e = torch.cuda.Event(enable_timing=True, external=self.external)
         s.record()
-        fn()
+        r = fn()
         e.record()
         self.records.append(_Rec(kind, 2.0 * m * n * k, m, n, k, s, e))
+        return r
 
     def linear_fwd(self, y, x, w, bias, act, residual=None, pre=None):
         self._timed("fwd", x.shape[0], w.shape[0], x.shape[1],
@@ -61,14 +88,29 @@ class TimedBackend(CudaBackend):
                     lambda: super(TimedBackend, self).linear_wgrad_sgd(master, shadow, grad, dy, x, lr,
                                                                        accumulate, store_grad))
 
+    @staticmethod
+    def preload(host_seconds: float, sm_hz: float = 1.965e9) -> None:
+        """Queue a GPU sleep longer than the host's enqueue time of what follows, so the
+        following launches run back to back and each event pair brackets only its kernel
+        (otherwise a host slower than the GPU stretches every measured duration)."""
+        torch.cuda._sleep(int(max(host_seconds, 1e-3) * 1.5 * sm_hz))
+
     def summary(self) -> dict:
-        """Aggregate FLOPs and device time of the recorded GEMM launches (sync first)."""
+        """GEMM FLOPs / device time (dense-operator GEMMs) and the total kernel time of
+        every recorded call (``busy_ms``); synchronises first."""
         torch.cuda.synchronize()
-        tot_f = tot_ms = 0.0
+        tot_f = tot_ms = busy = 0.0
         by_kind: dict[str, list[float]] = {}
         by_shape: dict[tuple, list[float]] = {}
+        other: dict[str, list[float]] = {}
         for r in self.records:
             ms = r.start.elapsed_time(r.end)
+            busy += ms
+            if r.kind not in GEMM_KINDS:
+                o = other.setdefault(r.kind, [0.0, 0])
+                o[0] += ms
+                o[1] += 1
+                continue
             tot_f += r.flops
             tot_ms += ms
             agg = by_kind.setdefault(r.kind, [0.0, 0.0, 0])
@@ -80,12 +122,14 @@ class TimedBackend(CudaBackend):
             sh[1] += ms
             sh[2] += 1
         return {
-            "launches": len(self.records),
+            "launches": sum(v[2] for v in by_kind.values()),
             "flops": tot_f,
             "ms": tot_ms,
+            "busy_ms": busy,
             "tflops": (tot_f / (tot_ms * 1e-3) / 1e12) if tot_ms > 0 else 0.0,
             "by_kind": {k: {"launches": v[2], "tflops": v[0] / (v[1] * 1e-3) / 1e12 if v[1] else 0.0,
                             "ms": v[1]} for k, v in by_kind.items()},
+            "other_ms": {k: {"launches": v[1], "ms": v[0]} for k, v in sorted(other.items())},
             "by_shape": {f"{k[0]}:{k[1]}x{k[2]}x{k[3]}": {"launches": v[2], "avg_us": 1e3 * v[1] / v[2],
                                                            "tflops": v[0] / (v[1] * 1e-3) / 1e12 if v[1] else 0.0}
                          for k, v in sorted(by_shape.items())},
@@ -155,4 +199,52 @@ def profile_dense(din: int, dout: int, act: str, batches, device, dtype=torch.bf
         out["b"].append(int(b))
         out["fwd_ms"].append(f / 1e3)
         out["bwd_ms"].append(bwt / 1e3)
+    return out
+
+
+class _LayerHost:
+    """The Executor attributes an ``MMTLayer`` reads, for profiling one layer alone
+    (single stage, no DP: the fused wgrad+SGD production path, one ring slot)."""
+
+    def __init__(self, be, m: int, spec, device):
+        from .mmt import mmt_params
+
+        self.be, self.m, self.dev = be, m, device
+        self.dtype, self.ell = torch.bfloat16, 1
+        self.fuse, self.lr, self.keep_grads, self.d, self.tp = True, 0.0, False, 1, None
+        self._ar_handles = []
+        params = mmt_params(spec, 0, 0)
+        self.P = {(0, n): t.to(device) for n, t in params}
+        self.G = {(0, n): torch.zeros_like(t, device=device) for n, t in params}
+        self.W = {(0, n): t.to(device, torch.bfloat16) for n, t in params}
+        self.shadow = True
+
+    def _ring(self, shape, dtype=None):
+        return [torch.zeros(shape, dtype=dtype or self.dtype, device=self.dev)]
+
+
+def profile_mmt_layer(S: int, d: int, H: int, ffn: int, pool: bool, batches, device, reps: int = 5) -> dict:
+    """fw and bw milliseconds of one MMT encoder layer (runtime.mmt.MMTLayer, the production
+    kernels) at each per-device micro-batch size in ``batches`` (samples of S tokens)."""
+    from ..workloads import LayerSpec
+    from .mmt import MMTLayer
+
+    be = CudaBackend(device)
+    spec = LayerSpec("mmt_layer", S * d, d if pool else S * d, extra=(S, d, H, ffn, pool))
+    out = {"b": [], "fwd_ms": [], "bwd_ms": []}
+    for b in batches:
+        host = _LayerHost(be, b, spec, device)
+        layer = MMTLayer(host, 0, spec)
+        x = torch.randn(b * S, d, device=device).to(torch.bfloat16)
+        y = torch.empty(b, spec.out_dim, device=device, dtype=torch.bfloat16)
+        dz = (0.01 * torch.randn(b, spec.out_dim, device=device)).to(torch.bfloat16)
+        dx = torch.empty(b * S, d, device=device, dtype=torch.bfloat16)
+        f = _time_us(lambda: layer.forward(x, y, 0), reps)
+        layer.forward(x, y, 0)
+        bwt = _time_us(lambda: layer.backward(dz, x, dx, 0, False, True), reps)
+        out["b"].append(int(b))
+        out["fwd_ms"].append(f / 1e3)
+        out["bwd_ms"].append(bwt / 1e3)
+        del layer, host
+        torch.cuda.empty_cache()
     return out

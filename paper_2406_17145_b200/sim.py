@@ -113,12 +113,23 @@ def simulate(
     durations: Callable[[int, str], float] | None = None,
     weight_multiplier: float = DEFAULT_WEIGHT_MULTIPLIER,
     sync_epilogue: bool = False,
+    op_granular: bool = False,
+    optimizer_bytes_per_param_byte: float = 0.0,
+    hbm_bytes_per_ms: float = 6.5395e9,
 ) -> SimReport:
     """Simulate one iteration of a configured StageGraph.
 
     Task durations: ``durations(stage_id, direction)`` if given, else the sum of
     the stage ops' fwd/bwd cost curves at b/d.  Edge delays use ``comm_time``
     over the cluster's inter-stage bandwidth (zero-byte edges are free).
+
+    ``op_granular`` (runtime twin, off for the SPEC semantics): a task runs its ops in
+    the executor's order (topological for fw, reversed for bw) and each op waits only for
+    its own remote inputs -- a producer's output leaves when the producing op finishes,
+    not when its whole task does (the B200 executor posts receives up front, waits at the
+    consuming op and ships pieces as soon as they are final, runtime/executor.py).
+    ``optimizer_bytes_per_param_byte`` adds, with ``sync_epilogue``, the unfused optimizer
+    pass a DP stage runs after its all-reduce (HBM-bound, ``hbm_bytes_per_ms``).
     """
     cg = _graph_of(g) if g is not None else None
     B = s.mini_batch
@@ -155,6 +166,26 @@ def simulate(
     times: dict[tuple[int, str, int], tuple[float, float]] = {}
     remaining = sum(len(st.schedule) for st in s.stages)
 
+    # op-granular twin: per-op order / costs and the op-level finish times of every task
+    op_fin: dict[tuple[int, str, int], dict[int, float]] = {}
+    if op_granular:
+        if cg is None:
+            raise ValueError("op_granular simulation needs the computation graph")
+        owner = {o: st.id for st in s.stages for o in st.op_ids}
+        # stage edges without operator data still order whole tasks (token messages)
+        data_pairs = {(owner[u], owner[v]) for u, v in cg.edges
+                      if u in owner and v in owner and owner[u] != owner[v]}
+        order = {}
+        costs = {}
+        for st in s.stages:
+            ops = [o for o in cg.topo_order if o in st.op_ids]
+            order[(st.id, "fw")] = ops
+            order[(st.id, "bw")] = ops[::-1]
+            per = st.micro_batch // st.dp_degree
+            for d in ("fw", "bw"):
+                costs[(st.id, d)] = {o: (cg.by_id[o].fwd_cost if d == "fw" else cg.by_id[o].bwd_cost).evaluate(per)
+                                     for o in ops}
+
     def ready_time(sid: int, direction: str, j: int):
         st = s.by_id[sid]
         t = free_at[sid]
@@ -176,16 +207,54 @@ def simulate(
                     t = max(t, times[key][1] + delay((sid, y), by))
         return t
 
+    def op_timeline(sid: int, direction: str, j: int):
+        """(start, end, per-op finish) of a task whose producers are all simulated."""
+        st = s.by_id[sid]
+        for nb in (preds[sid] if direction == "fw" else succs[sid]):
+            bn = s.by_id[nb].micro_batch
+            for i in covering_tasks(j, st.micro_batch, bn):
+                if (nb, direction, i) not in times:
+                    return None
+        t = free_at[sid]
+        t0 = None
+        for nb in (preds[sid] if direction == "fw" else succs[sid]):
+            if ((nb, sid) if direction == "fw" else (sid, nb)) in data_pairs:
+                continue
+            for i in covering_tasks(j, st.micro_batch, s.by_id[nb].micro_batch):
+                t = max(t, times[(nb, direction, i)][1])
+        fin = {}
+        for o in order[(sid, direction)]:
+            remote = ([u for u in cg.predecessors(o) if owner.get(u, sid) != sid] if direction == "fw"
+                      else [v for v in cg.successors(o) if owner.get(v, sid) != sid])
+            for u in remote:
+                nb = owner[u]
+                bn = s.by_id[nb].micro_batch
+                e = (nb, sid) if direction == "fw" else (sid, nb)
+                for i in covering_tasks(j, st.micro_batch, bn):
+                    t = max(t, op_fin[(nb, direction, i)][u] + delay(e, bn))
+            if t0 is None:
+                t0 = t  # the task starts with its first op
+            t += costs[(sid, direction)][o]
+            fin[o] = t
+        return (t if t0 is None else t0), t, fin
+
     while remaining:
         progressed = False
         for st in s.stages:  # ascending stage id
             sid = st.id
             while pos[sid] < len(st.schedule):
                 task = st.schedule[pos[sid]]
-                t0 = ready_time(sid, task.direction, task.index)
-                if t0 is None:
-                    break
-                t1 = t0 + dcache[(sid, task.direction)]
+                if op_granular:
+                    tl = op_timeline(sid, task.direction, task.index)
+                    if tl is None:
+                        break
+                    t0, t1, fin = tl
+                    op_fin[(sid, task.direction, task.index)] = fin
+                else:
+                    t0 = ready_time(sid, task.direction, task.index)
+                    if t0 is None:
+                        break
+                    t1 = t0 + dcache[(sid, task.direction)]
                 times[(sid, task.direction, task.index)] = (t0, t1)
                 free_at[sid] = t1
                 pos[sid] += 1
@@ -205,7 +274,8 @@ def simulate(
             if st.dp_degree > 1:
                 last = max(t1 for (sid, _, _), (_, t1) in times.items() if sid == st.id)
                 params = sum(cg.by_id[o].param_bytes for o in st.op_ids if o in cg.by_id)
-                iteration = max(iteration, last + dp_sync_time(params, st.dp_degree, cluster.intra_bw))
+                opt = optimizer_bytes_per_param_byte * params / hbm_bytes_per_ms
+                iteration = max(iteration, last + dp_sync_time(params, st.dp_degree, cluster.intra_bw) + opt)
     busy = {st.id: sum(dcache[(st.id, t.direction)] for t in st.schedule) for st in s.stages}
     idle = {sid: iteration - b for sid, b in busy.items()}
     peak: dict[int, int] = {}

@@ -74,8 +74,24 @@ def dense_profile_key(spec: "LayerSpec") -> str:
     return f"dense:{spec.in_dim}x{spec.out_dim}:{spec.act}:{'nodgrad' if spec.data_key else 'dgrad'}"
 
 
+def mmt_profile_key(spec: "LayerSpec") -> str:
+    """Profile key of an MMT encoder layer (tools/profile_costs.py mmt)."""
+    S, d, H, ffn, pool = spec.extra
+    return f"mmt:{S}x{d}x{H}x{ffn}:{'pool' if pool else 'seq'}"
+
+
+def profile_key(spec: "LayerSpec | None") -> str | None:
+    if spec is None:
+        return None
+    if spec.kind == "dense":
+        return dense_profile_key(spec)
+    if spec.kind == "mmt_layer":
+        return mmt_profile_key(spec)
+    return None
+
+
 def with_measured_curves(wl: "Workload", profile: dict | str | None = None) -> tuple["Workload", int]:
-    """Replace the analytic fw/bw curves of bf16 dense operators by measured B200 tables.
+    """Replace the analytic fw/bw curves of bf16 dense / MMT-layer operators by measured B200 tables.
 
     ``profile`` is the JSON written by tools/profile_costs.py (default: the committed
     ``profiles/cost_curves_b200.json``): ``curves[key] = {b: [...], fwd_ms: [...], bwd_ms:
@@ -94,7 +110,8 @@ def with_measured_curves(wl: "Workload", profile: dict | str | None = None) -> t
     ops, n = [], 0
     for op in wl.graph.ops:
         spec = wl.layers.get(op.id)
-        c = curves.get(dense_profile_key(spec)) if spec is not None and spec.kind == "dense" else None
+        key = profile_key(spec)
+        c = curves.get(key) if key else None
         if c:
             op = replace(op, fwd_cost=CostCurve.table(dict(zip(c["b"], c["fwd_ms"]))),
                          bwd_cost=CostCurve.table(dict(zip(c["b"], c["bwd_ms"]))))
@@ -106,9 +123,18 @@ def with_measured_curves(wl: "Workload", profile: dict | str | None = None) -> t
                    meta={**wl.meta, "costs": f"measured B200 tables for {n} ops"}), n
 
 
+# NCCL all-reduce bus bandwidth of 2.4 GB fp32 gradients through libgpp_b200 on one B200
+# box (tools/bench_allreduce.py, profiles/allreduce_b200.jsonl): 598 GB/s at 2 GPUs, 660 GB/s
+# at 4; the 8-GPU value is assumed equal to the 4-GPU one (not measured: gpurun gives <= 4).
+DP_BUSBW = {2: 5.98e8, 4: 6.6e8}
+
+
 def b200_cluster(n: int, mem_bytes: float = 180e9) -> DeviceCluster:
-    """NVLink 5 / NVSwitch box: 900 GB/s per direction = 9e8 bytes/ms, ~10 us latency."""
-    return DeviceCluster(num_devices=n, mem_per_device=mem_bytes, intra_bw=9e8, inter_bw=9e8, link_latency=0.01)
+    """NVLink 5 / NVSwitch box: P2P at the 900 GB/s per-direction link rate (9e8 bytes/ms,
+    ~10 us latency); the DP-sync bandwidth (``intra_bw``, priced by cost.dp_sync_time) is
+    the measured NCCL all-reduce bus bandwidth."""
+    dp = DP_BUSBW.get(n, DP_BUSBW[4]) if n > 1 else 9e8
+    return DeviceCluster(num_devices=n, mem_per_device=mem_bytes, intra_bw=dp, inter_bw=9e8, link_latency=0.01)
 
 
 def _gemm_curve(flops_per_sample: float, launches: int, fp32: bool = False) -> CostCurve:

@@ -36,23 +36,23 @@ def _free_port():
     return p
 
 
-def _stage_graph(layout, B, wl=None):
-    """layout: list of (op ids, micro_batch, devices)."""
+def _stage_graph(layout, B, wl=None, extra_edges=()):
+    """layout: list of (op ids, micro_batch, devices); extra_edges: data-less stage edges."""
     wl = wl or W.toy(B=B)
     stages = [M.Stage(i, frozenset(ops), b, frozenset(devs)) for i, (ops, b, devs) in enumerate(layout)]
     part = [st.op_ids for st in stages]
-    edges = M.induced_stage_edges(wl.graph, part)
+    edges = set(M.induced_stage_edges(wl.graph, part)) | set(extra_edges)
     sg = S.schedule_stage_graph(M.StageGraph(stages, edges, B))
     assert M.validate_strategy(wl.graph, M.DeviceCluster(8, 1e12, 1, 1), sg) == []
     return wl, sg
 
 
-def _worker(rank, world, port, layout, B, outdir, wl=None):
+def _worker(rank, world, port, layout, B, outdir, wl=None, extra_edges=()):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        wl, sg = _stage_graph(layout, B, wl)
+        wl, sg = _stage_graph(layout, B, wl, extra_edges)
         ex = Executor(wl, sg, rank, world, TorchBackend(), lr=LR, keep_grads=True)
         res = {"loss": [], "grads": []}
         for step in range(STEPS):
@@ -67,9 +67,9 @@ def _worker(rank, world, port, layout, B, outdir, wl=None):
         dist.destroy_process_group()
 
 
-def _run(layout, B, world, wl=None):
+def _run(layout, B, world, wl=None, extra_edges=()):
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), layout, B, d, wl), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), layout, B, d, wl, extra_edges), nprocs=world, join=True)
         outs = [torch.load(os.path.join(d, f"rank{r}.pt")) for r in range(world)]
     wl = wl or W.toy(B=B)
     ref = ReferenceModel(wl)
@@ -95,6 +95,24 @@ def test_two_stage_gpp_gloo():
 def test_unequal_microbatch_and_dp_gloo():
     # tower A b=16 on rank 0; tower B b=32 as a DP-2 stage; tail b=8 on rank 3
     _run([(TOWER_A, 16, [0]), (TOWER_B, 32, [1, 2]), (TAIL, 8, [3])], 64, 4)
+
+
+def test_sequential_chain_token_edges_gloo():
+    """SPP-shaped layout: tower A -> tower B -> tail as a stage chain.  The chain edge
+    A -> B carries no operator data (the towers are independent) but still orders the
+    tasks, so the executor realises it with token messages; results
+    still equal the reference."""
+    layout = [(TOWER_A, 16, [0]), (TOWER_B, 16, [1]), (TAIL, 16, [2])]
+    _run(layout, 64, 3, extra_edges=[(0, 1)])
+
+
+def test_token_pieces_only_on_dataless_edges():
+    wl, sg = _stage_graph([(TOWER_A, 16, [0]), (TOWER_B, 32, [1]), (TAIL, 16, [2])], 64, extra_edges=[(0, 1)])
+    exs = [Executor(wl, sg, r, 3, TorchBackend(), use_dist=False) for r in range(3)]
+    # stage 0 -> stage 1 (b 16 -> 32): two producer tasks feed each consumer task
+    assert [len(exs[1].tok_in[j]) for j in range(2)] == [2, 2]
+    assert [len(exs[0].tok_out[j]) for j in range(4)] == [1, 1, 1, 1]
+    assert all(not v for v in exs[2].tok_in.values()) and all(not v for v in exs[1].tok_out.values())
 
 
 def test_single_rank_matches_reference():

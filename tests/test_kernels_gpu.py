@@ -428,3 +428,36 @@ def test_fused_attention_softmax(cuda_lib, m, S, d, H):
     tb.attn_softmax_bwd(dSr, S, P.cpu(), S, do.cpu(), d, T, qkv.cpu(), 3 * d, T, S, S, dh, scale, spec_b)
     torch.cuda.synchronize()
     assert _rel(dS.cpu(), dSr) < 2e-2
+
+
+@pytest.mark.parametrize("m,S,d,H", [(2, 128, 128, 2), (3, 256, 256, 4), (2, 384, 256, 4), (2, 512, 1024, 16)])
+def test_fused_attention_fwd_bwd(cuda_lib, m, S, d, H):
+    """One-kernel attention (csrc/attn_sm100.cu) vs the torch restatement in
+    oracle/torch_backend.py on the MMT packed-QKV layout: P and O forward, dS and the Q
+    block of dQKV backward (bf16 operands / outputs, fp32 accumulation)."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle.torch_backend import TorchBackend
+    g = torch.Generator(device="cuda").manual_seed(7 * S + d)
+    T, Z = m * S, m * H
+    scale = 64 ** -0.5
+    qkv = torch.randn(T, 3 * d, device="cuda", generator=g).bfloat16()
+    do = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    P = torch.empty(Z * S, S, device="cuda", dtype=torch.bfloat16)
+    o = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+    cuda_lib.attn_fwd(qkv, P, o, m, S, d, H, scale)
+    tb = TorchBackend("cpu")
+    Pr, orf = torch.zeros(Z * S, S, dtype=torch.bfloat16), torch.zeros(T, d, dtype=torch.bfloat16)
+    tb.attn_fwd(qkv.cpu(), Pr, orf, m, S, d, H, scale)
+    torch.cuda.synchronize()
+    assert _rel(P.cpu(), Pr) < 1e-2
+    assert _rel(o.cpu(), orf) < 1e-2
+    dS = torch.empty_like(P)
+    dqkv = torch.full((T, 3 * d), 7.0, device="cuda", dtype=torch.bfloat16)
+    cuda_lib.attn_bwd(qkv, P, o, do, dS, dqkv, m, S, d, H, scale)
+    dSr, dqr = torch.zeros(Z * S, S, dtype=torch.bfloat16), torch.zeros(T, 3 * d, dtype=torch.bfloat16)
+    tb.attn_bwd(qkv.cpu(), P.cpu(), o.cpu(), do.cpu(), dSr, dqr, m, S, d, H, scale)
+    torch.cuda.synchronize()
+    assert _rel(dS.cpu(), dSr) < 2e-2
+    assert _rel(dqkv[:, :d].cpu(), dqr[:, :d]) < 2e-2
+    assert (dqkv[:, d:] == 7.0).all(), "attn_bwd wrote outside the Q block of dqkv"

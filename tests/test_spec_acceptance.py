@@ -299,11 +299,16 @@ def test_branch_scaling_ratio_nondecreasing():
 # ---------------------------------------------------------------- search cost (acceptance 8)
 def test_search_states_grow_about_linearly_in_branches():
     """DP states reported by the optimizer, fixed 8 devices and b, 4-layer towers: doubling
-    the branch count at most ~doubles the states (measured x2.3 / x2.2)."""
+    the branch count at most ~doubles the states (measured x2.3 / x2.2).  The
+    cluster is the nominal 900 GB/s NVLink box: the pruning (hence the state count) depends
+    on the bandwidths, and this checks the search, not the B200 calibration."""
+    from paper_2406_17145_b200.model import DeviceCluster
+
     states = {}
     for n in (4, 8, 16):
         wl = W.candle(B=1024, towers=n)
-        st = P.optimize(wl.graph, W.b200_cluster(8), 1024, P.PartitionOptions(micro_batches=(128,)))
+        cl = DeviceCluster(num_devices=8, mem_per_device=180e9, intra_bw=9e8, inter_bw=9e8, link_latency=0.01)
+        st = P.optimize(wl.graph, cl, 1024, P.PartitionOptions(micro_batches=(128,)))
         assert st.probes > 0
         states[n] = st.dp_states
     assert states[8] / states[4] <= 2.5 and states[16] / states[8] <= 2.5, states
