@@ -49,7 +49,7 @@ class ReferenceModel:
             if spec.kind == "dense":
                 w = _round(P[(o, "w")], self.bf16)
                 z = x @ w.t() + P[(o, "b")]
-                y = torch.relu(z) if spec.act == "relu" else (torch.nn.functional.gelu(z) if spec.act == "gelu" else z)
+                y = torch.relu(z) if spec.act == "relu" else (torch.nn.functional.gelu(z, approximate="tanh") if spec.act == "gelu" else z)
                 out[o] = _round(y, self.bf16)
             elif spec.kind == "concat":
                 out[o] = torch.cat([out[u] for u in g.predecessors(o)], dim=1)
@@ -101,7 +101,7 @@ class ReferenceModel:
         att = R((pr @ v).transpose(1, 2).reshape(B * S, d))
         y1 = R(att @ W("wo").t() + P[(o, "bo")] + x)
         h2 = R(torch.nn.functional.layer_norm(y1, (d,), P[(o, "ln2_g")], P[(o, "ln2_b")], eps=1e-5))
-        f = R(torch.nn.functional.gelu(h2 @ W("w1").t() + P[(o, "b1")]))
+        f = R(torch.nn.functional.gelu(h2 @ W("w1").t() + P[(o, "b1")], approximate="tanh"))
         y2 = R(f @ W("w2").t() + P[(o, "b2")] + y1)
         if pool:
             return R(y2.reshape(B, S, d).mean(1))

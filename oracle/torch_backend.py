@@ -15,7 +15,7 @@ def _act(z, act):
     if act == "relu":
         return torch.relu(z)
     if act == "gelu":
-        return torch.nn.functional.gelu(z)
+        return torch.nn.functional.gelu(z, approximate="tanh")
     return z
 
 
@@ -23,10 +23,10 @@ def _dact(saved, act):
     s = saved.float()
     if act == "relu":
         return (s > 0).float()
-    if act == "gelu":
-        cdf = 0.5 * (1.0 + torch.erf(s / math.sqrt(2.0)))
-        pdf = torch.exp(-0.5 * s * s) / math.sqrt(2.0 * math.pi)
-        return cdf + s * pdf
+    if act == "gelu":  # d/dx of x * sigmoid(2u), u = sqrt(2/pi) (x + 0.044715 x^3)
+        c = math.sqrt(2.0 / math.pi)
+        sg = torch.sigmoid(2.0 * c * (s + 0.044715 * s ** 3))
+        return sg + s * sg * (1.0 - sg) * 2.0 * c * (1.0 + 3.0 * 0.044715 * s * s)
     return torch.ones_like(s)
 
 

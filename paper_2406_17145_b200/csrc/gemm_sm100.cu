@@ -530,6 +530,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 
+// ---- aux tiles by TMA (bf16 epilogues with a residual / act'-saved operand) ----
+#define AUX_TMA_EPI(E) ((E) == EPI_FWD || (E) == EPI_DGRAD)
+
+// this lane's row of a 64B-swizzled [32 x 32] bf16 tile -> 32 floats (conflict-free)
+__device__ __forceinline__ void read_aux_tile(const uint8_t* tile, int lane, float (&a)[32]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint4 r = *reinterpret_cast<const uint4*>(tile + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
+    const uint32_t* u = reinterpret_cast<const uint32_t*>(&r);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[t]));
+      a[8 * j + 2 * t] = x.x;
+      a[8 * j + 2 * t + 1] = x.y;
+    }
+  }
+}
+
 // ------------------------------------------------------------------------
 // Persistent CTA-pair GEMM: cluster (2,1,1), tcgen05.mma.cta_group::2 with
 // M = 256 (128 rows per CTA) x N = BN, TMEM accumulators double-buffered
@@ -543,7 +561,8 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
                         const __grid_constant__ CUtensorMap tma_b, EpiParams ep, int M, int N,
-                        int K, int k_splits, int m_fast) {
+                        int K, int k_splits, int m_fast, const __grid_constant__ CUtensorMap tma_aux,
+                        int aux_tma) {
   constexpr int A_BYTES = BM * BK * 2;            // 16 KB: this CTA's 128 rows of A
   constexpr int B_BYTES = (BN / 2) * BK * 2;      // this CTA's BN/2 rows of B
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -559,6 +578,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   uint64_t* tempty_bar = tfull_bar + 2;           // [2] (leader's copy is the live one)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   float* epi_stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);  // per warp 32 x 36 (x2 SGD)
+  // bf16 epilogues: per-warp double-buffered 64B-swizzled 32 x 32 aux tiles filled by TMA
+  uint64_t* aux_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + 512);
+  uint8_t* aux_tiles = smem + STAGES * STAGE_BYTES + 1024;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -583,6 +605,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 2 * PAIR_EPI_WARPS);
     }
+    if (AUX_TMA_EPI(EPI))
+      for (int i = 0; i < 2 * PAIR_EPI_WARPS; ++i) mbar_init(&aux_bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -669,7 +693,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     // ---------------- epilogue (warps 2..5 of both CTAs) ----------------
     const int q = warp & 3;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
-    uint32_t lt = 0;
+    uint32_t lt = 0, aux_it = 0;
     for (int u = cluster_id; u < num_units; u += num_clusters, ++lt) {
       const int tile = u / k_splits;
       EpiParams epu = ep;
@@ -706,6 +730,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
           continue;
         }
       }
+      // The aux tile (residual / act'-saved) of a bf16 epilogue arrives by TMA, 32 x 32 per
+      // chunk, one chunk ahead, into this warp's double buffer (row-per-lane global loads
+      // touched 32 lines per instruction and exposed a DRAM latency per chunk).
+      uint8_t* my_aux = aux_tiles + (warp - 2) * 4096;
+      uint64_t* my_bar = aux_bar + 2 * (warp - 2);
+      auto issue_aux = [&](int c) {
+        if (lane == 0) {
+          const uint32_t b = aux_it & 1;
+          mbar_expect_tx(&my_bar[b], 2048);
+          tma_load_2d(my_aux + b * 2048, &tma_aux, &my_bar[b], n_blk * BN + c * 32, row0);
+        }
+      };
+      if (AUX_TMA_EPI(EPI) && aux_tma) issue_aux(group);
       mbar_wait(&tfull_bar[acc], aph);
       tc_fence_after();
 #pragma unroll 1
@@ -717,7 +754,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
                                       n_blk * BN + c * 32, M, N, lane);
         } else {
           float aux[32];
-          epilogue_aux<EPI>(epu, row, n_blk * BN + c * 32, M, N, aux);
+          if (AUX_TMA_EPI(EPI) && aux_tma) {
+            const uint32_t b = aux_it & 1, ph = (aux_it >> 1) & 1;
+            ++aux_it;
+            if (c + GSTEP < BN / 32) issue_aux(c + GSTEP);  // into the other buffer (consumed)
+            mbar_wait(&my_bar[b], ph);
+            read_aux_tile(my_aux + b * 2048, lane, aux);
+            __syncwarp();  // every lane done with buffer b before it is refilled
+          } else {
+            epilogue_aux<EPI>(epu, row, n_blk * BN + c * 32, M, N, aux);
+          }
           tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
           epilogue_chunk<EPI>(epu, v, aux, row, n_blk * BN + c * 32, M, N);
         }
@@ -764,27 +810,27 @@ static EncodeTiledFn encode_fn() {
 struct MapKey {
   const void* ptr;
   int64_t inner, outer, ld;
-  int box_inner, box_outer;
+  int box_inner, box_outer, swz;
   bool operator==(const MapKey& o) const {
     return ptr == o.ptr && inner == o.inner && outer == o.outer && ld == o.ld &&
-           box_inner == o.box_inner && box_outer == o.box_outer;
+           box_inner == o.box_inner && box_outer == o.box_outer && swz == o.swz;
   }
 };
 struct MapKeyHash {
   size_t operator()(const MapKey& k) const {
     size_t h = std::hash<const void*>()(k.ptr);
     h ^= std::hash<int64_t>()(k.inner * 1315423911LL + k.outer) + 0x9e3779b9 + (h << 6) + (h >> 2);
-    h ^= std::hash<int64_t>()(k.ld * 31 + k.box_inner * 7 + k.box_outer) + (h << 6) + (h >> 2);
+    h ^= std::hash<int64_t>()(k.ld * 31 + k.box_inner * 7 + k.box_outer * 3 + k.swz) + (h << 6) + (h >> 2);
     return h;
   }
 };
 
 // 2-D bf16 tensor map over a row-major buffer: `outer` rows of `inner` elements, row pitch ld.
 static int make_map(CUtensorMap* out, const void* ptr, int64_t inner, int64_t outer, int64_t ld,
-                    int box_inner, int box_outer) {
+                    int box_inner, int box_outer, int swizzle_bytes = 128) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  MapKey key{ptr, inner, outer, ld, box_inner, box_outer};
+  MapKey key{ptr, inner, outer, ld, box_inner, box_outer, swizzle_bytes};
   {
     std::lock_guard<std::mutex> g(mu);
     auto it = cache.find(key);
@@ -803,7 +849,8 @@ static int make_map(CUtensorMap* out, const void* ptr, int64_t inner, int64_t ou
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed with code " + std::to_string(static_cast<int>(r)));
@@ -859,6 +906,14 @@ static int launch_tc(const void* a, int64_t lda, const void* b, int64_t ldb, con
 }
 
 
+static bool aux_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GPP_AUX_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static bool pair_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -905,7 +960,16 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   // fp32 epilogues stage through smem (fused SGD double-buffers its master chunks);
   // the bf16 epilogues write straight from registers and give that space to the ring
   constexpr int EPI_BUFS = EPI == EPI_SGD ? 2 : (EPI == EPI_F32 ? 1 : 0);
-  constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + PAIR_EPI_WARPS * 32 * STAGE_LD * 4 * EPI_BUFS;
+  constexpr int SMEM = AUX_TMA_EPI(EPI) ? STAGES * STAGE_BYTES + 1024 + 1024 + PAIR_EPI_WARPS * 4096
+                                        : STAGES * STAGE_BYTES + 1024 + 256 + PAIR_EPI_WARPS * 32 * STAGE_LD * 4 * EPI_BUFS;
+  CUtensorMap mx = ma;
+  int aux_tma = 0;
+  if constexpr (AUX_TMA_EPI(EPI)) {
+    const bool need = (EPI == EPI_FWD && ep.aux != nullptr) || (EPI == EPI_DGRAD && ep.act != GPP_ACT_NONE);
+    aux_tma = need && k_splits == 1 && (reinterpret_cast<uintptr_t>(ep.aux) & 15) == 0 && ep.ldaux % 8 == 0 &&
+              aux_tma_enabled();
+    if (aux_tma && (rc = make_map(&mx, ep.aux, N, M, ep.ldaux, 32, 32, 64))) return rc;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI>,
@@ -917,7 +981,8 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   if (units < clusters) clusters = units;
   gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(2 * clusters),
                                                      PAIR_THREADS, SMEM, stream>>>(
-      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits, M < N ? 1 : 0);
+      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits, M < N ? 1 : 0, mx,
+      aux_tma);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("gemm_tc_pair launch: ") + cudaGetErrorString(e));
