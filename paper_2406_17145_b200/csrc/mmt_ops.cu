@@ -132,9 +132,78 @@ __global__ void ln_bwd_final_kernel(float* __restrict__ dgamma, float* __restric
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= 2 * D) return;
   float t = 0.f;
+#pragma unroll 8
   for (int k = 0; k < nblocks; ++k) t += part[static_cast<int64_t>(k) * 2 * D + c];
   float* o = c < D ? dgamma + c : dbeta + (c - D);
   *o = accumulate ? *o + t : t;
+}
+
+// ---- 16-byte vectorised LayerNorm forward (D % 256 == 0): lane owns 8-element chunks
+// lane + 32 i, so every warp instruction moves 512 contiguous bytes of a row --------------
+__device__ __forceinline__ void unpack8(const uint4& r, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const float2 x = __bfloat1622float2(h[t]);
+    f[2 * t] = x.x;
+    f[2 * t + 1] = x.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  uint4 r;
+  uint32_t* u = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * t], f[2 * t + 1]);
+    u[t] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  return r;
+}
+__device__ __forceinline__ void load8f(const float* p, float* f) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+template <int PER>
+__global__ void __launch_bounds__(256) ln_fwd_vec_kernel(bf16* __restrict__ y, float* __restrict__ mean,
+                                                         float* __restrict__ rstd, const bf16* __restrict__ x,
+                                                         const float* __restrict__ g, const float* __restrict__ b,
+                                                         int64_t T, int D, float eps) {
+  constexpr int NV = PER / 8;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= T) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + r * D);
+  uint4 raw[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) raw[i] = __ldg(xr + lane + 32 * i);
+  float v[PER];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) unpack8(raw[i], v + 8 * i);
+  float sm = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) sm += v[i];
+  const float mu = wsum(sm) / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) q += (v[i] - mu) * (v[i] - mu);
+  const float rs = rsqrtf(wsum(q) / D + eps);
+  uint4* yr = reinterpret_cast<uint4*>(y + r * D);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = 8 * (lane + 32 * i);
+    float gg[8], bb[8], o[8];
+    load8f(g + c, gg);
+    load8f(b + c, bb);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) o[t] = (v[8 * i + t] - mu) * rs * gg[t] + bb[t];
+    yr[lane + 32 * i] = pack8(o);
+  }
+  if (lane == 0) {
+    mean[r] = mu;
+    rstd[r] = rs;
+  }
 }
 
 // ---- attention softmax: P = softmax(s) row-wise (fp32 scores, already scaled) ------------
@@ -253,6 +322,8 @@ float* ln_scratch(size_t floats) {
 using namespace gpp;
 
 
+static bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 extern "C" {
 
 int gpp_layernorm_fwd(void* y, float* mean, float* rstd, const void* x, const float* gamma,
@@ -261,11 +332,12 @@ int gpp_layernorm_fwd(void* y, float* mean, float* rstd, const void* x, const fl
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const unsigned grid = static_cast<unsigned>((T + 7) / 8);
   const int d = static_cast<int>(D);
+  GPP_ARG_CHECK(D == 128 || (a16(y) && a16(x) && a16(gamma) && a16(beta)), "16-byte aligned rows / affine params");
   switch (D) {
     case 128: ln_fwd_kernel<4><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
-    case 256: ln_fwd_kernel<8><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
-    case 512: ln_fwd_kernel<16><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
-    case 1024: ln_fwd_kernel<32><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
+    case 256: ln_fwd_vec_kernel<8><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
+    case 512: ln_fwd_vec_kernel<16><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
+    case 1024: ln_fwd_vec_kernel<32><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
     default: set_error("layernorm: D must be 128/256/512/1024"); return GPP_ERR_UNSUPPORTED;
   }
   GPP_LAUNCH_CHECK();
