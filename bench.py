@@ -223,12 +223,17 @@ def _time_arm(wl, world, rank, dev, mode, args, clocks=True):
         sampler.start()
     launches0 = lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nvtx = os.environ.get("GPP_NVTX") == "1"  # ncu --nvtx --nvtx-include "timed/": steady-state launch lists
     torch.cuda.synchronize()
+    if nvtx:
+        torch.cuda.nvtx.range_push("timed")
     e0.record()
     for _ in range(args.steps):
         step()
     e1.record()
     torch.cuda.synchronize()
+    if nvtx:
+        torch.cuda.nvtx.range_pop()
     launches = lib.launch_count() - launches0
     if graphed is not None:  # replays launch the captured kernels without host calls
         launches = graphed_launches * args.steps

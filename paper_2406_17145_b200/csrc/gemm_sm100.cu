@@ -30,6 +30,11 @@ namespace gpp {
 namespace tc {
 
 constexpr int NUM_THREADS = 192;
+#ifndef GPP_SGD_DEPTH
+#define GPP_SGD_DEPTH 2
+#endif
+constexpr int SGD_DEPTH = GPP_SGD_DEPTH;  // master chunks in flight per warp (3 with a 3-stage ring measured slower)
+constexpr int SGD_STAGES256 = SGD_DEPTH >= 3 ? 3 : 4;     // operand ring of the 256-wide SGD GEMM
 constexpr int PAIR_EPI_WARPS = 8;                          // two epilogue warpgroups
 constexpr int PAIR_THREADS = 64 + 32 * PAIR_EPI_WARPS;     // + TMA warp + MMA warp
 
@@ -708,21 +713,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       constexpr int CH = BN / 32 / GSTEP;  // chunks per warp per tile (even)
       if constexpr (EPI == EPI_SGD) {
         if (sgd_fast_ok(epu, N) && k_splits == 1) {
-          float* b0 = epi_stage + (warp - 2) * 2 * 32 * STAGE_LD;
-          float* b1 = b0 + 32 * STAGE_LD;
+          // SGD_DEPTH master chunks in flight per warp, issued before the accumulator is ready
+          float* b0 = epi_stage + (warp - 2) * SGD_DEPTH * 32 * STAGE_LD;
           auto col_of = [&](int p) { return n_blk * BN + (group + p * GSTEP) * 32; };
-          sgd_fast_issue(epu, b0, row0, col_of(0), M, N, lane);
-          sgd_fast_issue(epu, b1, row0, col_of(1), M, N, lane);
+#pragma unroll
+          for (int p = 0; p < SGD_DEPTH && p < CH; ++p) sgd_fast_issue(epu, b0 + p * 32 * STAGE_LD, row0, col_of(p), M, N, lane);
           mbar_wait(&tfull_bar[acc], aph);
           tc_fence_after();
 #pragma unroll
           for (int p = 0; p < CH; ++p) {
-            float* buf = (p & 1) ? b1 : b0;
+            float* buf = b0 + (p % SGD_DEPTH) * 32 * STAGE_LD;
             uint32_t v[32];
             tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + (group + p * GSTEP) * 32, v);
-            if (p + 1 < CH) cp_async_wait<1>(); else cp_async_wait<0>();
+            // groups committed after chunk p's: min(SGD_DEPTH, CH - p) - 1
+            const int after = (CH - p < SGD_DEPTH ? CH - p : SGD_DEPTH) - 1;
+            if (after >= 2) cp_async_wait<2>(); else if (after == 1) cp_async_wait<1>(); else cp_async_wait<0>();
             sgd_fast_update(epu, v, buf, row0, col_of(p), M, N, lane);
-            if (p + 2 < CH) sgd_fast_issue(epu, buf, row0, col_of(p + 2), M, N, lane);
+            if (p + SGD_DEPTH < CH) sgd_fast_issue(epu, buf, row0, col_of(p + SGD_DEPTH), M, N, lane);
           }
           tc_fence_before();
           __syncwarp();
@@ -959,7 +966,7 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   constexpr int STAGE_BYTES = (BM + BN / 2) * BK * 2;
   // fp32 epilogues stage through smem (fused SGD double-buffers its master chunks);
   // the bf16 epilogues write straight from registers and give that space to the ring
-  constexpr int EPI_BUFS = EPI == EPI_SGD ? 2 : (EPI == EPI_F32 ? 1 : 0);
+  constexpr int EPI_BUFS = EPI == EPI_SGD ? SGD_DEPTH : (EPI == EPI_F32 ? 1 : 0);
   constexpr int SMEM = AUX_TMA_EPI(EPI) ? STAGES * STAGE_BYTES + 1024 + 1024 + PAIR_EPI_WARPS * 4096
                                         : STAGES * STAGE_BYTES + 1024 + 256 + PAIR_EPI_WARPS * 32 * STAGE_LD * 4 * EPI_BUFS;
   CUtensorMap mx = ma;
@@ -1106,8 +1113,8 @@ static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
     constexpr int E = decltype(epi_tag)::value;
     if (pair) {
       // EPI_SGD gives one smem stage to its double-buffered master chunks
-      constexpr int S256 = E == EPI_SGD ? 4 : (E == EPI_F32 ? 5 : 6);
-      constexpr int S128 = E == EPI_SGD ? 6 : (E == EPI_F32 ? 7 : 8);
+      constexpr int S256 = E == EPI_SGD ? SGD_STAGES256 : (E == EPI_F32 ? 5 : 6);
+      constexpr int S128 = E == EPI_SGD ? (SGD_DEPTH >= 3 ? 4 : 6) : (E == EPI_F32 ? 7 : 8);
       if (bn == 256) return launch_tc_pair<256, S256, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
       return launch_tc_pair<128, S128, A_MN, B_MN, E>(a, lda, b, ldb, e, M, N, K, ks, stream);
     }

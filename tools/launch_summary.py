@@ -1,6 +1,8 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel.
 
-    python tools/launch_summary.py profiles/launches_r1e_candle.csv
+    python tools/launch_summary.py profiles/launches_r1e_candle.csv [--steps K]
+
+--steps K divides the totals by K (per-step figures for a K-step capture).
 """
 import collections
 import csv
@@ -8,7 +10,7 @@ import re
 import sys
 
 
-def main(path):
+def main(path, steps=1):
     rows = [r for r in csv.reader(open(path)) if len(r) > 5]
     h, data = rows[0], rows[1:]
     ki, vi, ni = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name")
@@ -25,11 +27,12 @@ def main(path):
         tot[key] += us
         cnt[key] += 1
     T = sum(tot.values())
-    print(f"{sum(cnt.values())} launches, {T:.1f} us total (ncu: serialised, cold-cache)")
+    print(f"{sum(cnt.values())} launches, {T:.1f} us total (ncu: serialised, cold-cache)"
+          + (f"; per step: {sum(cnt.values()) / steps:.0f} launches, {T / steps:.1f} us" if steps > 1 else ""))
     print(f"{'share':>6} {'n':>5} {'avg us':>9}  kernel")
     for k, v in tot.most_common():
         print(f"{100 * v / T:5.1f}% {cnt[k]:5d} {v / cnt[k]:9.2f}  {k}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 1)
