@@ -29,7 +29,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, layout, B, outdir, graphed=False):
+def _worker(rank, world, port, layout, B, outdir, graphed=False, extra_edges=()):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
@@ -44,7 +44,8 @@ def _worker(rank, world, port, layout, B, outdir, graphed=False):
 
         wl = W.toy(B=B)
         stages = [M.Stage(i, frozenset(ops), b, frozenset(devs)) for i, (ops, b, devs) in enumerate(layout)]
-        sg = S.schedule_stage_graph(M.StageGraph(stages, M.induced_stage_edges(wl.graph, [s.op_ids for s in stages]), B))
+        edges = set(M.induced_stage_edges(wl.graph, [s.op_ids for s in stages])) | set(extra_edges)
+        sg = S.schedule_stage_graph(M.StageGraph(stages, edges, B))
         dev = torch.device("cuda", rank)
         ex = Executor(wl, sg, rank, world, CudaBackend(dev), lr=LR, keep_grads=True)
         res = {"loss": [], "grads": []}
@@ -77,7 +78,7 @@ def _worker(rank, world, port, layout, B, outdir, graphed=False):
         dist.destroy_process_group()
 
 
-def _run(layout, B, world, graphed=False):
+def _run(layout, B, world, graphed=False, extra_edges=()):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     from oracle.reference_model import ReferenceModel
@@ -85,7 +86,7 @@ def _run(layout, B, world, graphed=False):
     from paper_2406_17145_b200.runtime.data import make_batch
 
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), layout, B, d, graphed), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), layout, B, d, graphed, extra_edges), nprocs=world, join=True)
         outs = [torch.load(os.path.join(d, f"rank{r}.pt")) for r in range(world)]
     wl = W.toy(B=B)
     ref = ReferenceModel(wl)
@@ -116,3 +117,9 @@ def test_two_stage_gpp_nccl_cuda_graph():
 
 def test_four_rank_dp_nccl_cuda_graph():
     _run([(TOWER_A, 16, [0]), (TOWER_B, 32, [1, 2]), (TAIL, 8, [3])], 64, 4, graphed=True)
+
+
+def test_sequential_chain_tokens_nccl_cuda_graph():
+    """SPP-shaped chain tower A -> tower B -> tail on 3 GPUs: the data-less chain edge
+    A -> B is realised with NCCL token messages, inside the captured graph too."""
+    _run([(TOWER_A, 16, [0]), (TOWER_B, 16, [1]), (TAIL, 16, [2])], 64, 3, graphed=True, extra_edges=[(0, 1)])
