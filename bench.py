@@ -95,7 +95,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def _workload(name: str, world: int, per_gpu: int | None):
+def _workload(name: str, world: int, per_gpu: int | None, branches: int | None = None):
     from paper_2406_17145_b200 import workloads as W
 
     if name == "candle":
@@ -104,8 +104,8 @@ def _workload(name: str, world: int, per_gpu: int | None):
         return W.toy(B=(per_gpu or 64) * world)
     if name == "dlrm":
         return W.dlrm(B=(per_gpu or 8192) * world)
-    if name == "mmt":
-        return W.mmt(B=(per_gpu or 16) * world)
+    if name == "mmt":  # --branches: the BASELINE configs[4] branch sweep (2 / 4 / 8 branches)
+        return W.mmt(B=(per_gpu or 16) * world, branches=branches or 4)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -262,6 +262,7 @@ def main():
     ap.add_argument("--costs", default="measured", choices=["measured", "analytic"],
                     help="partitioner cost curves: frozen B200 tables (profiles/) or analytic FLOP curves")
     ap.add_argument("--per-gpu-batch", type=int, default=None)
+    ap.add_argument("--branches", type=int, default=None, help="MMT branch count (default 4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--no-spp", action="store_true", help="skip the SPP comparison arm (N > 1)")
@@ -283,7 +284,7 @@ def main():
     from paper_2406_17145_b200.runtime.api import twin
     from paper_2406_17145_b200.workloads import b200_cluster, with_measured_curves
 
-    wl = _workload(args.workload, world, args.per_gpu_batch)
+    wl = _workload(args.workload, world, args.per_gpu_batch, args.branches)
     dev = torch.device("cuda", local)
     arm = _time_arm(wl, world, rank, dev, args.mode, args)
     ex, sg, graphed, dev_batch, ms, launches, clk, t_plan, be = (
@@ -441,7 +442,8 @@ def main():
             "vs_baseline": None, "dtype": "bf16" if wl.dtype != "fp32" else "fp32", "data": "synthetic",
             "config": {
                 "workload": f"{wl.name}: 7 towers x 4 x Linear(4096,4096)+ReLU -> concat -> Linear(28672,1024)+ReLU -> Linear(1024,1) MSE"
-                if wl.name == "candle" else wl.name,
+                if wl.name == "candle" else (f"mmt: {args.branches or 4} branches x 12 pre-LN layers, d=1024, S=512"
+                                            if wl.name == "mmt" else wl.name),
                 "global_batch": wl.mini_batch, "mode": args.mode,
                 "parallelism": f"{args.mode} stages={len(sg.stages)} depth={sim.depth}",
                 "stages": [{"ops": len(s.op_ids), "b": s.micro_batch, "d": s.dp_degree,
