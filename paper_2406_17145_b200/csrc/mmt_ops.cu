@@ -126,16 +126,27 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(bf16* __restrict__ dx, floa
   }
 }
 
-__global__ void ln_bwd_final_kernel(float* __restrict__ dgamma, float* __restrict__ dbeta,
-                                    const float* __restrict__ part, int nblocks, int D,
-                                    int accumulate) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= 2 * D) return;
+// 32 columns per block, the partial rows split over the 8 warps (coalesced 128 B loads,
+// nblocks / 8 independent loads per thread), then a fixed-order smem reduction.
+__global__ void __launch_bounds__(256) ln_bwd_final_kernel(float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                           const float* __restrict__ part, int nblocks, int D,
+                                                           int accumulate) {
+  __shared__ float red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
   float t = 0.f;
-#pragma unroll 8
-  for (int k = 0; k < nblocks; ++k) t += part[static_cast<int64_t>(k) * 2 * D + c];
-  float* o = c < D ? dgamma + c : dbeta + (c - D);
-  *o = accumulate ? *o + t : t;
+  if (c < 2 * D) {
+#pragma unroll 4
+    for (int k = ty; k < nblocks; k += 8) t += part[static_cast<int64_t>(k) * 2 * D + c];
+  }
+  red[ty][tx] = t;
+  __syncthreads();
+  if (ty == 0 && c < 2 * D) {
+#pragma unroll
+    for (int i = 1; i < 8; ++i) t += red[i][tx];
+    float* o = c < D ? dgamma + c : dbeta + (c - D);
+    *o = accumulate ? *o + t : t;
+  }
 }
 
 // ---- 16-byte vectorised LayerNorm forward (D % 256 == 0): lane owns 8-element chunks
@@ -369,7 +380,7 @@ int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, con
     default: set_error("layernorm: D must be 128/256/512/1024"); return GPP_ERR_UNSUPPORTED;
   }
   GPP_LAUNCH_CHECK();
-  ln_bwd_final_kernel<<<static_cast<unsigned>((2 * D + 255) / 256), 256, 0, s>>>(dgamma, dbeta, part, nblk, d, accumulate);
+  ln_bwd_final_kernel<<<static_cast<unsigned>((2 * D + 31) / 32), 256, 0, s>>>(dgamma, dbeta, part, nblk, d, accumulate);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
