@@ -251,6 +251,29 @@ def _time_arm(wl, world, rank, dev, mode, args, clocks=True):
             "clocks": clk, "plan_s": t_plan, "be": be}
 
 
+def _ncu_cross_check(workload: str, peak: float) -> dict | None:
+    """The committed ncu --set full capture of the CANDLE step's forward tower GEMMs
+    (profiles/ncu_candle_fw_gemm_r1g_summary.csv): per-launch duration without the event
+    nodes the live timing needs (which add ~2-4 us per launch), for comparison."""
+    if workload != "candle":
+        return None
+    import csv
+
+    path = os.path.join(ROOT, "profiles", "ncu_candle_fw_gemm_r1g_summary.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+    except OSError:
+        return None
+    h = rows[0]
+    us = [float(r[h.index("gpu__time_duration.sum")].split()[0]) for r in rows[1:]]
+    tens = [float(r[h.index("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")].split()[0]) for r in rows[1:]]
+    avg = sum(us) / len(us)
+    tf = 2.0 * 1024 * 4096 * 4096 / (avg * 1e-6) / 1e12
+    return {"kernel": "fw tower GEMM 1024x4096x4096 (+bias+ReLU)", "us": round(avg, 2), "tflops": round(tf, 1),
+            "frac": round(tf / peak, 4), "tensor_pipe_active_pct": round(sum(tens) / len(tens), 1),
+            "source": "profiles/ncu_candle_fw_gemm_r1g_summary.csv"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -464,6 +487,7 @@ def main():
                          **_gemm_traffic(args.workload),
                          "peak_source": f"{peak_src} bf16_tflops_sustained",
                          "share_of_step": round(gemm_share, 4), "timing": timing,
+                         "ncu_cross_check": _ncu_cross_check(args.workload, peak),
                          "by_kind": summ.get("by_kind", {}),
                          "other_kernels_ms": summ.get("other_ms", {})},
             "clocks": clk,
