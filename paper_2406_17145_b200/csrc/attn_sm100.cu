@@ -3,6 +3,9 @@
 // One CTA per (z = sample x head, 128 query rows); the whole 128 x S score block lives
 // in TMEM (512 fp32 columns), so the thread owning a query row sees every key of it.
 //
+//   attn_fwd2_kernel (default): as below, but P stays in TMEM (bf16 pairs over the consumed
+//                     score columns) as the A operand of O = P V, and goes to HBM through a
+//                     small row staging buffer: ~103 KB of smem, two CTAs per SM.
 //   attn_fwd_kernel : S = Q K^T (tcgen05, TMEM)  ->  P = softmax(alpha S)  (3 TMEM passes:
 //                     max, exp parked back with tcgen05.st, normalise) written as bf16 into
 //                     shared memory in the 128B-swizzled K-major operand layout, from where
@@ -21,6 +24,8 @@
 // TMEM and P passes.  Layout: packed QKV [m S, 3d] (Q | K | V, head h at columns h*64),
 // o / dout [m S, d] head-interleaved, P / dS [Z S, S] with z = sample * H + head.
 #include <cuda.h>
+
+#include <cstdlib>
 
 #include "gemm.cuh"
 #include "tc_ptx.cuh"
@@ -95,6 +100,25 @@ __device__ __forceinline__ void store_row32(bf16* dst, const uint32_t (&v)[32]) 
   }
 }
 
+// 16 consecutive 32-bit TMEM columns of this warp's 32 lanes (one per thread), then wait
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+// D(tmem) (+)= A(tmem, K-major bf16 pairs: lane = row, column j = elements 2j, 2j+1) x B(smem)
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 struct AttnShape {
   int S, d, H;
   float alpha;
@@ -108,6 +132,12 @@ constexpr uint32_t SM_BW_A = 128 * 1024;   // bw: dO (16 KB) + V (2 x 32 KB), th
 constexpr uint32_t SM_BW_O = 208 * 1024;   // bw: O tile (16 KB)
 constexpr uint32_t SM_BW_BAR = 224 * 1024;
 constexpr int SMEM_FW = SM_FW_BAR + 1024 + 1024;
+// fw2 (P kept in TMEM): Q 16 KB | K, then V, 64 KB | per-warp P row staging | barriers
+constexpr uint32_t SM2_KV = 16 * 1024;
+constexpr uint32_t SM2_STG = 80 * 1024;
+constexpr int STG_LD = 80;  // bytes per staged 32-key row (64 + pad: conflict-free)
+constexpr uint32_t SM2_BAR = SM2_STG + AT_EPI_WARPS * 32 * STG_LD;
+constexpr int SMEM_FW2 = SM2_BAR + 1024 + 1024;  // ~103 KB: two CTAs per SM
 constexpr int SMEM_BW = SM_BW_BAR + 1024 + 1024;
 
 }  // namespace
@@ -249,6 +279,167 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       tc_fence_after();
       uint32_t v[32];
       tmem_ld32(trow + hf * 32, v);
+      store_row32(o + static_cast<int64_t>(row0 + m_blk * 128 + lr) * ldo + head * AT_DH + hf * 32, v);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Forward with P kept in TMEM: the normalised bf16 P is written back over the consumed
+// score columns (keys [0,256) -> columns [0,128), keys [256,512) -> [256,384)) and is the
+// A operand of O = P V straight from TMEM (tcgen05.mma [d], [a_tmem], b_desc); O goes to
+// columns [448, 512).  Shared memory drops to Q + K/V (V loaded over K once the scores
+// MMA is done) + row staging for the P stores to HBM, so two CTAs fit per SM: the second
+// issues its Q/K loads (before its TMEM allocation) while the first runs its softmax.
+__global__ void __launch_bounds__(AT_THREADS, 2)
+    attn_fwd2_kernel(const __grid_constant__ CUtensorMap m_q, const __grid_constant__ CUtensorMap m_k,
+                     const __grid_constant__ CUtensorMap m_v, bf16* __restrict__ P, bf16* __restrict__ o,
+                     int64_t ldo, AttnShape sh) {
+  constexpr uint32_t IDESC_S = idesc_bf16<256, false, false>();
+  constexpr uint32_t IDESC_O = idesc_bf16<AT_DH, false, true>();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sq = smem;
+  uint8_t* skv = smem + SM2_KV;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM2_BAR);
+  uint64_t* bar_qk = bar + 0;
+  uint64_t* bar_v = bar + 1;
+  uint64_t* bar_s = bar + 2;
+  uint64_t* bar_p = bar + 3;   // P in TMEM (8 epilogue warps)
+  uint64_t* bar_o = bar + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+  float* red = reinterpret_cast<float*>(smem + SM2_BAR + 128);
+
+  const int S = sh.S, d = sh.d, H = sh.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mblocks = S / 128;
+  const int z = static_cast<int>(blockIdx.x) / mblocks;
+  const int m_blk = static_cast<int>(blockIdx.x) % mblocks;
+  const int sample = z / H, head = z % H;
+  const int row0 = sample * S;
+  const int nkb = S / 64;
+  const int nh = (S + 255) / 256;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 5; ++i) mbar_init(&bar[i], i == 3 ? AT_EPI_WARPS : 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(bar_qk, 128 * 128 + nh * 256 * 128);
+      tma_load_2d(sq, &m_q, bar_qk, head * AT_DH, row0 + m_blk * 128);
+      for (int h = 0; h < nh; ++h)
+        tma_load_2d(skv + h * 32768, &m_k, bar_qk, d + head * AT_DH, row0 + h * 256);
+      mbar_wait(bar_s, 0);  // K consumed: V (MN-major key blocks) over it
+      mbar_expect_tx(bar_v, nkb * 8192);
+      for (int kb = 0; kb < nkb; ++kb) tma_load_2d(skv + kb * 8192, &m_v, bar_v, 2 * d + head * AT_DH, row0 + kb * 64);
+    }
+  } else {
+    if (warp == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    asm volatile("bar.sync 2, %0;" ::"n"(32 + 32 * AT_EPI_WARPS) : "memory");
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp == 1) {
+      if (lane == 0) {
+        mbar_wait(bar_qk, 0);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(sq), ka = smem_u32(skv);
+#pragma unroll
+        for (int k = 0; k < AT_DH / 16; ++k)
+          for (int h = 0; h < nh; ++h)
+            umma_bf16(tmem + h * 256, sdesc_sw128(qa + k * 32, 16, 1024),
+                      sdesc_sw128(ka + h * 32768 + k * 32, 16, 1024), IDESC_S, k != 0);
+        umma_commit(bar_s);
+        mbar_wait(bar_p, 0);
+        mbar_wait(bar_v, 0);
+        tc_fence_after();
+        const uint32_t va = smem_u32(skv);
+        for (int kb = 0; kb < nkb; ++kb)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int key = kb * 64 + k * 16;
+            const uint32_t acol = (key >> 8) * 256 + ((key & 255) >> 1);
+            umma_ts(tmem + 448, tmem + acol, sdesc_sw128(va + kb * 8192 + k * 2048, 8192, 1024), IDESC_O,
+                    (kb | k) != 0);
+          }
+        umma_commit(bar_o);
+      }
+    } else {
+      const int q = warp & 3, hf = (warp - 2) / 4;
+      const int lr = q * 32 + lane;
+      const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+      const int c_lo = hf * 8, c_hi = min(S / 32, hf * 8 + 8);
+      uint8_t* stg = smem + SM2_STG + (warp - 2) * 32 * STG_LD;
+      const int row_base = m_blk * 128 + q * 32;  // within z
+      bf16* pz = P + static_cast<int64_t>(z) * S * S;
+      mbar_wait(bar_s, 0);
+      tc_fence_after();
+      float mx = -INFINITY;
+      for (int c = c_lo; c < c_hi; ++c) {
+        uint32_t v[32];
+        tmem_ld32(trow + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
+      }
+      mx = combine_halves(red, hf, lr, mx, true);
+      const float sl2 = sh.alpha * 1.4426950408889634f;
+      const float mb = mx * sl2;
+      float sum = 0.f;
+      for (int c = c_lo; c < c_hi; ++c) {
+        uint32_t v[32];
+        tmem_ld32(trow + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float e = exp2f(fmaf(__uint_as_float(v[j]), sl2, -mb));
+          sum += e;
+          v[j] = __float_as_uint(e);
+        }
+        tmem_st32(trow + c * 32, v);
+      }
+      const float inv = 1.f / combine_halves(red, hf, lr, sum, false);
+      for (int c = c_lo; c < c_hi; ++c) {
+        uint32_t v[32];
+        tmem_ld32(trow + c * 32, v);
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          pk[j] = pack_bf16(__uint_as_float(v[2 * j]) * inv, __uint_as_float(v[2 * j + 1]) * inv);
+        // packed P over consumed score columns of this half (chunk c -> columns of chunk <= c)
+        tmem_st16(trow + (c >> 3) * 256 + (c & 7) * 16, pk);
+        // and to HBM: this thread's 64 B -> smem -> 4 lanes per row, 16 B each (coalesced)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          *reinterpret_cast<uint4*>(stg + lane * STG_LD + i * 16) = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = (lane >> 2) + 8 * i, seg = lane & 3;
+          const uint4 val = *reinterpret_cast<const uint4*>(stg + r * STG_LD + seg * 16);
+          *reinterpret_cast<uint4*>(pz + static_cast<int64_t>(row_base + r) * S + c * 32 + seg * 8) = val;
+        }
+        __syncwarp();
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_p);
+      mbar_wait(bar_o, 0);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32(trow + 448 + hf * 32, v);
       store_row32(o + static_cast<int64_t>(row0 + m_blk * 128 + lr) * ldo + head * AT_DH + hf * 32, v);
     }
   }
@@ -443,12 +634,25 @@ int tc_attn_fwd(const void* qkv, void* P, void* o, int64_t ldo, int64_t m, int64
   if ((rc = tc::make_map_bf16(&mk, qkv, 3 * d, T, 3 * d, 64, 256))) return rc;
   if ((rc = tc::make_map_bf16(&mv, qkv, 3 * d, T, 3 * d, 64, 64))) return rc;
   if ((rc = tc::make_map_bf16(&mp, P, S, Z * S, S, 64, 128))) return rc;
+  tc::AttnShape sh{static_cast<int>(S), static_cast<int>(d), static_cast<int>(H), alpha};
+  // P kept in TMEM (two CTAs per SM) by default; GPP_ATTN_FWD2=0 selects the smem-P kernel
+  static const bool p_in_tmem = [] { const char* e = std::getenv("GPP_ATTN_FWD2"); return !(e && e[0] == '0'); }();
+  if (p_in_tmem) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(tc::attn_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_FW2);
+      attr2 = true;
+    }
+    tc::attn_fwd2_kernel<<<static_cast<unsigned>(Z * (S / 128)), tc::AT_THREADS, tc::SMEM_FW2, stream>>>(
+        mq, mk, mv, static_cast<bf16*>(P), static_cast<bf16*>(o), ldo, sh);
+    GPP_LAUNCH_CHECK();
+    return GPP_OK;
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc::attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_FW);
     attr = true;
   }
-  tc::AttnShape sh{static_cast<int>(S), static_cast<int>(d), static_cast<int>(H), alpha};
   tc::attn_fwd_kernel<<<static_cast<unsigned>(Z * (S / 128)), tc::AT_THREADS, tc::SMEM_FW, stream>>>(
       mq, mk, mv, mp, static_cast<bf16*>(o), ldo, sh);
   GPP_LAUNCH_CHECK();

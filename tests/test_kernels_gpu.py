@@ -465,3 +465,12 @@ def test_fused_attention_fwd_bwd(cuda_lib, m, S, d, H):
     assert _rel(dS.cpu(), dSr) < 2e-2
     assert _rel(dqkv[:, :d].cpu(), dqr[:, :d]) < 2e-2
     assert (dqkv[:, d:] == 7.0).all(), "attn_bwd wrote outside the Q block of dqkv"
+
+
+def test_fused_attention_fwd_smem_p_variant(cuda_lib):
+    """The smem-P forward kernel (GPP_ATTN_FWD2=0) in a fresh process, vs the oracle."""
+    import os, subprocess, sys
+    env = dict(os.environ, GPP_ATTN_FWD2="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.abspath(__file__),
+                        "-k", "test_fused_attention_fwd_bwd"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
