@@ -109,33 +109,39 @@ def _workload(name: str, world: int, per_gpu: int | None, branches: int | None =
     raise SystemExit(f"unknown workload {name}")
 
 
-def cpu_reference_run(wl_name: str, sample_B: int, steps: int):
-    """Time the reference's CPU path (monolithic torch-CPU step) on a bounded sample."""
+def cpu_reference_run(wl_name: str, sample_B: int, steps: int, min_seconds: float = 0.0, warmup: int = 1):
+    """Time the reference's CPU path (monolithic torch-CPU step) on a bounded sample:
+    ``steps`` steps, continued until at least ``min_seconds`` of CPU work are timed.
+    Returns (samples/s, seconds, steps run)."""
     from oracle.reference_model import ReferenceModel
     from paper_2406_17145_b200.runtime.data import make_batch
 
     torch.set_num_threads(os.cpu_count() or 1)
     wl = _workload(wl_name, 1, sample_B)
     ref = ReferenceModel(wl)
-    batch = make_batch(wl, 0)
-    ref.step(batch, 1e-3)  # warm-up (allocations, thread pools)
+    for w in range(max(1, warmup)):  # warm-up (allocations, thread pools)
+        ref.step(make_batch(wl, 10_000 + w), 1e-3)
     t0 = time.perf_counter()
-    for s in range(steps):
-        ref.step(make_batch(wl, s + 1), 1e-3)
+    n = 0
+    while n < steps or (time.perf_counter() - t0 < min_seconds and n < 1000):
+        ref.step(make_batch(wl, n + 1), 1e-3)
+        n += 1
     dt = time.perf_counter() - t0
-    return sample_B * steps / dt, dt
+    return sample_B * n / dt, dt, n
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     sample = {"candle": 32, "toy": 64, "dlrm": 16, "mmt": 1}[args.workload]
-    val, dt = cpu_reference_run(args.workload, sample, max(1, min(args.steps, 3)))
+    # every step is one bounded CPU sample of the workload (B = sample); K steps
+    val, dt, n_run = cpu_reference_run(args.workload, sample, max(1, min(args.steps, 50)),
+                                       warmup=min(args.warmup, 5))
     cores = torch.get_num_threads()
     line = {
         "metric": "train samples/sec", "value": round(val, 3), "unit": "samples/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": max(1, min(args.steps, 3)), "warmup": 1,
-        "ms_per_step": round(1e3 * dt / max(1, min(args.steps, 3)), 3), "higher_is_better": True,
+        "n_gpus": args.gpus, "steps": n_run, "warmup": min(args.warmup, 5),
+        "ms_per_step": round(1e3 * dt / n_run, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16-emulated fp32 (CPU)", "data": "synthetic",
         "config": {"workload": f"{args.workload} (CPU sample B={sample} per step)", "device": "host CPU"},
         "cpu_baseline": {"value": round(val, 3), "unit": "samples/s", "cores": cores, "kind": "port",
@@ -452,9 +458,9 @@ def main():
         cpu = None
         if not args.no_cpu_baseline:
             sample = {"candle": 32, "toy": 64, "dlrm": 16, "mmt": 1}[args.workload]
-            cv, cdt = cpu_reference_run(args.workload, sample, 2)
+            cv, cdt, cn = cpu_reference_run(args.workload, sample, 2, min_seconds=10.0)
             cpu = {"value": round(cv, 3), "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "port",
-                   "sample": f"{args.workload}, 2 steps x B={sample}, monolithic torch-CPU training step "
+                   "sample": f"{args.workload}, {cn} steps x B={sample}, monolithic torch-CPU training step "
                              f"(oracle/reference_model.py), {cdt:.1f}s"}
         achieved = summ["tflops"]
         peak = peaks["bf16_tflops_sustained"]
