@@ -51,7 +51,11 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled DURING the timed region.
+
+    NVML polled every 5 ms from a thread (a 20-step region is ~70 ms: one nvidia-smi
+    process per sample caught at most one reading), the device matched by PCI bus id;
+    falls back to polling nvidia-smi if NVML is unavailable."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -60,10 +64,53 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.rows: list[list[str]] = []
+        self.sm: list[float] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        self._h = None
+        try:
+            import pynvml
 
-    def _run(self):
+            pynvml.nvmlInit()
+            h = None
+            try:
+                pr = torch.cuda.get_device_properties(gpu_index)
+                for fmt in ("{:08x}:{:02x}:{:02x}.0", "{:04x}:{:02x}:{:02x}.0"):
+                    try:
+                        h = pynvml.nvmlDeviceGetHandleByPciBusId(
+                            fmt.format(pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id).encode())
+                        break
+                    except Exception:  # noqa: BLE001
+                        continue
+            except Exception:  # noqa: BLE001
+                h = None
+            self._h = h or pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self._nv = pynvml
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # noqa: BLE001
+            self._nv = None
+
+    def _run_nvml(self):
+        nv, h = self._nv, self._h
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for name, b in bits.items():
+                    if r & b:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.005)
+
+    def _run_smi(self):
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
@@ -71,18 +118,21 @@ class ClockSampler:
                     capture_output=True, text=True, timeout=5).stdout.strip()
                 if out:
                     self.rows.append([c.strip() for c in out.split(",")])
-            except Exception:
+            except Exception:  # noqa: BLE001
                 pass
             self._stop.wait(0.2)
 
     def start(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t = threading.Thread(target=self._run_nvml if self._nv else self._run_smi, daemon=True)
         self._t.start()
 
     def stop(self) -> dict:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        if self._nv:
+            return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                    "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 5 ms"}
         sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -92,7 +142,7 @@ class ClockSampler:
                 if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(self.rows), "source": "nvidia-smi"}
 
 
 def _workload(name: str, world: int, per_gpu: int | None, branches: int | None = None):
