@@ -87,6 +87,11 @@ class PartitionOptions:
     # necessarily contains the concatenation operator", which the
     # SP-aligned DP alone cannot express (it would spend a device on the join).
     merge_join: bool = False
+    # B200 extension (off for the SPEC tests): bundles of <= max_exhaustive_branches also
+    # try every contiguous cut of the canonical branch order besides the reference's
+    # one-vs-rest + balanced cuts (spgraph.parallel_splits), so e.g. 6 towers can form
+    # three 2-tower stages -- unreachable from one-vs-rest / halves.
+    rich_splits: bool = False
 
 
 @dataclass
@@ -375,8 +380,17 @@ class _DP:
 
         if len(kids) <= self.opts.max_exhaustive_branches:
             out = []
+            seen = set()
             for one, rest in parallel_splits(node):
                 out.append((bundle([c for c in kids if c.ops <= one]), bundle([c for c in kids if c.ops <= rest])))
+                seen.add(frozenset((one, rest)))
+            if self.opts.rich_splits:
+                for k in range(2, len(kids) - 1):
+                    one = frozenset().union(*(c.ops for c in kids[:k]))
+                    rest = frozenset().union(*(c.ops for c in kids[k:]))
+                    if frozenset((one, rest)) not in seen:
+                        seen.add(frozenset((one, rest)))
+                        out.append((bundle(kids[:k]), bundle(kids[k:])))
             return out
         return [(bundle(kids[:k]), bundle(kids[k:])) for k in range(1, len(kids))]
 

@@ -74,7 +74,8 @@ def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions 
             if not (min_microbatches <= B // b <= max_microbatches):
                 continue
             for mj in merges:
-                o = P.PartitionOptions(**{**opts.__dict__, "micro_batches": (b,), "merge_join": mj})
+                o = P.PartitionOptions(**{**opts.__dict__, "micro_batches": (b,), "merge_join": mj,
+                                          "rich_splits": mode == "gpp"})
                 try:
                     cand = fn(wl.graph, cluster, B, o)
                 except P.NoFeasibleStrategy:
