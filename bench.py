@@ -506,7 +506,7 @@ def main():
 
     if rank == 0:
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only (the contract)
             sample = {"candle": 32, "toy": 64, "dlrm": 16, "mmt": 1}[args.workload]
             cv, cdt, cn = cpu_reference_run(args.workload, sample, 2, min_seconds=10.0)
             cpu = {"value": round(cv, 3), "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "port",
