@@ -2,6 +2,8 @@
 // SURVEY.md §2.3): pre-LN LayerNorm fwd/bwd, attention softmax fwd/bwd over fp32 scores,
 // token mean-pool fwd/bwd, and the batched attention GEMM entry point.  Warp-per-row,
 // registers only, fp32 statistics; deterministic column reductions via partial buffers.
+#include <algorithm>
+
 #include "gemm.cuh"
 
 namespace gpp {
@@ -360,7 +362,9 @@ int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, con
                       int64_t T, int64_t D, int accumulate, void* stream) {
   GPP_ARG_CHECK(dx && dgamma && dbeta && dy && x && mean && rstd && gamma && T > 0, "bad argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int rpb = 64;
+  // one block per SM: rows per block = ceil(T / 148) rounded up to the 8 warps (T = 8192:
+  // 56 rows, 147 blocks; 64 rows left 20 SMs idle)
+  const int rpb = static_cast<int>(std::max<int64_t>(8, ((T + 147) / 148 + 7) / 8 * 8));
   const int nblk = static_cast<int>((T + rpb - 1) / rpb);
   float* part = ln_scratch(static_cast<size_t>(nblk) * 2 * D);
   if (!part) { set_error("layernorm scratch allocation failed"); return GPP_ERR_CUDA; }
