@@ -360,11 +360,28 @@ __global__ void ce_kernel(float* loss_acc, T* dl, int64_t lddl, const T* logits,
   if (threadIdx.x == 0) atomicAdd(loss_acc, scale * (lse - to_f<T>(lr[lab])));
 }
 
-__global__ void sum_into_kernel(float* acc, const float* v, int64_t n) {
-  float s = 0.f;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
-  s = block_sum(s);
-  if (threadIdx.x == 0) acc[0] += s;
+// Strided row copy (concat / split of branch activations and their gradients): rows of
+// `cv` vectors of type V, flattened over rows x cv, 4 independent loads in flight per thread.
+// cudaMemcpy2DAsync ran these 8 MB slices at ~1 TB/s (copy-engine path); this is HBM-bound.
+template <typename V, typename I>  // I: uint32_t index math when rows x cv < 2^32
+__global__ void __launch_bounds__(256) copy_rows_kernel(V* __restrict__ dst, int64_t ldd,
+                                                        const V* __restrict__ src, int64_t lds,
+                                                        I cv, I n) {
+  constexpr int U = 4;
+  const I stride = static_cast<I>(gridDim.x) * blockDim.x;
+  for (I base = static_cast<I>(blockIdx.x) * blockDim.x + threadIdx.x; base < n; base += stride * U) {
+    V v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const I i = base + u * stride;
+      if (i < n) v[u] = __ldcs(src + (i / cv) * lds + (i % cv));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const I i = base + u * stride;
+      if (i < n) dst[(i / cv) * ldd + (i % cv)] = v[u];
+    }
+  }
 }
 
 // ---------------- optimizer ----------------
@@ -587,13 +604,32 @@ int gpp_copy_rows(void* dst, int64_t lddst, const void* src, int64_t ldsrc, int6
                   int64_t cols, int elem_bytes, void* stream) {
   GPP_ARG_CHECK(dst && src && rows >= 0 && cols >= 0, "bad argument");
   if (rows == 0 || cols == 0) return GPP_OK;
-  cudaError_t e = cudaMemcpy2DAsync(dst, lddst * elem_bytes, src, ldsrc * elem_bytes,
-                                    cols * elem_bytes, rows, cudaMemcpyDeviceToDevice,
-                                    static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) {
-    set_error(std::string("gpp_copy_rows: ") + cudaGetErrorString(e));
-    return GPP_ERR_CUDA;
+  GPP_ARG_CHECK(lddst >= cols && ldsrc >= cols && elem_bytes > 0, "bad leading dimension");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t rb = static_cast<uint64_t>(cols) * elem_bytes;
+  const uint64_t db = static_cast<uint64_t>(lddst) * elem_bytes, sb = static_cast<uint64_t>(ldsrc) * elem_bytes;
+  const uint64_t al = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | rb | db | sb;
+  // widest vector every row start, row length and pitch is aligned to
+  const int vb = (al % 16 == 0) ? 16 : (al % 8 == 0) ? 8 : (al % 4 == 0) ? 4 : (al % 2 == 0) ? 2 : 1;
+  const uint64_t cv = rb / vb, n = cv * static_cast<uint64_t>(rows);
+  const int g = grid_for(static_cast<int64_t>((n + 3) / 4), 256);
+  const bool i32 = n + 4ull * 256 * g < (1ull << 32);  // no wrap of base + u * stride either
+#define GPP_COPY_ROWS(V)                                                                          \
+  if (i32)                                                                                        \
+    copy_rows_kernel<V, uint32_t><<<g, 256, 0, s>>>(static_cast<V*>(dst), db / vb,                \
+        static_cast<const V*>(src), sb / vb, static_cast<uint32_t>(cv), static_cast<uint32_t>(n)); \
+  else                                                                                            \
+    copy_rows_kernel<V, uint64_t><<<g, 256, 0, s>>>(static_cast<V*>(dst), db / vb,                \
+        static_cast<const V*>(src), sb / vb, cv, n)
+  switch (vb) {
+    case 16: GPP_COPY_ROWS(uint4); break;
+    case 8: GPP_COPY_ROWS(uint2); break;
+    case 4: GPP_COPY_ROWS(uint32_t); break;
+    case 2: GPP_COPY_ROWS(uint16_t); break;
+    default: GPP_COPY_ROWS(uint8_t); break;
   }
+#undef GPP_COPY_ROWS
+  GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
 

@@ -474,3 +474,26 @@ def test_fused_attention_fwd_smem_p_variant(cuda_lib):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.abspath(__file__),
                         "-k", "test_fused_attention_fwd_bwd"], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.uint8])
+@pytest.mark.parametrize("rows,cols,ld_src,ld_dst,off", [
+    (1024, 4096, 4096, 28672, 8192),   # CANDLE concat: tower output -> column slice (16 B vectors)
+    (1024, 4096, 28672, 4096, 0),      # and the backward split
+    (8192, 64, 64, 1728, 64 * 5),      # DLRM interaction slices
+    (37, 13, 13, 45, 3),               # odd widths / offsets: narrow vector paths
+    (5, 1, 1, 7, 6),
+    (0, 16, 16, 16, 0),
+])
+def test_copy_rows(cuda_lib, dtype, rows, cols, ld_src, ld_dst, off):
+    g = torch.Generator(device="cuda").manual_seed(rows + cols + off)
+    src_full = (torch.rand(max(rows, 1), ld_src, device="cuda", generator=g) * 200).to(dtype)
+    dst_full = torch.zeros(max(rows, 1), ld_dst, device="cuda", dtype=dtype)
+    src = src_full[:rows, (ld_src - cols) if ld_src > cols else 0:][:, :cols]
+    dst = dst_full[:rows, off:off + cols] if ld_dst > cols else dst_full[:rows]
+    cuda_lib.copy_rows(dst, src)
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src)
+    mask = torch.ones_like(dst_full, dtype=torch.bool)
+    mask[:rows, off:off + cols] = False  # nothing outside the slice is touched
+    assert torch.equal(dst_full[mask], torch.zeros_like(dst_full[mask]))
