@@ -29,6 +29,7 @@
  *   gpp_interaction_fwd / _bwd  DLRM dot interaction
  *   gpp_copy_rows               strided row-block copy (concat slices, DP re-shard,
  *                               same-device stage edges)
+ *   gpp_copy_rows_multi         all slices of one concat / split in one launch
  *
  * Conventions:
  *   - every function returns 0 on success, a nonzero gpp_status otherwise;
@@ -147,6 +148,13 @@ int gpp_sgd_step(float* master, void* shadow_bf16, const float* grad, int64_t n,
 /* dst[r, :cols] = src[r, :cols] for r < rows (same device; elem_bytes 2 or 4). */
 int gpp_copy_rows(void* dst, int64_t lddst, const void* src, int64_t ldsrc, int64_t rows,
                   int64_t cols, int elem_bytes, void* stream);
+/* n slices of one concat / split (same rows) in one launch:
+ * dst[k][r, :cols[k]] = src[k][r, :cols[k]].  The arrays are read during the call (a
+ * captured graph keeps its own copy).  Replaces the per-predecessor slice copies of the
+ * reference executor's concat (PAPER.md:589 stage executor; not in the reference code). */
+int gpp_copy_rows_multi(int n, void* const* dst, const int64_t* lddst, const void* const* src,
+                        const int64_t* ldsrc, int64_t rows, const int64_t* cols, int elem_bytes,
+                        void* stream);
 /* dst_f32[i] = float(src[i]) or dst_bf16[i] = bf16(src_f32[i]). */
 int gpp_cast(void* dst, int dst_dtype, const void* src, int src_dtype, int64_t n, void* stream);
 

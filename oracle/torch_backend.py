@@ -123,6 +123,10 @@ class TorchBackend:
     def copy_rows(self, dst, src):
         dst.copy_(src)
 
+    def copy_rows_multi(self, dsts, srcs):
+        for d, s in zip(dsts, srcs):
+            d.copy_(s)
+
     def sgd_step(self, master, shadow, grad, lr):
         master.sub_(lr * grad)
         if shadow is not None:

@@ -1,3 +1,4 @@
+#include <algorithm>
 // C-ABI entry points (include/gpp_b200.h) and the SIMT kernels around the GEMMs:
 // N=1 heads, fused losses, bias-grad column sums, the fused SGD step, casts and
 // strided row copies.  All memory-bound; vectorised where alignment allows.
@@ -384,6 +385,40 @@ __global__ void __launch_bounds__(256) copy_rows_kernel(V* __restrict__ dst, int
   }
 }
 
+// Several slices of one concat / split in one launch: blockIdx.y = slice.  The descriptors
+// travel by value in the kernel parameters, so a captured CUDA graph owns them.
+constexpr int kMaxCopySlices = 32;
+struct CopySlices {
+  char* dst[kMaxCopySlices];
+  const char* src[kMaxCopySlices];
+  int64_t ldd[kMaxCopySlices], lds[kMaxCopySlices];  // in vectors
+  uint32_t cv[kMaxCopySlices];                         // vectors per row
+};
+
+template <typename V>
+__global__ void __launch_bounds__(256) copy_slices_kernel(const __grid_constant__ CopySlices d,
+                                                          uint32_t rows) {
+  constexpr int U = 4;
+  const int k = blockIdx.y;
+  const uint32_t cv = d.cv[k], n = cv * rows;
+  V* __restrict__ dst = reinterpret_cast<V*>(d.dst[k]);
+  const V* __restrict__ src = reinterpret_cast<const V*>(d.src[k]);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < n; base += stride * U) {
+    V v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = base + u * stride;
+      if (i < n) v[u] = __ldcs(src + (i / cv) * d.lds[k] + (i % cv));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = base + u * stride;
+      if (i < n) dst[(i / cv) * d.ldd[k] + (i % cv)] = v[u];
+    }
+  }
+}
+
 // ---------------- optimizer ----------------
 __global__ void sgd_kernel(float* __restrict__ master, bf16* __restrict__ shadow,
                            const float* __restrict__ grad, int64_t n, float lr) {
@@ -602,8 +637,9 @@ int gpp_sgd_step(float* master, void* shadow_bf16, const float* grad, int64_t n,
 
 int gpp_copy_rows(void* dst, int64_t lddst, const void* src, int64_t ldsrc, int64_t rows,
                   int64_t cols, int elem_bytes, void* stream) {
-  GPP_ARG_CHECK(dst && src && rows >= 0 && cols >= 0, "bad argument");
-  if (rows == 0 || cols == 0) return GPP_OK;
+  GPP_ARG_CHECK(rows >= 0 && cols >= 0, "bad argument");
+  if (rows == 0 || cols == 0) return GPP_OK;  // empty tensors may carry null pointers
+  GPP_ARG_CHECK(dst && src, "bad argument");
   GPP_ARG_CHECK(lddst >= cols && ldsrc >= cols && elem_bytes > 0, "bad leading dimension");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t rb = static_cast<uint64_t>(cols) * elem_bytes;
@@ -630,6 +666,54 @@ int gpp_copy_rows(void* dst, int64_t lddst, const void* src, int64_t ldsrc, int6
   }
 #undef GPP_COPY_ROWS
   GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_copy_rows_multi(int n, void* const* dst, const int64_t* lddst, const void* const* src,
+                        const int64_t* ldsrc, int64_t rows, const int64_t* cols, int elem_bytes,
+                        void* stream) {
+  GPP_ARG_CHECK(n >= 0 && rows >= 0 && elem_bytes > 0 && (n == 0 || (dst && lddst && src && ldsrc && cols)),
+                "bad argument");
+  if (n == 0 || rows == 0) return GPP_OK;
+  uint64_t al = 0, most = 0;
+  for (int k = 0; k < n; ++k) {
+    GPP_ARG_CHECK(cols[k] >= 0, "bad slice");
+    if (cols[k] == 0) continue;
+    GPP_ARG_CHECK(dst[k] && src[k] && lddst[k] >= cols[k] && ldsrc[k] >= cols[k],
+                  "bad slice");
+    al |= reinterpret_cast<uintptr_t>(dst[k]) | reinterpret_cast<uintptr_t>(src[k]) |
+          static_cast<uint64_t>(cols[k]) * elem_bytes | static_cast<uint64_t>(lddst[k]) * elem_bytes |
+          static_cast<uint64_t>(ldsrc[k]) * elem_bytes;
+    most = std::max(most, static_cast<uint64_t>(cols[k]) * elem_bytes * rows);
+  }
+  // one vector width for all slices: 16 B for the bf16 concat / interaction slices, else
+  // (or for > 4 GB slices) one strided copy per slice
+  if (al % 16 != 0 || most / 16 + 4ull * 256 * 148 * 16 >= (1ull << 32)) {
+    for (int k = 0; k < n; ++k) {
+      const int rc = gpp_copy_rows(dst[k], lddst[k], src[k], ldsrc[k], rows, cols[k], elem_bytes, stream);
+      if (rc != GPP_OK) return rc;
+    }
+    return GPP_OK;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int k0 = 0; k0 < n; k0 += kMaxCopySlices) {
+    const int nk = std::min(kMaxCopySlices, n - k0);
+    CopySlices d{};
+    uint64_t big = 0;
+    for (int k = 0; k < nk; ++k) {
+      d.dst[k] = static_cast<char*>(dst[k0 + k]);
+      d.src[k] = static_cast<const char*>(src[k0 + k]);
+      d.ldd[k] = lddst[k0 + k] * elem_bytes / 16;
+      d.lds[k] = ldsrc[k0 + k] * elem_bytes / 16;
+      d.cv[k] = static_cast<uint32_t>(cols[k0 + k] * elem_bytes / 16);
+      big = std::max(big, static_cast<uint64_t>(d.cv[k]) * rows);
+    }
+    // ~148*16 blocks over all slices
+    int gx = grid_for(static_cast<int64_t>((big + 3) / 4), 256);
+    gx = std::max(1, std::min(gx, (148 * 16 + nk - 1) / nk));
+    copy_slices_kernel<uint4><<<dim3(gx, nk), 256, 0, s>>>(d, static_cast<uint32_t>(rows));
+    GPP_LAUNCH_CHECK();
+  }
   return GPP_OK;
 }
 

@@ -41,7 +41,7 @@ def twin(sg: StageGraph, cluster, graph):
 
 def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions | None = None,
          mem_bytes: float = 180e9, sweep: bool | None = None, min_microbatches: int = 1,
-         max_microbatches: int = 32, costs: str = "measured") -> P.Strategy:
+         max_microbatches: int = 32, costs: str = "measured", include_spp: bool | None = None) -> P.Strategy:
     """Run the GPP (or SPP baseline) partitioner + scheduler for ``n_gpus`` B200s.
 
     The TPS objective (Eq. 1) is a steady-state measure: with launch overheads in the
@@ -51,6 +51,12 @@ def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions 
     once per uniform micro-batch size b (B/b in [min_microbatches, max_microbatches])
     and keeps the strategy with the shortest simulated iteration (sim.simulate),
     which does see warm-up / cool-down bubbles.  Single-GPU plans skip the sweep.
+
+    A sequential pipeline is itself a graph pipeline (a chain of stages), but the SP-DP
+    only cuts at series/parallel boundaries, so it can miss a balanced chain cut through
+    the middle of a parallel region (DLRM at 2 GPUs: 30/5 ops, twin 8.63 ms, vs the
+    sequential 18/17-op cut, 7.46 ms).  With ``include_spp`` (default for GPP sweeps) the
+    SPP candidates join the GPP sweep and the twin picks; ``optimize`` itself is unchanged.
     """
     from ..sim import simulate
     from ..workloads import with_measured_curves
@@ -73,11 +79,14 @@ def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions 
         for b, _ in P.candidate_configs(B):
             if not (min_microbatches <= B // b <= max_microbatches):
                 continue
-            for mj in merges:
+            if include_spp is None:
+                include_spp = mode == "gpp"
+            arms = [(fn, mj) for mj in merges] + ([(P.spp_optimize, False)] if include_spp and mode == "gpp" else [])
+            for f, mj in arms:
                 o = P.PartitionOptions(**{**opts.__dict__, "micro_batches": (b,), "merge_join": mj,
-                                          "rich_splits": mode == "gpp"})
+                                          "rich_splits": f is P.optimize})
                 try:
-                    cand = fn(wl.graph, cluster, B, o)
+                    cand = f(wl.graph, cluster, B, o)
                 except P.NoFeasibleStrategy:
                     continue
                 t = twin(cand.stage_graph, cluster, wl.graph).iteration_ms

@@ -65,6 +65,9 @@ class CudaBackend:
     def copy_rows(self, dst, src):
         lib.copy_rows(dst, src)
 
+    def copy_rows_multi(self, dsts, srcs):
+        lib.copy_rows_multi(dsts, srcs)
+
     def sgd_step(self, master, shadow, grad, lr):
         lib.sgd_step(master, shadow, grad, lr)
 

@@ -486,15 +486,19 @@ class Executor:
                 pre = self.pre[o][slot] if o in self.pre else None
                 be.linear_fwd(self.out[o][slot], x, self.W[(o, "w")], self.P[(o, "b")], spec.act, pre=pre)
             elif spec.kind == "concat":
-                off = 0
+                off, dst, src, pdst, psrc = 0, [], [], [], []
                 for u in self.wl.graph.predecessors(o):
                     w_u = _width(self.wl.layers[u])
-                    be.copy_rows(self.out[o][slot][:, off:off + w_u], self._x_of(u, slot))
+                    dst.append(self.out[o][slot][:, off:off + w_u])
+                    src.append(self._x_of(u, slot))
                     if o in self.pre:
                         if u not in self.pre:
                             raise NotImplementedError(f"GELU pre-activation of op {u} is not on this stage")
-                        be.copy_rows(self.pre[o][slot][:, off:off + w_u], self.pre[u][slot])
+                        pdst.append(self.pre[o][slot][:, off:off + w_u])
+                        psrc.append(self.pre[u][slot])
                     off += w_u
+                be.copy_rows_multi(dst, src)
+                be.copy_rows_multi(pdst, psrc)
             elif spec.kind in ("mse_head", "bce_head"):
                 x = self._input(o, j, slot, batch)
                 be.rowdot_fwd(self.pred[o][slot], x, self.P[(o, "w")], self.P[(o, "b")])
@@ -509,10 +513,9 @@ class Executor:
                 idx = batch[spec.data_key][j * self.m:(j + 1) * self.m]
                 be.embbag_fwd(self.out[o][slot], self.tables[o], idx)
             elif spec.kind == "interaction":
-                off = 0
-                for u in self.wl.graph.predecessors(o):
-                    be.copy_rows(self.zbuf[o][slot][:, off:off + 64], self._x_of(u, slot))
-                    off += 64
+                us = self.wl.graph.predecessors(o)
+                be.copy_rows_multi([self.zbuf[o][slot][:, 64 * i:64 * (i + 1)] for i in range(len(us))],
+                                   [self._x_of(u, slot) for u in us])
                 be.interaction_fwd(self.out[o][slot], self.zbuf[o][slot], spec.in_dim, spec.out_dim)
             elif spec.kind == "ce_head":
                 x = self._input(o, j, slot, batch)
@@ -589,17 +592,17 @@ class Executor:
                     raise NotImplementedError("interaction inputs: ReLU/none first feature, linear others")
                 be.interaction_bwd(self.dzbuf[o], self._dz_of(o, slot), self.zbuf[o][slot], spec.in_dim,
                                    first_act == "relu")
-                off = 0
-                for u in us:
-                    be.copy_rows(self._dx_target(u, slot), self.dzbuf[o][:, off:off + 64])
-                    off += 64
+                be.copy_rows_multi([self._dx_target(u, slot) for u in us],
+                                   [self.dzbuf[o][:, 64 * i:64 * (i + 1)] for i in range(len(us))])
             elif spec.kind == "concat":
                 dz = self._dz_of(o, slot)
-                off = 0
+                off, dst, src = 0, [], []
                 for u in preds:
                     w_u = _width(self.wl.layers[u])
-                    be.copy_rows(self._dx_target(u, slot), dz[:, off:off + w_u])
+                    dst.append(self._dx_target(u, slot))
+                    src.append(dz[:, off:off + w_u])
                     off += w_u
+                be.copy_rows_multi(dst, src)
             elif spec.kind in ("mse_head", "bce_head"):
                 x = self._input(o, j, slot, batch)
                 u = preds[0] if needs_dx else None

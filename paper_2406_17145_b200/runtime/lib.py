@@ -41,6 +41,7 @@ _SIGS = {
     "gpp_colsum": ([_vp, _vp, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_sgd_step": ([_vp, _vp, _vp, _i64, _f32, _vp], _i32),
     "gpp_copy_rows": ([_vp, _i64, _vp, _i64, _i64, _i64, _i32, _vp], _i32),
+    "gpp_copy_rows_multi": ([_i32, _vp, _vp, _vp, _vp, _i64, _vp, _i32, _vp], _i32),
     "gpp_cast": ([_vp, _i32, _vp, _i32, _i64, _vp], _i32),
     "gpp_nccl_available": ([], _i32),
     "gpp_nccl_unique_id": ([_vp], _i32),
@@ -222,6 +223,20 @@ def sgd_step(master, shadow, grad, lr: float, stream=None):
 def copy_rows(dst, src, stream=None):
     rows, cols = src.shape
     call("gpp_copy_rows", _ptr(dst), _ld(dst), _ptr(src), _ld(src), rows, cols, src.element_size(), _stream(stream))
+
+
+def copy_rows_multi(dsts, srcs, stream=None):
+    """All slices of one concat / split (same row count, same dtype) in one launch."""
+    n = len(dsts)
+    if n == 0:
+        return
+    rows = srcs[0].shape[0]
+    if any(s.shape[0] != rows or d.shape != s.shape or d.dtype != s.dtype for d, s in zip(dsts, srcs)):
+        raise ValueError("copy_rows_multi: slices must share rows and dtype and match shapes")
+    P, L = ctypes.c_void_p * n, ctypes.c_int64 * n
+    call("gpp_copy_rows_multi", n, P(*[_ptr(d) for d in dsts]), L(*[_ld(d) for d in dsts]),
+         P(*[_ptr(s) for s in srcs]), L(*[_ld(s) for s in srcs]), rows, L(*[s.shape[1] for s in srcs]),
+         srcs[0].element_size(), _stream(stream))
 
 
 def embbag_fwd(out, table, idx, stream=None):

@@ -497,3 +497,19 @@ def test_copy_rows(cuda_lib, dtype, rows, cols, ld_src, ld_dst, off):
     mask = torch.ones_like(dst_full, dtype=torch.bool)
     mask[:rows, off:off + cols] = False  # nothing outside the slice is touched
     assert torch.equal(dst_full[mask], torch.zeros_like(dst_full[mask]))
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("widths,rows", [([4096] * 7, 1024), ([64] * 27, 8192), ([13, 64, 8], 37),
+                                          ([64] * 40, 16)])  # > 32 slices: two launches
+def test_copy_rows_multi(cuda_lib, dtype, widths, rows):
+    g = torch.Generator(device="cuda").manual_seed(rows + len(widths))
+    parts = [(torch.rand(rows, w, device="cuda", generator=g) * 100).to(dtype) for w in widths]
+    cat = torch.empty(rows, sum(widths), device="cuda", dtype=dtype)
+    offs = [sum(widths[:i]) for i in range(len(widths))]
+    cuda_lib.copy_rows_multi([cat[:, o:o + w] for o, w in zip(offs, widths)], parts)  # concat
+    back = [torch.empty_like(p) for p in parts]
+    cuda_lib.copy_rows_multi(back, [cat[:, o:o + w] for o, w in zip(offs, widths)])  # split
+    torch.cuda.synchronize()
+    assert torch.equal(cat, torch.cat(parts, dim=1))
+    assert all(torch.equal(a, b) for a, b in zip(back, parts))
