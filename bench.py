@@ -507,7 +507,8 @@ def main():
                "stages": [{"ops": len(s.op_ids), "b": s.micro_batch, "d": s.dp_degree} for s in sp["sg"].stages],
                "gpp_stages": [{"ops": a, "b": b, "d": d} for a, b, d in spp_sg_gpp],
                # the GPP sweep keeps a sequential candidate when the twin rates it faster
-               "gpp_picked_sequential": [s.op_ids for s in sg.stages] == [s.op_ids for s in sp["sg"].stages],
+               "gpp_picked_sequential": ([(s.op_ids, s.micro_batch) for s in sg.stages], sg.edges)
+                                        == ([(s.op_ids, s.micro_batch) for s in sp["sg"].stages], sp["sg"].edges),
                "note": "SPP = spp_optimize (SPEC.md:384-392) strategy on this same runtime, CUDA-graph replay"}
 
     # ---------------- simulated twin + bubble estimate ----------------
