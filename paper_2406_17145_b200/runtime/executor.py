@@ -549,6 +549,7 @@ class Executor:
         post = lambda pcs: self._isend_many([(self.gsend[pc.tensor][slot][pc.c_row0:pc.c_row0 + pc.rows],
                                                 pc.producer) for pc in pcs])
         works = []
+        emb_dst, emb_src = [], []
         g = self.wl.graph
         for o in reversed(self.ops):
             spec = self.layers[o]
@@ -583,8 +584,9 @@ class Executor:
                 dx = self._dx_target(preds[0], slot).reshape(lay.T, lay.d) if needs_dx else None
                 lay.backward(self._dz_of(o, slot), x.reshape(lay.T, lay.d), dx, slot, accumulate,
                              j == self.last_bw)
-            elif spec.kind == "embbag":
-                be.copy_rows(self.emb_grad[o][j * self.m:(j + 1) * self.m], self._dz_of(o, slot))
+            elif spec.kind == "embbag":  # gathered: one launch for all tables after the loop
+                emb_dst.append(self.emb_grad[o][j * self.m:(j + 1) * self.m])
+                emb_src.append(self._dz_of(o, slot))
             elif spec.kind == "interaction":
                 us = list(preds)
                 first_act = self.eff_act(us[0])
@@ -625,6 +627,7 @@ class Executor:
                     marked = True
             if marked:
                 works += sends.flush(post)
+        be.copy_rows_multi(emb_dst, emb_src)  # embedding-bag output grads -> the SGD scatter's rows
         for ws in pending.values():
             for w in ws:
                 w.wait()
