@@ -105,6 +105,41 @@ __global__ void rowdot_dx_kernel(T* dx, int64_t lddx, const float* dout, const f
   }
 }
 
+// bf16 rows of K % 8 == 0: 8 columns (one 16 B vector of dx / saved) per thread, 32-bit
+// indices.  The scalar kernel above ran the DLRM head (8192 x 4096) at ~1.5 TB/s.
+__global__ void __launch_bounds__(256) rowdot_dx_vec_kernel(bf16* dx, int64_t lddx, const float* dout,
+                                                            const float* w, const bf16* saved,
+                                                            int64_t ldsaved, int act, uint32_t M,
+                                                            uint32_t K8) {
+  const uint32_t n = M * K8;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t m = i / K8, k = (i % K8) * 8;
+    const float d = dout[m];
+    float v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] = d * __ldg(w + k + t);  // w: K floats, L1-resident
+    if (act != GPP_ACT_NONE) {
+      const uint4 sv = __ldcs(reinterpret_cast<const uint4*>(saved + static_cast<int64_t>(m) * ldsaved + k));
+      const bf16* sp = reinterpret_cast<const bf16*>(&sv);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] *= act_bwd(__bfloat162float(sp[t]), act);
+    }
+    uint4 o;
+    bf16* op = reinterpret_cast<bf16*>(&o);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) op[t] = __float2bfloat16(v[t]);
+    *reinterpret_cast<uint4*>(dx + static_cast<int64_t>(m) * lddx + k) = o;
+  }
+}
+
+// out[0] (+)= sum_m v[m]: one block, fixed-order (per-thread strided sums, then block_sum).
+__global__ void __launch_bounds__(1024) sum_kernel(float* out, const float* v, int64_t M, int accumulate) {
+  float s = 0.f;
+  for (int64_t m = threadIdx.x; m < M; m += blockDim.x) s += v[m];
+  s = block_sum(s);
+  if (threadIdx.x == 0) out[0] = (accumulate ? out[0] : 0.f) + s;
+}
+
 // out[n] (+)= sum_m wts[m] * x[m, n]   (wts == nullptr -> 1).  Deterministic:
 // block = 8 row-groups x 32 columns, fixed-order smem reduction.
 template <typename T>
@@ -561,7 +596,14 @@ int gpp_rowdot_bwd(void* dx, int64_t lddx, float* dw, float* dbias, const float*
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (dx) {
     const int g = grid_for(M * K, 256);
-    if (dtype == GPP_BF16)
+    const bool vec = dtype == GPP_BF16 && K % 8 == 0 && lddx % 8 == 0 && M * K < (1ll << 31) &&
+                     reinterpret_cast<uintptr_t>(dx) % 16 == 0 &&
+                     (act == GPP_ACT_NONE || (ldsaved % 8 == 0 && reinterpret_cast<uintptr_t>(saved) % 16 == 0));
+    if (vec)
+      rowdot_dx_vec_kernel<<<grid_for(M * K / 8, 256), 256, 0, s>>>(
+          static_cast<bf16*>(dx), lddx, dout, w, static_cast<const bf16*>(saved), ldsaved, act,
+          static_cast<uint32_t>(M), static_cast<uint32_t>(K / 8));
+    else if (dtype == GPP_BF16)
       rowdot_dx_kernel<bf16><<<g, 256, 0, s>>>(static_cast<bf16*>(dx), lddx, dout, w,
                                                static_cast<const bf16*>(saved), ldsaved, act, M, K);
     else
@@ -576,7 +618,7 @@ int gpp_rowdot_bwd(void* dx, int64_t lddx, float* dw, float* dbias, const float*
     if (rc) return rc;
   }
   if (dbias) {
-    colsum_kernel<float><<<1, 256, 0, s>>>(dbias, dout, 1, nullptr, M, 1, accumulate);
+    sum_kernel<<<1, 1024, 0, s>>>(dbias, dout, M, accumulate);
     GPP_LAUNCH_CHECK();
   }
   return GPP_OK;

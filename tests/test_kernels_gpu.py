@@ -513,3 +513,28 @@ def test_copy_rows_multi(cuda_lib, dtype, widths, rows):
     torch.cuda.synchronize()
     assert torch.equal(cat, torch.cat(parts, dim=1))
     assert all(torch.equal(a, b) for a, b in zip(back, parts))
+
+
+@pytest.mark.parametrize("act", ["none", "relu", "gelu"])
+def test_rowdot_bwd_vector_path(cuda_lib, act):
+    """K % 8 == 0 bf16 head (the DLRM top-MLP output layer shape, scaled down): 16 B vector dx
+    kernel and the one-block dbias sum (with accumulate)."""
+    M, K = 4096, 1024
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = torch.randn(K + 1, device="cuda", generator=g)[1:]  # 4 B-offset weights are fine
+    dpred = torch.randn(M, device="cuda", generator=g)
+    dx = torch.empty(M, K, device="cuda", dtype=torch.bfloat16)
+    dw = torch.zeros(K, device="cuda")
+    db = torch.full((1,), 0.5, device="cuda")
+    cuda_lib.rowdot_bwd(dx, dw, db, dpred, x, w, saved=x if act != "none" else None, act=act, accumulate=True)
+    torch.cuda.synchronize()
+    ref = dpred[:, None] * w[None, :]
+    if act == "relu":
+        ref = ref * (x.float() > 0)
+    elif act == "gelu":
+        xf = x.float().requires_grad_()
+        _gelu(xf).backward(torch.ones_like(xf))
+        ref = ref * xf.grad
+    assert _rel(dx, ref) < 1e-2
+    assert abs(db.item() - (0.5 + dpred.sum().item())) < 1e-3
