@@ -63,6 +63,9 @@ enum gpp_act { GPP_ACT_NONE = 0, GPP_ACT_RELU = 1, GPP_ACT_GELU = 2 };
 
 /* ---- library ---------------------------------------------------------- */
 int gpp_version(void);
+/* "gpp-digest:<sha256>" of the csrc/include sources and nvcc flags the binary was built
+ * from: build() rebuilds and lib.load() refuses a binary whose digest is stale. */
+const char* gpp_source_digest(void);
 const char* gpp_last_error(void);
 /* Number of kernels this library has launched since load (evidence counter). */
 uint64_t gpp_launch_count(void);
@@ -214,7 +217,11 @@ int gpp_attn_bwd(const void* qkv, const void* p, const void* o, int64_t ldo, con
                  void* ds, void* dqkv, int64_t m, int64_t S, int64_t d, int64_t H, float scale, void* stream);
 
 /* ---- DLRM: embedding bags and the dot interaction ------------- */
-/* pooled[m, :D] = sum_b table[idx[m*ldi + b], :D]; fp32 table [rows, D], bf16 pooled, D = 64. */
+/* pooled[m, :D] = sum_b table[idx[m*ldi + b], :D]; fp32 table [rows, D], bf16 pooled, D = 64.
+ * An index outside [0, rows) contributes nothing (gather) / updates nothing (scatter) and
+ * is counted; the host reads the count with gpp_embbag_bad_indices and raises (the
+ * oracle's torch.nn.functional.embedding_bag raises IndexError on such input). */
+int gpp_embbag_bad_indices(uint64_t* count, int reset);
 int gpp_embbag_fwd(void* out, int64_t ldo, const float* table, const int64_t* idx, int64_t ldi,
                    int64_t M, int64_t bag, int64_t D, int64_t rows, void* stream);
 /* Synchronous sparse SGD: table[idx[m, b], :] -= lr * dpooled[m, :] for all (m, b)

@@ -34,7 +34,13 @@ class ReferenceModel:
             for name, t in init_params(wl.layers[o], o, seed):
                 self.params[(o, name)] = t.clone().requires_grad_(True)
 
-    def loss(self, batch: dict[str, torch.Tensor]) -> torch.Tensor:
+    def loss(self, batch: dict[str, torch.Tensor], relu_masks: dict | None = None) -> torch.Tensor:
+        """``relu_masks`` (op -> bool [B, width], global sample order): take the ReLU
+        pattern of those ops from the device run instead of recomputing it.  A ReLU's
+        gradient is discontinuous at 0, so a pre-activation within bf16 rounding of zero
+        may land on either side under a different (equally valid) summation order and
+        move a whole gradient row; with the device's own masks the comparison measures
+        the arithmetic, not those coin flips."""
         wl, g, P = self.wl, self.wl.graph, self.params
         B = wl.mini_batch
         out: dict[int, torch.Tensor] = {}
@@ -49,7 +55,10 @@ class ReferenceModel:
             if spec.kind == "dense":
                 w = _round(P[(o, "w")], self.bf16)
                 z = x @ w.t() + P[(o, "b")]
-                y = torch.relu(z) if spec.act == "relu" else (torch.nn.functional.gelu(z, approximate="tanh") if spec.act == "gelu" else z)
+                if spec.act == "relu" and relu_masks is not None and o in relu_masks:
+                    y = z * relu_masks[o].to(z.dtype)
+                else:
+                    y = torch.relu(z) if spec.act == "relu" else (torch.nn.functional.gelu(z, approximate="tanh") if spec.act == "gelu" else z)
                 out[o] = _round(y, self.bf16)
             elif spec.kind == "concat":
                 out[o] = torch.cat([out[u] for u in g.predecessors(o)], dim=1)
@@ -113,11 +122,11 @@ class ReferenceModel:
             for k, p in self.params.items():
                 p.copy_(params[k].detach().float().cpu().reshape(p.shape))
 
-    def step(self, batch, lr: float):
+    def step(self, batch, lr: float, relu_masks: dict | None = None):
         """loss, grads (dict) and the SGD update applied in place."""
         for p in self.params.values():
             p.grad = None
-        loss = self.loss(batch)
+        loss = self.loss(batch, relu_masks)
         loss.backward()
         grads = {k: p.grad.detach().clone() for k, p in self.params.items()}
         with torch.no_grad():

@@ -2,10 +2,17 @@
 // gather-sum, its sparse SGD scatter, and the pairwise dot interaction.
 // All HBM / latency bound: warp-per-bag with 8-byte vector row loads, ILP over the
 // bag, warp-per-sample interaction staged through padded shared memory.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace gpp {
 namespace {
+
+// Count of out-of-range embedding indices seen by the gather / scatter kernels since the
+// last gpp_embbag_bad_indices() read.  Such a bag element contributes nothing and updates
+// nothing (PyTorch's embedding_bag raises on them; the host API raises on a nonzero count).
+__device__ unsigned long long g_bad_indices = 0;
 
 // pooled[m, :D] = sum_b table[idx[m, b], :D]   (fp32 table, bf16 pooled, D = 64)
 __global__ void __launch_bounds__(256) embbag_fwd_kernel(bf16* __restrict__ out, int64_t ldo,
@@ -21,22 +28,26 @@ __global__ void __launch_bounds__(256) embbag_fwd_kernel(bf16* __restrict__ out,
   for (int b0 = 0; b0 < bag; b0 += 32) {
     const int nb = bag - b0 < 32 ? bag - b0 : 32;
     int64_t my = lane < nb ? __ldg(ix + b0 + lane) : 0;
-    if (my < 0 || my >= rows) my = 0;  // defensive: never read out of the table
+    const bool bad = my < 0 || my >= rows;
+    if (bad) atomicAdd(&g_bad_indices, 1ull);
+    my = bad ? -1 : my;  // -1: contributes zero, never read out of the table
     int b = 0;
     for (; b + 4 <= nb; b += 4) {
       const int64_t r0 = __shfl_sync(0xffffffffu, my, b);
       const int64_t r1 = __shfl_sync(0xffffffffu, my, b + 1);
       const int64_t r2 = __shfl_sync(0xffffffffu, my, b + 2);
       const int64_t r3 = __shfl_sync(0xffffffffu, my, b + 3);
-      const float2 v0 = __ldg(reinterpret_cast<const float2*>(table + r0 * 64) + lane);
-      const float2 v1 = __ldg(reinterpret_cast<const float2*>(table + r1 * 64) + lane);
-      const float2 v2 = __ldg(reinterpret_cast<const float2*>(table + r2 * 64) + lane);
-      const float2 v3 = __ldg(reinterpret_cast<const float2*>(table + r3 * 64) + lane);
+      const float2 z = make_float2(0.f, 0.f);
+      const float2 v0 = r0 >= 0 ? __ldg(reinterpret_cast<const float2*>(table + r0 * 64) + lane) : z;
+      const float2 v1 = r1 >= 0 ? __ldg(reinterpret_cast<const float2*>(table + r1 * 64) + lane) : z;
+      const float2 v2 = r2 >= 0 ? __ldg(reinterpret_cast<const float2*>(table + r2 * 64) + lane) : z;
+      const float2 v3 = r3 >= 0 ? __ldg(reinterpret_cast<const float2*>(table + r3 * 64) + lane) : z;
       acc.x += (v0.x + v1.x) + (v2.x + v3.x);
       acc.y += (v0.y + v1.y) + (v2.y + v3.y);
     }
     for (; b < nb; ++b) {
       const int64_t r = __shfl_sync(0xffffffffu, my, b);
+      if (r < 0) continue;
       const float2 v = __ldg(reinterpret_cast<const float2*>(table + r * 64) + lane);
       acc.x += v.x;
       acc.y += v.y;
@@ -60,9 +71,13 @@ __global__ void __launch_bounds__(256) embbag_sgd_kernel(float* __restrict__ tab
   for (int b0 = 0; b0 < bag; b0 += 32) {
     const int nb = bag - b0 < 32 ? bag - b0 : 32;
     int64_t my = lane < nb ? __ldg(ix + b0 + lane) : 0;
-    if (my < 0 || my >= rows) my = 0;
+    if (my < 0 || my >= rows) {  // skipped (never redirected to row 0), counted for the host
+      atomicAdd(&g_bad_indices, 1ull);
+      my = -1;
+    }
     for (int b = 0; b < nb; ++b) {
       const int64_t r = __shfl_sync(0xffffffffu, my, b);
+      if (r < 0) continue;
       float* p = table + r * 64 + 2 * lane;
       atomicAdd(reinterpret_cast<float2*>(p), u);
     }
@@ -213,6 +228,22 @@ using namespace gpp;
 
 extern "C" {
 
+int gpp_embbag_bad_indices(uint64_t* count, int reset) {
+  GPP_ARG_CHECK(count, "bad argument");
+  unsigned long long v = 0;
+  cudaError_t e = cudaMemcpyFromSymbol(&v, g_bad_indices, sizeof(v));
+  if (e == cudaSuccess && reset && v) {
+    const unsigned long long zero = 0;
+    e = cudaMemcpyToSymbol(g_bad_indices, &zero, sizeof(zero));
+  }
+  if (e != cudaSuccess) {
+    set_error(std::string("gpp_embbag_bad_indices: ") + cudaGetErrorString(e));
+    return GPP_ERR_CUDA;
+  }
+  *count = v;
+  return GPP_OK;
+}
+
 int gpp_embbag_fwd(void* out, int64_t ldo, const float* table, const int64_t* idx, int64_t ldi,
                    int64_t M, int64_t bag, int64_t D, int64_t rows, void* stream) {
   GPP_ARG_CHECK(out && table && idx && M > 0 && bag > 0, "bad argument");
@@ -248,7 +279,9 @@ int gpp_interaction_fwd(void* out, int64_t ldo, int64_t out_cols, const void* z,
 int gpp_interaction_bwd(void* dz, int64_t lddz, const void* dout, int64_t lddo, const void* z,
                         int64_t ldz, int64_t M, int64_t F, int64_t D, int mask_first, void* stream) {
   GPP_ARG_CHECK(dz && dout && z && M > 0 && F >= 2 && D == 64, "bad argument");
-  if (F == 27) {  // DLRM: 26 tables + the bottom MLP
+  // GPP_INTERACTION_GENERIC=1 forces the generic kernel (tests assert both are bit-identical)
+  const char* gen = getenv("GPP_INTERACTION_GENERIC");
+  if (F == 27 && !(gen && gen[0] == '1')) {  // DLRM: 26 tables + the bottom MLP
     interaction_bwd_reg_kernel<27><<<static_cast<unsigned>((M + 3) / 4), 128, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<bf16*>(dz), lddz, static_cast<const bf16*>(dout), lddo, static_cast<const bf16*>(z), ldz, M,
         mask_first);

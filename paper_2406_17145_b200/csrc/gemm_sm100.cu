@@ -1014,10 +1014,7 @@ static float* splitk_workspace(size_t floats, cudaStream_t stream) {
     return nullptr;
   }
   size_t want = floats < (size_t(16) << 20) ? (size_t(16) << 20) : floats;
-  if (bufs[dev]) {
-    cudaStreamSynchronize(stream);
-    cudaFree(bufs[dev]);
-  }
+  // the old buffer is retired, not freed: graphs captured earlier may still reference it
   if (cudaMalloc(&bufs[dev], want * sizeof(float)) != cudaSuccess) {
     bufs[dev] = nullptr;
     caps[dev] = 0;

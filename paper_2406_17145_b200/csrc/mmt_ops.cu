@@ -311,22 +311,30 @@ __global__ void meanpool_bwd_kernel(bf16* __restrict__ dx, const bf16* __restric
   }
 }
 
-float* ln_scratch(size_t floats) {
+// Per-device scratch for the LayerNorm-backward dgamma/dbeta partials.  Grows only outside
+// CUDA-graph capture and never frees: a graph captured earlier may still reference the old
+// buffer, so a grown-out buffer is retired (kept allocated) instead of released.
+float* ln_scratch(size_t floats, cudaStream_t stream) {
   static float* bufs[64] = {nullptr};
   static size_t caps[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (caps[dev] < floats) {
-    if (bufs[dev]) cudaFree(bufs[dev]);
-    size_t want = floats < (size_t(4) << 20) ? (size_t(4) << 20) : floats;
-    if (cudaMalloc(&bufs[dev], want * sizeof(float)) != cudaSuccess) {
-      bufs[dev] = nullptr;
-      caps[dev] = 0;
-      return nullptr;
-    }
-    caps[dev] = want;
+  if (caps[dev] >= floats) return bufs[dev];
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &st);
+  if (st != cudaStreamCaptureStatusNone) {
+    set_error("LayerNorm scratch must be sized before CUDA-graph capture (run one eager step first)");
+    return nullptr;
   }
-  return bufs[dev];
+  size_t want = floats < (size_t(4) << 20) ? (size_t(4) << 20) : floats;
+  float* p = nullptr;
+  if (cudaMalloc(&p, want * sizeof(float)) != cudaSuccess) {
+    set_error("LayerNorm scratch allocation failed");
+    return nullptr;
+  }
+  bufs[dev] = p;
+  caps[dev] = want;
+  return p;
 }
 
 }  // namespace
@@ -366,8 +374,8 @@ int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, con
   // 56 rows, 147 blocks; 64 rows left 20 SMs idle)
   const int rpb = static_cast<int>(std::max<int64_t>(8, ((T + 147) / 148 + 7) / 8 * 8));
   const int nblk = static_cast<int>((T + rpb - 1) / rpb);
-  float* part = ln_scratch(static_cast<size_t>(nblk) * 2 * D);
-  if (!part) { set_error("layernorm scratch allocation failed"); return GPP_ERR_CUDA; }
+  float* part = ln_scratch(static_cast<size_t>(nblk) * 2 * D, s);
+  if (!part) return GPP_ERR_CUDA;
   const size_t smem = 8 * 2 * D * sizeof(float);
   const int d = static_cast<int>(D);
   auto* dxp = static_cast<bf16*>(dx);

@@ -507,6 +507,12 @@ extern "C" {
 
 int gpp_version(void) { return 1; }
 
+#ifndef GPP_SOURCE_DIGEST
+#define GPP_SOURCE_DIGEST "unknown"
+#endif
+/* digest of the sources this binary was built from (checked by _build.py / lib.load) */
+const char* gpp_source_digest(void) { return "gpp-digest:" GPP_SOURCE_DIGEST; }
+
 int gpp_gemm_prefetch_hint(const void* ptr, int64_t bytes) {
   g_pf_ptr = ptr;
   g_pf_bytes = ptr ? bytes : 0;

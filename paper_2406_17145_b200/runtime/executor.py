@@ -163,6 +163,9 @@ class Executor:
         self.keep_grads = keep_grads
         self._fuse_req = fuse_optimizer
         self._transport_kind = transport
+        # test hook: when a dict, every dense op's forward output is copied into it under
+        # (op, task) -- the oracle takes the device's ReLU masks from these (tests only)
+        self.tap: dict | None = None
         g = wl.graph
         self.owner = {op: st.id for st in sg.stages for op in st.op_ids}
         mine = [st for st in sg.stages if rank in st.devices]
@@ -210,6 +213,10 @@ class Executor:
                     pairs.add((c, p))
         dp_groups = [tuple(sorted(st.devices)) for st in self.sg.stages if st.dp_degree > 1]
         kind = self._transport_kind
+        if callable(kind):  # an injected transport (tests: host-staged gloo, ranks sharing a GPU)
+            self.tp = kind(self.rank, pairs, dp_groups, self.dev)
+            self.dp_group = getattr(self.tp, "dp", None)
+            return
         if kind == "auto":
             kind = "nccl" if self.dev.type == "cuda" else "torch"
         if kind == "nccl":
@@ -485,6 +492,8 @@ class Executor:
                 x = self._input(o, j, slot, batch)
                 pre = self.pre[o][slot] if o in self.pre else None
                 be.linear_fwd(self.out[o][slot], x, self.W[(o, "w")], self.P[(o, "b")], spec.act, pre=pre)
+                if self.tap is not None:
+                    self.tap[(o, j)] = self.out[o][slot].detach().clone()
             elif spec.kind == "concat":
                 off, dst, src, pdst, psrc = 0, [], [], [], []
                 for u in self.wl.graph.predecessors(o):

@@ -25,6 +25,7 @@ _vp, _i64, _i32, _f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_
 
 _SIGS = {
     "gpp_version": ([], _i32),
+    "gpp_source_digest": ([], ctypes.c_char_p),
     "gpp_last_error": ([], ctypes.c_char_p),
     "gpp_launch_count": ([], ctypes.c_uint64),
     "gpp_linear_fwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
@@ -64,6 +65,7 @@ _SIGS = {
     "gpp_attn_bwd": ([_vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_attn_softmax": ([_vp, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp, _vp], _i32),
     "gpp_attn_softmax_bwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp, _vp], _i32),
+    "gpp_embbag_bad_indices": ([ctypes.POINTER(ctypes.c_uint64), _i32], _i32),
     "gpp_embbag_fwd": ([_vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp], _i32),
     "gpp_embbag_sgd": ([_vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_interaction_fwd": ([_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
@@ -87,6 +89,13 @@ def load(path: str | os.PathLike | None = None):
             f"libgpp_b200.so not found at {p}; build it with "
             "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
         )
+    if path is None and os.environ.get("GPP_ALLOW_STALE_LIB") != "1":
+        from .. import _build
+
+        if _build.CSRC.exists() and not _build.binary_is_current(p):
+            raise RuntimeError(
+                f"{p} was not built from the current csrc/ sources (digest mismatch); rebuild with "
+                "`python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(str(p))
     for name, (args, res) in _SIGS.items():
         fn = getattr(lib, name, None)
@@ -249,6 +258,15 @@ def embbag_sgd(table, dpooled, idx, lr, stream=None):
     M, bag = idx.shape
     call("gpp_embbag_sgd", _ptr(table), _ptr(dpooled), _ld(dpooled), _ptr(idx), _ld(idx), M, bag,
          table.shape[1], table.shape[0], float(lr), _stream(stream))
+
+
+def embbag_check_indices(reset: bool = True) -> None:
+    """Raise IndexError if any gather / scatter since the last check saw an index outside
+    its table (those bag elements were skipped, never redirected; synchronising read)."""
+    n = ctypes.c_uint64(0)
+    call("gpp_embbag_bad_indices", ctypes.byref(n), 1 if reset else 0)
+    if n.value:
+        raise IndexError(f"embedding bag: {n.value} indices out of range of their table")
 
 
 def interaction_fwd(out, z, F, out_cols, stream=None):

@@ -246,9 +246,10 @@ def test_wgrad_sgd_fast_path(cuda_lib, N, K, M):
     assert torch.equal(shadow, master.bfloat16())
 
 
-def test_embbag_and_interaction_kernels(cuda_lib):
+@pytest.mark.parametrize("F", [7, 26, 27])
+def test_embbag_and_interaction_kernels(cuda_lib, F, monkeypatch):
     g = torch.Generator(device="cuda").manual_seed(21)
-    rows, M, bag, F = 5000, 300, 100, 27
+    rows, M, bag = 5000, 300, 100
     table = torch.randn(rows, 64, device="cuda", generator=g)
     idx = torch.randint(0, rows, (M, bag), device="cuda", generator=g)
     out = torch.empty(M, 64, device="cuda", dtype=torch.bfloat16)
@@ -263,7 +264,7 @@ def test_embbag_and_interaction_kernels(cuda_lib):
     torch.cuda.synchronize()
     assert torch.allclose(t2, exp, rtol=1e-5, atol=1e-5)
     z = torch.randn(M, F * 64, device="cuda", generator=g).bfloat16()
-    cols = 416
+    cols = 64 + F * (F - 1) // 2 + 1
     o = torch.empty(M, cols, device="cuda", dtype=torch.bfloat16)
     cuda_lib.interaction_fwd(o, z, F, cols)
     zz = z.float().reshape(M, F, 64)
@@ -284,6 +285,33 @@ def test_embbag_and_interaction_kernels(cuda_lib):
     gref[:, 0] *= (zz[:, 0] > 0).float()
     torch.cuda.synchronize()
     assert _rel(dz.float().reshape(M, F, 64), gref) < 1e-2
+    # the register-tiled F=27 kernel and the generic smem kernel: bit-identical
+    monkeypatch.setenv("GPP_INTERACTION_GENERIC", "1")
+    dz_gen = torch.empty_like(z)
+    cuda_lib.interaction_bwd(dz_gen, dout, z, F, True)
+    torch.cuda.synchronize()
+    assert torch.equal(dz_gen, dz)
+
+
+def test_embbag_bad_indices_skipped_and_reported(cuda_lib):
+    """Out-of-range indices are skipped (never redirected to row 0) and reported."""
+    rows = 100
+    table = torch.randn(rows, 64, device="cuda")
+    idx = torch.tensor([[1, 2, rows], [-1, 3, 4]], device="cuda")
+    cuda_lib.embbag_check_indices()  # clear
+    out = torch.empty(2, 64, device="cuda", dtype=torch.bfloat16)
+    cuda_lib.embbag_fwd(out, table, idx)
+    with pytest.raises(IndexError):
+        cuda_lib.embbag_check_indices()
+    exp = torch.stack([table[1] + table[2], table[3] + table[4]])
+    assert torch.allclose(out.float(), exp, rtol=1e-2, atol=1e-2)
+    t2 = table.clone()
+    cuda_lib.embbag_sgd(t2, torch.ones(2, 64, device="cuda", dtype=torch.bfloat16), idx, 1.0)
+    with pytest.raises(IndexError):
+        cuda_lib.embbag_check_indices()
+    assert torch.equal(t2[0], table[0]) and torch.equal(t2[rows - 1], table[rows - 1])
+    assert torch.allclose(t2[1], table[1] - 1)
+    cuda_lib.embbag_check_indices()  # reset by the previous read: no error
 
 
 @pytest.mark.parametrize("D", [128, 1024])
