@@ -2,23 +2,30 @@
 """Benchmark: GPP training throughput on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
-                    [--workload candle|toy] [--mode gpp|spp]
+                    [--workload all|mmt|candle|dlrm|toy] [--mode gpp|spp]
 
-One process per GPU (torchrun for N > 1).  A "step" is one synchronous training
-iteration of the workload's configured StageGraph: every stage's kFkB task
-list, the P2P activation/gradient transfers, the DP all-reduce and the SGD
-update.  Workload at N GPUs: CANDLE-Uno (BASELINE configs[1]) with mini-batch
-1024*N (PAPER.md:1100 scales B with the device count; 4096 at 4 GPUs), random
-init, synthetic N(0,1) features.
+One process per GPU.  ``--gpus N`` with N > 1 outside torchrun re-launches this
+script under ``torch.distributed.run`` (127.0.0.1) with N ranks; every rank
+checks WORLD_SIZE == N.  A "step" is one synchronous training iteration of the
+workload's configured StageGraph: every stage's kFkB task list, the P2P
+activation/gradient transfers, the DP all-reduce and the SGD update.
 
-value : samples/s with the inputs already resident in HBM (CUDA events, max
-        over ranks; per-iteration working set = 0.94 GB bf16 weights + 1.9 GB
-        fp32 master/grad >> 126 MB L2, so every timed step starts L2-cold).
-e2e   : same metric through the public API with pinned HOST buffers: every
-        step's H2D input copy (double-buffered on a copy stream) and the D2H
-        loss read are inside the timed region.
---impl reference : the CPU path (oracle/reference_model.py: the monolithic
-        torch-CPU training step) on a bounded sample, rank 0 only.
+Headline: the Multi-Modal Transformer (BASELINE configs[2], the north-star
+target: 4 branches x 12 pre-LN layers, d=1024, S=512), mini-batch 16 per GPU
+(weak scaling; PAPER.md:1099-1101 doubles B per doubling of devices).  With the
+default ``--workload all`` the line carries ``sub_results`` for CANDLE-Uno
+(configs[1], B = 1024 N) and DLRM (configs[3], B = 8192 N), each with its own
+value / e2e / roofline / cpu_baseline / GPP-vs-SPP fields.  Strategies come from
+the frozen StrategyFiles in profiles/strategies/ (planned afresh if stale).
+
+value : samples/s with the inputs already resident in HBM, the iteration replayed
+        from a CUDA graph, CUDA events, max over ranks (the per-step working set —
+        weights + fp32 master/grad — is GBs >> the 126 MB L2: every step is L2-cold).
+e2e   : the same metric through the public API ``runtime.api.execute``: pinned host
+        batches, each step's H2D copy (double-buffered) and the loss D2H inside the
+        timed region.
+--impl reference : the CPU path (the monolithic torch-CPU training step of the
+        workload, native bf16 on the host cores) on a bounded sample, rank 0 only.
 """
 
 from __future__ import annotations
@@ -39,6 +46,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+CPU_SAMPLE = {"mmt": 2, "candle": 256, "dlrm": 1024, "toy": 64}  # per CPU step (bounded sample)
 
 
 def _peaks():
@@ -159,44 +167,61 @@ def _workload(name: str, world: int, per_gpu: int | None, branches: int | None =
     raise SystemExit(f"unknown workload {name}")
 
 
-def cpu_reference_run(wl_name: str, sample_B: int, steps: int, min_seconds: float = 0.0, warmup: int = 1):
-    """Time the reference's CPU path (monolithic torch-CPU step) on a bounded sample:
-    ``steps`` steps, continued until at least ``min_seconds`` of CPU work are timed.
-    Returns (samples/s, seconds, steps run)."""
+def _describe(wl, branches=None) -> str:
+    if wl.name == "candle":
+        return "candle: 7 towers x 4 x Linear(4096,4096)+ReLU -> concat -> Linear(28672,1024)+ReLU -> Linear(1024,1) MSE"
+    if wl.name == "mmt":
+        return (f"mmt: {branches or 4} branches x 12 pre-LN encoder layers (d=1024, 16 heads, FFN 4096 GELU, S=512) "
+                "-> mean-pool -> concat -> Linear(., 1000) CE")
+    if wl.name == "dlrm":
+        return "dlrm: bottom 13->4096x3->64, 26 x 1M x 64 fp32 tables bag 100 (sum), dot interaction 415, top 416->4096x3->1 BCE"
+    return wl.name
+
+
+def cpu_reference_run(wl_name: str, sample_B: int, steps: int, min_seconds: float = 0.0, warmup: int = 1,
+                      branches: int | None = None):
+    """Time the reference's CPU path (the monolithic torch-CPU training step of the same
+    model, parameters and activations in native bf16 on the host cores, all threads) on
+    a bounded sample: ``steps`` steps of ``sample_B`` samples, continued until at least
+    ``min_seconds`` are timed.  Returns (samples/s, seconds, steps run, threads)."""
     from oracle.reference_model import ReferenceModel
     from paper_2406_17145_b200.runtime.data import make_batch
 
     torch.set_num_threads(os.cpu_count() or 1)
-    wl = _workload(wl_name, 1, sample_B)
-    ref = ReferenceModel(wl)
-    for w in range(max(1, warmup)):  # warm-up (allocations, thread pools)
-        ref.step(make_batch(wl, 10_000 + w), 1e-3)
+    wl = _workload(wl_name, 1, sample_B, branches)
+    ref = ReferenceModel(wl, native_bf16=True)
+    batches = [make_batch(wl, i) for i in range(2)]
+    for w in range(max(1, warmup)):  # warm-up (allocations, thread pools, oneDNN kernels)
+        ref.step(batches[w % 2], 1e-4)
     t0 = time.perf_counter()
     n = 0
     while n < steps or (time.perf_counter() - t0 < min_seconds and n < 1000):
-        ref.step(make_batch(wl, n + 1), 1e-3)
+        ref.step(batches[n % 2], 1e-4)
         n += 1
     dt = time.perf_counter() - t0
-    return sample_B * n / dt, dt, n
+    return sample_B * n / dt, dt, n, torch.get_num_threads()
 
 
 def run_reference(args, rank, world):
+    """--impl reference: rank 0 times the CPU path of the headline workload; others exit."""
     if rank != 0:
         return
-    sample = {"candle": 32, "toy": 64, "dlrm": 16, "mmt": 1}[args.workload]
-    # every step is one bounded CPU sample of the workload (B = sample); K steps
-    val, dt, n_run = cpu_reference_run(args.workload, sample, max(1, min(args.steps, 50)),
-                                       warmup=min(args.warmup, 5))
-    cores = torch.get_num_threads()
+    name = "mmt" if args.workload == "all" else args.workload
+    sample = CPU_SAMPLE[name]
+    val, dt, n_run, cores = cpu_reference_run(name, sample, max(1, min(args.steps, 20)),
+                                              warmup=min(args.warmup, 2), branches=args.branches)
+    wl = _workload(name, world, args.per_gpu_batch, args.branches)
     line = {
-        "metric": "train samples/sec", "value": round(val, 3), "unit": "samples/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": n_run, "warmup": min(args.warmup, 5),
+        "metric": "train samples/sec", "value": round(val, 4), "unit": "samples/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": n_run, "warmup": min(args.warmup, 2),
         "ms_per_step": round(1e3 * dt / n_run, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16-emulated fp32 (CPU)", "data": "synthetic",
-        "config": {"workload": f"{args.workload} (CPU sample B={sample} per step)", "device": "host CPU"},
-        "cpu_baseline": {"value": round(val, 3), "unit": "samples/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.workload} mini-batch of {sample} samples, monolithic torch-CPU step"},
-        "e2e": {"value": round(val, 3), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": _describe(wl, args.branches), "global_batch": wl.mini_batch,
+                   "cpu_sample_per_step": sample, "device": "host CPU"},
+        "cpu_baseline": {"value": round(val, 4), "unit": "samples/s", "cores": cores, "kind": "port",
+                         "sample": f"{name}: {n_run} steps x B={sample}, monolithic torch-CPU training step in "
+                                   f"native bf16 (oracle/reference_model.py, native_bf16=True), {dt:.1f}s"},
+        "e2e": {"value": round(val, 4), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -234,37 +259,24 @@ def _gemm_traffic(workload: str) -> dict:
             "traffic_source": "profiles/ncu_step_gemms_r1d_summary.csv"}
 
 
-def _time_arm(wl, world, rank, dev, mode, args, clocks=True):
-    """Plan ``mode`` (gpp | spp) for ``world`` GPUs, build this rank's executor, capture its
-    iteration in a CUDA graph and time ``args.steps`` replays (max over ranks)."""
+def _time_arm(wl, sg, world, rank, dev, args, clocks=True):
+    """Build this rank's executor for ``sg``, capture its iteration in a CUDA graph and time
+    ``args.steps`` replays on device-resident inputs (max over ranks)."""
     from paper_2406_17145_b200.runtime import lib
-    from paper_2406_17145_b200.runtime.api import plan
     from paper_2406_17145_b200.runtime.data import make_batch, to_device_rows
     from paper_2406_17145_b200.runtime.executor import Executor
+    from paper_2406_17145_b200.runtime.graph import GraphedIteration
     from paper_2406_17145_b200.runtime.profiler import TimedBackend
 
-    t_plan = time.perf_counter()
-    strategy = plan(wl, world, mode, costs=args.costs)
-    t_plan = time.perf_counter() - t_plan
-    sg = strategy.stage_graph
     be = TimedBackend(dev)
     be.enabled = False
     ex = Executor(wl, sg, rank, world, be, lr=1e-4)
     keys = set(ex.data_keys()) if ex.stage else set()
-    full = make_batch(wl, 0, keys=keys)
-    dev_batch = to_device_rows(ex, full, ex.dtype, dev) if ex.stage else {}
-    graphed = None
-    graphed_launches = 0
-    if not args.no_graph and (ex.stage is not None or world > 1):
-        from paper_2406_17145_b200.runtime.graph import GraphedIteration
-
-        n_before = lib.launch_count()
-        ex.run_iteration(dev_batch)
-        graphed_launches = lib.launch_count() - n_before  # libgpp kernels per iteration
-        graphed = GraphedIteration(ex, dev_batch)
-        for b in graphed.bufs:
-            for k in b:
-                b[k].copy_(dev_batch[k])
+    dev_batch = to_device_rows(ex, make_batch(wl, 0, keys=keys), ex.dtype, dev) if ex.stage else {}
+    n0 = lib.launch_count()
+    ex.run_iteration(dev_batch)
+    per_iter = lib.launch_count() - n0  # this rank's libgpp kernels per iteration
+    graphed = None if args.no_graph else GraphedIteration(ex, dev_batch)
 
     def step(i=0):
         return graphed.replay(i) if graphed is not None else ex.run_iteration(dev_batch)
@@ -277,7 +289,6 @@ def _time_arm(wl, world, rank, dev, mode, args, clocks=True):
     sampler = ClockSampler(dev.index) if clocks else None
     if sampler:
         sampler.start()
-    launches0 = lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nvtx = os.environ.get("GPP_NVTX") == "1"  # ncu --nvtx --nvtx-include "timed/": steady-state launch lists
     torch.cuda.synchronize()
@@ -290,11 +301,9 @@ def _time_arm(wl, world, rank, dev, mode, args, clocks=True):
     torch.cuda.synchronize()
     if nvtx:
         torch.cuda.nvtx.range_pop()
-    launches = lib.launch_count() - launches0
-    if graphed is not None:  # replays launch the captured kernels without host calls
-        launches = graphed_launches * args.steps
     ms = e0.elapsed_time(e1)
     clk = sampler.stop() if sampler else None
+    launches = per_iter * args.steps
     if world > 1:
         dist.barrier()
         t = torch.tensor([ms], device=dev)
@@ -303,31 +312,214 @@ def _time_arm(wl, world, rank, dev, mode, args, clocks=True):
         lt = torch.tensor([float(launches)], device=dev)
         dist.all_reduce(lt)
         launches = int(lt.item())
-    return {"ex": ex, "sg": sg, "graphed": graphed, "dev_batch": dev_batch, "ms": ms, "launches": launches,
-            "clocks": clk, "plan_s": t_plan, "be": be}
+    return {"ex": ex, "graphed": graphed, "dev_batch": dev_batch, "ms": ms, "launches": launches, "clocks": clk,
+            "be": be}
 
 
-def _ncu_cross_check(workload: str, peak: float) -> dict | None:
-    """The committed ncu --set full capture of the CANDLE step's forward tower GEMMs
-    (profiles/ncu_candle_fw_gemm_r1g_summary.csv): per-launch duration without the event
-    nodes the live timing needs (which add ~2-4 us per launch), for comparison."""
-    if workload != "candle":
+def _attn_flops_per_launch(wl, ex) -> dict:
+    """Algorithmic FLOPs of one attention launch on this rank (all heads of a micro-batch):
+    fw = 2 GEMMs (QK^T, PV) = 4 S^2 dh per head; bw = 5 GEMM-equivalents with the
+    recompute of S = QK^T (dV, dP, dQ, dK, S) = 10 S^2 dh per head, 2 without it."""
+    for o in (ex.ops if ex.stage else []):
+        spec = wl.layers[o]
+        if spec.kind == "mmt_layer":
+            S, d, H, _, _ = spec.extra
+            z = ex.m * H
+            return {"attn_fwd": 4.0 * S * S * (d // H) * z, "attn_bwd": 10.0 * S * S * (d // H) * z}
+    return {}
+
+
+def bench_workload(name, args, rank, world, dev, peaks, peak_src, cpu_ok: bool) -> dict | None:
+    from paper_2406_17145_b200.runtime.api import execute, plan_cached, twin
+    from paper_2406_17145_b200.runtime.data import make_batch
+    from paper_2406_17145_b200.runtime.trace import trace_diff
+    from paper_2406_17145_b200.workloads import b200_cluster, with_measured_curves
+
+    wl = _workload(name, world, args.per_gpu_batch, args.branches if name == "mmt" else None)
+    cluster = b200_cluster(world)
+    sg, meta = plan_cached(wl, world, args.mode, costs=args.costs)
+    arm = _time_arm(wl, sg, world, rank, dev, args)
+    ex, be, ms = arm["ex"], arm["be"], arm["ms"]
+    launches, clk, graphed_flag = arm["launches"], arm["clocks"], arm["graphed"] is not None
+    value = wl.mini_batch * args.steps / (ms / 1e3)
+
+    # e2e through the public API: pinned host batches, H2D + loss D2H every step
+    fulls = [make_batch(wl, s + 1, keys=set(ex.data_keys()) if ex.stage else set()) for s in range(2)]
+    rep = execute(sg, cluster, wl, batch_source=lambda i: fulls[i % 2], iters=args.steps, graph=not args.no_graph,
+                  ex=ex)
+    e2e = rep.samples_per_s
+    # one traced iteration: CUDA-event nodes around every kernel (graph-replayed) -> measured
+    # Chrome trace, busy / idle per stage, kernel-family times; diffed against the twin
+    be.reset()
+    trep = execute(sg, cluster, wl, batch_source=lambda i: fulls[i % 2], iters=2, graph=not args.no_graph,
+                   trace=True, ex=ex)
+    summ = be.summary() if ex.stage else {"flops": 0.0, "ms": 0.0, "busy_ms": 0.0, "tflops": 0.0, "launches": 0}
+    sim_graph = with_measured_curves(wl)[0].graph if args.costs == "measured" else wl.graph
+    sim = twin(sg, cluster, sim_graph)
+    tdiff = trace_diff(trep.task_times, sim)
+    if args.trace_out and rank == 0:
+        with open(f"{args.trace_out}.{name}.n{world}.measured.json", "w") as f:
+            f.write(trep.trace)
+        from paper_2406_17145_b200.sim import emit_trace
+
+        with open(f"{args.trace_out}.{name}.n{world}.sim.json", "w") as f:
+            f.write(emit_trace(sim))
+    # the same iteration's dense GEMMs replayed back to back from one graph (no event nodes)
+    alone = None
+    if ex.stage is not None:
+        try:
+            alone = be.time_gemms_alone(lambda: ex.run_iteration(arm["dev_batch"]))
+        except Exception as exc:  # noqa: BLE001 - report, keep the event-node figure
+            alone = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+    # attention kernels (MMT): algorithmic FLOPs / event-node durations of the traced iteration
+    attn = {}
+    fl = _attn_flops_per_launch(wl, ex)
+    for k, f in fl.items():
+        o = summ.get("other_ms", {}).get(k)
+        if o and o["launches"]:
+            us = 1e3 * o["ms"] / o["launches"]
+            attn[k] = {"launches_per_step": o["launches"], "avg_us": round(us, 2),
+                       "tflops": round(f / (us * 1e-6) / 1e12, 1), "frac_burst": round(f / (us * 1e-6) / 1e12 / peaks["bf16_tflops"], 4),
+                       "ms_per_step": round(o["ms"], 3)}
+    t_iter = ms / args.steps
+    busy = summ["busy_ms"]
+    bt = torch.tensor([busy], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(bt)
+    bubble = max(0.0, 1.0 - float(bt.item()) / (world * t_iter))
+    t_roof = wl.mini_batch * (wl.flops_per_sample / (peaks["bf16_tflops_sustained"] * 1e12)
+                              + wl.bytes_per_sample / (peaks["hbm_gbs"] * 1e9)) / world * 1e3
+
+    spp = None
+    if world > 1 and args.mode == "gpp" and not args.no_spp:
+        gpp_sg = [(sorted(s.op_ids), s.micro_batch, s.sched_cfg.k if s.sched_cfg else None) for s in sg.stages]
+        del arm, ex, be
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        ssg, smeta = plan_cached(wl, world, "spp", costs=args.costs)
+        sp = _time_arm(wl, ssg, world, rank, dev, args, clocks=False)
+        spp_value = wl.mini_batch * args.steps / (sp["ms"] / 1e3)
+        sp_sg = [(sorted(s.op_ids), s.micro_batch, s.sched_cfg.k if s.sched_cfg else None) for s in ssg.stages]
+        spp = {"value": round(spp_value, 3), "ms_per_step": round(sp["ms"] / args.steps, 4),
+               "gpp_vs_spp_speedup": round(value / spp_value, 4), "plan": smeta.get("source"),
+               "stages": [{"ops": len(s.op_ids), "b": s.micro_batch, "d": s.dp_degree} for s in ssg.stages],
+               # the runtime sweep keeps a sequential candidate when the twin rates it faster;
+               # equal (op sets, micro-batch, k) per stage and equal edges = the same pipeline
+               "gpp_picked_sequential": (gpp_sg, sorted(sg.edges)) == (sp_sg, sorted(ssg.edges)),
+               "note": "SPP = spp_optimize (SPEC.md:384-392) strategy on this same runtime, CUDA-graph replay"}
+        del sp
+        gc.collect()
+        torch.cuda.empty_cache()
+    if rank != 0:
         return None
-    import csv
+    cpu = None
+    if cpu_ok and world == 1 and not args.no_cpu_baseline:
+        sample = CPU_SAMPLE[name]
+        cv, cdt, cn, cores = cpu_reference_run(name, sample, 2, min_seconds=args.cpu_seconds,
+                                               branches=args.branches if name == "mmt" else None)
+        cpu = {"value": round(cv, 4), "unit": "samples/s", "cores": cores, "kind": "port",
+               "sample": f"{name}: {cn} steps x B={sample}, monolithic torch-CPU training step in native bf16 "
+                         f"(oracle/reference_model.py, native_bf16=True), {cdt:.1f}s"}
+    peak = peaks["bf16_tflops"]  # the GEMMs are timed ALONE (back to back): the burst figure
+    achieved = alone["tflops"] if alone and alone.get("tflops") else summ["tflops"]
+    gp = meta.get("gpp_partitioner")
+    line = {
+        "metric": "train samples/sec", "value": round(value, 3), "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t_iter, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16" if wl.dtype != "fp32" else "fp32", "data": "synthetic",
+        "config": {
+            "workload": _describe(wl, args.branches), "global_batch": wl.mini_batch, "mode": args.mode,
+            "parallelism": f"{args.mode} stages={len(sg.stages)} depth={sim.depth}",
+            "stages": [{"ops": len(s.op_ids), "b": s.micro_batch, "d": s.dp_degree,
+                        "inflight": s.sched_cfg.inflight_samples} for s in sg.stages],
+            "plan": {k: v for k, v in meta.items() if k != "gpp_partitioner"},
+            "gpp_partitioner": None if gp is None else {"twin_ms": gp["twin_ms"],
+                                                        "stages": [{"ops": len(s["ops"]), "b": s["b"], "d": len(s["devices"])}
+                                                                   for s in gp["stages"]]},
+            "l2": {"candle": "per-step working set (weights+master+grads ~2.9 GB) >> 126 MB L2",
+                   "dlrm": "per-step working set (26 x 256 MB fp32 tables + MLP master/grads) >> 126 MB L2",
+                   "mmt": "per-step working set (48 layers x ~150 MB master/grad/shadow + activations) >> 126 MB L2",
+                   "toy": "toy model fits in L2 (launch-bound; no roofline claim)"}.get(name),
+            "optimizer": "SGD fp32 master + bf16 shadow (fused into the last wgrad epilogue when DP=1)",
+            "cuda_graph": graphed_flag, "costs": args.costs,
+        },
+        "e2e": {"value": round(e2e, 3), "unit": "samples/s", "h2d_bytes_per_step": rep.h2d_bytes_per_step,
+                "d2h_bytes_per_step": rep.d2h_bytes_per_step, "api": "paper_2406_17145_b200.runtime.api.execute"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "kernel": "gemm_tc_pair_kernel / gemm_tc_kernel (tcgen05 bf16 GEMM family: every dense "
+                                                  "fw / dgrad / wgrad(+SGD) launch of the iteration)",
+                     "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+                     "frac": round(achieved / peak, 4) if peak else None,
+                     **(_gemm_traffic(name)),
+                     "peak_source": f"{peak_src} bf16_tflops (burst: the GEMMs are replayed alone)",
+                     "timing": "one iteration's GEMM launches replayed back to back from a CUDA graph, CUDA events "
+                               "around the replay (gemms_alone)",
+                     "gemms_alone": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in (alone or {}).items()},
+                     "achieved_event_nodes": round(summ["tflops"], 2),
+                     "share_of_step": round(summ["ms"] / t_iter, 4) if t_iter > 0 else None,
+                     "attention": attn or None,
+                     "by_kind": summ.get("by_kind", {}), "other_kernels_ms": summ.get("other_ms", {})},
+        "clocks": clk,
+        "step_roofline": {"t_roof_ms": round(t_roof, 4), "frac": round(t_roof / t_iter, 4),
+                          "flops_per_sample": wl.flops_per_sample, "bytes_per_sample": wl.bytes_per_sample,
+                          "note": "summed stage-compute roofline: B*(F/P_sustained + bytes/BW_hbm)/N vs measured step"},
+        "bubble": {"measured": round(bubble, 4), "model": round(sim.bubble_fraction, 4),
+                   "note": "1 - sum over ranks of kernel busy time / (N * step time); kernel time from CUDA-event "
+                           "nodes around every kernel of a graph-replayed iteration"},
+        "report": {"iteration_ms": round(trep.iteration_ms, 4), "peak_inflight_samples": trep.peak_inflight_samples,
+                   "busy_ms": {k: round(v, 4) for k, v in trep.busy_ms.items()},
+                   "idle_ms": {k: round(v, 4) for k, v in trep.idle_ms.items()},
+                   "peak_mem_gb": {k: round(v / 1e9, 2) for k, v in trep.peak_mem_bytes.items()},
+                   "warm_up_microbatches": trep.warm_up_microbatches, "depth": trep.depth,
+                   "note": "runtime.api.execute(trace=True) RunReport (SimReport fields, measured)"},
+        "trace_vs_sim": tdiff,
+        "sim": {"iteration_ms_model": round(sim.iteration_ms, 4), "bubble_fraction_model": round(sim.bubble_fraction, 4)},
+        "spp": spp,
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    return line
 
-    path = os.path.join(ROOT, "profiles", "ncu_candle_fw_gemm_r1g_summary.csv")
-    try:
-        rows = list(csv.reader(open(path)))
-    except OSError:
+
+def _spawn_ranks(args) -> int:
+    """``--gpus N`` (N > 1) outside torchrun: re-launch this script with N ranks under
+    torch.distributed.run on 127.0.0.1 and return its exit code."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def _init_ranks(args, rank, world, local):
+    """One process per GPU: NCCL (or gloo for --dry-run) process group; every rank prints
+    its init line so the rank/world check is observable."""
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun --nproc-per-node "
+                         f"{args.gpus} (or without torchrun and let bench.py spawn the ranks)")
+    if args.dry_run:
+        if world > 1:
+            dist.init_process_group("gloo")
+        print(f"[bench] rank {rank}/{world} backend={'gloo' if world > 1 else 'none'} dry-run pid={os.getpid()}",
+              file=sys.stderr, flush=True)
         return None
-    h = rows[0]
-    us = [float(r[h.index("gpu__time_duration.sum")].split()[0]) for r in rows[1:]]
-    tens = [float(r[h.index("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")].split()[0]) for r in rows[1:]]
-    avg = sum(us) / len(us)
-    tf = 2.0 * 1024 * 4096 * 4096 / (avg * 1e-6) / 1e12
-    return {"kernel": "fw tower GEMM 1024x4096x4096 (+bias+ReLU)", "us": round(avg, 2), "tflops": round(tf, 1),
-            "frac": round(tf / peak, 4), "tensor_pipe_active_pct": round(sum(tens) / len(tens), 1),
-            "source": "profiles/ncu_candle_fw_gemm_r1g_summary.csv"}
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nccl = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        nccl = ".".join(str(x) for x in torch.cuda.nccl.version())
+    print(f"[bench] rank {rank}/{world} on cuda:{local} ({torch.cuda.get_device_name(dev)}) "
+          f"backend={'nccl ' + nccl if nccl else 'none'} pid={os.getpid()}", file=sys.stderr, flush=True)
+    return dev
 
 
 def main():
@@ -336,249 +528,53 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="candle", choices=["candle", "toy", "dlrm", "mmt"])
+    ap.add_argument("--workload", default="all", choices=["all", "mmt", "candle", "dlrm", "toy"],
+                    help="all = MMT headline + CANDLE-Uno and DLRM sub-results")
     ap.add_argument("--mode", default="gpp", choices=["gpp", "spp"])
     ap.add_argument("--costs", default="measured", choices=["measured", "analytic"],
                     help="partitioner cost curves: frozen B200 tables (profiles/) or analytic FLOP curves")
     ap.add_argument("--per-gpu-batch", type=int, default=None)
     ap.add_argument("--branches", type=int, default=None, help="MMT branch count (default 4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="minimum timed CPU work per cpu_baseline")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--no-spp", action="store_true", help="skip the SPP comparison arm (N > 1)")
+    ap.add_argument("--trace-out", default=None, help="write measured + simulated Chrome traces to PREFIX.*.json")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch / rendezvous only (gloo, no GPU): print one line per rank and exit")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
     from paper_2406_17145_b200.runtime.api import dist_env
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args))
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    from paper_2406_17145_b200.runtime.data import make_batch
-    from paper_2406_17145_b200.runtime.api import twin
-    from paper_2406_17145_b200.workloads import b200_cluster, with_measured_curves
-
-    wl = _workload(args.workload, world, args.per_gpu_batch, args.branches)
-    dev = torch.device("cuda", local)
-    arm = _time_arm(wl, world, rank, dev, args.mode, args)
-    ex, sg, graphed, dev_batch, ms, launches, clk, t_plan, be = (
-        arm["ex"], arm["sg"], arm["graphed"], arm["dev_batch"], arm["ms"], arm["launches"], arm["clocks"],
-        arm["plan_s"], arm["be"])
-    keys = set(ex.data_keys()) if ex.stage else set()
-    value = wl.mini_batch * args.steps / (ms / 1e3)
-
-    # ---------------- e2e: host buffers through the public API ----------------
-    host = []
-    h2d_bytes = 0
-    for s in range(2):
-        fb = make_batch(wl, s + 1, keys=keys)
-        hb = {}
-        for k in ex.data_keys() if ex.stage else []:
-            t = ex.local_rows(fb[k])
-            if t.is_floating_point():
-                t = t.to(ex.dtype) if t.dim() > 1 else t.float()
-            hb[k] = t.pin_memory()
-        host.append(hb)
-    h2d_bytes = sum(t.numel() * t.element_size() for t in host[0].values())
-    dbufs = graphed.bufs if graphed is not None else [{k: torch.empty_like(v, device=dev) for k, v in hb.items()} for hb in host]
-    loss_host = torch.zeros(args.steps, dtype=torch.float32).pin_memory()
-    copy_stream = torch.cuda.Stream(dev)
-    ready = [torch.cuda.Event(), torch.cuda.Event()]
-    consumed = [torch.cuda.Event(), torch.cuda.Event()]
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record()
-
-    def h2d(i):
-        with torch.cuda.stream(copy_stream):
-            copy_stream.wait_event(consumed[i % 2])
-            for k, v in host[i % 2].items():
-                dbufs[i % 2][k].copy_(v, non_blocking=True)
-            ready[i % 2].record(copy_stream)
-
-    for i in range(2):
-        consumed[i].record()
-    h2d(0)
-    for i in range(args.steps):
-        if i + 1 < args.steps:
-            h2d(i + 1)
-        torch.cuda.current_stream().wait_event(ready[i % 2])
-        loss = graphed.replay(i % 2) if graphed is not None else ex.run_iteration(dbufs[i % 2])
-        consumed[i % 2].record()
-        if loss is not None:
-            loss_host[i:i + 1].copy_(loss, non_blocking=True)
-    f1.record()
-    torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e = wl.mini_batch * args.steps / (e2e_ms / 1e3)
-
-    # ---------------- roofline + busy time: events around every kernel call ----------------
-    # One iteration captured in a CUDA graph with an event-record node on each side of every
-    # kernel call (external events keep their timestamps across replays) and replayed: the
-    # durations are those of the graph-replayed step.  Fallback: eager iterations with the
-    # GPU queue kept ahead of the host (a sleep longer than the host's enqueue time).
-    prof_iters = 1
-    timing = "cuda-graph event nodes"
-    torch.cuda.synchronize()
-    be.enabled = True
-    be.external = True
-    be.reset()
-    try:
-        side = torch.cuda.Stream(dev)
-        side.wait_stream(torch.cuda.current_stream(dev))
-        pg = torch.cuda.CUDAGraph()
+    dev = _init_ranks(args, rank, world, local)
+    if args.dry_run:
         if world > 1:
             dist.barrier()
-        with torch.cuda.graph(pg):
-            ex.run_iteration(dev_batch)
-        be.enabled = False
-        for _ in range(3):
-            pg.replay()
-        torch.cuda.synchronize()
-    except Exception as exc:  # noqa: BLE001 - report and fall back to eager timing
-        timing = f"eager events, queue preloaded (graph capture failed: {type(exc).__name__})"
-        be.external = False
-        be.enabled = False
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        h0 = time.perf_counter()
-        ex.run_iteration(dev_batch)
-        host_s = time.perf_counter() - h0
-        torch.cuda.synchronize()
-        be.enabled = True
-        be.reset()
-        if world > 1:
-            dist.barrier()
-        be.preload(host_s)
-        ex.run_iteration(dev_batch)
-        torch.cuda.synchronize()
-    summ = be.summary() if ex.stage else {"flops": 0.0, "ms": 0.0, "busy_ms": 0.0, "tflops": 0.0, "launches": 0}
-    be.enabled = False
-    # the same iteration's GEMMs replayed back to back from one graph, two events around
-    # it: per-launch durations free of the event nodes above (timed on this rank; the
-    # GEMMs do no communication)
-    alone = None
-    if ex.stage is not None:
-        try:
-            alone = be.time_gemms_alone(lambda: ex.run_iteration(dev_batch))
-        except Exception as exc:  # noqa: BLE001 - report, keep the event-node figure
-            alone = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+            dist.destroy_process_group()
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world}), flush=True)
+        return
     peaks, peak_src = _peaks()
-    t_iter = ms / args.steps
-    cuda_graph = graphed is not None
-    gemm_share = (summ["ms"] / prof_iters) / t_iter if ms > 0 else 0.0
-    busy = summ["busy_ms"] / prof_iters  # this rank's kernel time per iteration
-    busy_sum = busy
-    if world > 1:
-        bt = torch.tensor([busy], device=dev, dtype=torch.float64)
-        dist.all_reduce(bt)
-        busy_sum = float(bt.item())
-    bubble = max(0.0, 1.0 - busy_sum / (world * t_iter))
-    # summed stage-compute roofline: every sample's algorithmic FLOPs at the
-    # sustained tensor peak plus its HBM-bound bytes at the measured copy bandwidth, over N GPUs
-    t_roof = wl.mini_batch * (wl.flops_per_sample / (peaks["bf16_tflops_sustained"] * 1e12)
-                              + wl.bytes_per_sample / (peaks["hbm_gbs"] * 1e9)) / world * 1e3
-
-    # ---------------- GPP vs the sequential pipeline (SPP) on the same runtime ----------------
-    spp = None
-    if world > 1 and args.mode == "gpp" and not args.no_spp:
-        spp_sg_gpp = [(len(s.op_ids), s.micro_batch, s.dp_degree) for s in sg.stages]
-        del graphed, ex, dev_batch, arm
+    names = ["mmt", "candle", "dlrm"] if args.workload == "all" else [args.workload]
+    results = {}
+    for i, name in enumerate(names):
+        results[name] = bench_workload(name, args, rank, world, dev, peaks, peak_src, cpu_ok=True)
         import gc
 
         gc.collect()
         torch.cuda.empty_cache()
-        sp = _time_arm(wl, world, rank, dev, "spp", args, clocks=False)
-        spp_value = wl.mini_batch * args.steps / (sp["ms"] / 1e3)
-        spp = {"value": round(spp_value, 3), "ms_per_step": round(sp["ms"] / args.steps, 4),
-               "gpp_vs_spp_speedup": round(value / spp_value, 4), "plan_s": round(sp["plan_s"], 3),
-               "stages": [{"ops": len(s.op_ids), "b": s.micro_batch, "d": s.dp_degree} for s in sp["sg"].stages],
-               "gpp_stages": [{"ops": a, "b": b, "d": d} for a, b, d in spp_sg_gpp],
-               # the GPP sweep keeps a sequential candidate when the twin rates it faster
-               "gpp_picked_sequential": ([(s.op_ids, s.micro_batch) for s in sg.stages], sg.edges)
-                                        == ([(s.op_ids, s.micro_batch) for s in sp["sg"].stages], sp["sg"].edges),
-               "note": "SPP = spp_optimize (SPEC.md:384-392) strategy on this same runtime, CUDA-graph replay"}
-
-    # ---------------- simulated twin + bubble estimate ----------------
-    cluster = b200_cluster(world)
-    sim_graph = with_measured_curves(wl)[0].graph if args.costs == "measured" else wl.graph
-    sim = twin(sg, cluster, sim_graph)
-
     if rank == 0:
-        cpu = None
-        if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only (the contract)
-            sample = {"candle": 32, "toy": 64, "dlrm": 16, "mmt": 1}[args.workload]
-            cv, cdt, cn = cpu_reference_run(args.workload, sample, 2, min_seconds=10.0)
-            cpu = {"value": round(cv, 3), "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "port",
-                   "sample": f"{args.workload}, {cn} steps x B={sample}, monolithic torch-CPU training step "
-                             f"(oracle/reference_model.py), {cdt:.1f}s"}
-        peak = peaks["bf16_tflops_sustained"]
-        achieved = alone["tflops"] if alone and alone.get("tflops") else summ["tflops"]
-        line = {
-            "metric": "train samples/sec", "value": round(value, 3), "unit": "samples/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16" if wl.dtype != "fp32" else "fp32", "data": "synthetic",
-            "config": {
-                "workload": f"{wl.name}: 7 towers x 4 x Linear(4096,4096)+ReLU -> concat -> Linear(28672,1024)+ReLU -> Linear(1024,1) MSE"
-                if wl.name == "candle" else (f"mmt: {args.branches or 4} branches x 12 pre-LN layers, d=1024, S=512"
-                                            if wl.name == "mmt" else wl.name),
-                "global_batch": wl.mini_batch, "mode": args.mode,
-                "parallelism": f"{args.mode} stages={len(sg.stages)} depth={sim.depth}",
-                "stages": [{"ops": len(s.op_ids), "b": s.micro_batch, "d": s.dp_degree,
-                            "inflight": s.sched_cfg.inflight_samples} for s in sg.stages],
-                "l2": {"candle": "per-step working set (weights+master+grads ~2.9 GB) >> 126 MB L2",
-                       "dlrm": "per-step working set (26 x 256 MB fp32 tables + MLP master/grads) >> 126 MB L2",
-                       "mmt": "per-step working set (48 layers x ~150 MB master/grad/shadow + activations) >> 126 MB L2",
-                       "toy": "toy model fits in L2 (launch-bound; no roofline claim)"}.get(args.workload),
-                "optimizer": "SGD fp32 master + bf16 shadow (fused into last wgrad epilogue when DP=1)",
-                "plan_s": round(t_plan, 3), "cuda_graph": cuda_graph, "costs": args.costs,
-            },
-            "e2e": {"value": round(e2e, 3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d_bytes),
-                    "d2h_bytes_per_step": 4},
-            "gpu_launches": int(launches),
-            "roofline": {"bound": "tensor", "kernel": "gemm_tc_pair_kernel (tcgen05 cta_group::2 bf16 GEMM, all dense fw/dgrad/wgrad+SGD)",
-                         "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
-                         "frac": round(achieved / peak, 4) if peak else None,
-                         **_gemm_traffic(args.workload),
-                         "peak_source": f"{peak_src} bf16_tflops_sustained",
-                         "timing": "one iteration's GEMM launches replayed back to back from a CUDA graph, "
-                                   "CUDA events around the replay (gemms_alone); the event-node figures below time "
-                                   "each launch inside the full iteration graph",
-                         "gemms_alone": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in (alone or {}).items()},
-                         "achieved_event_nodes": round(summ["tflops"], 2),
-                         "share_of_step": round(gemm_share, 4), "event_node_timing": timing,
-                         "ncu_cross_check": _ncu_cross_check(args.workload, peak),
-                         "by_kind": summ.get("by_kind", {}),
-                         "other_kernels_ms": summ.get("other_ms", {})},
-            "clocks": clk,
-            "step_roofline": {"t_roof_ms": round(t_roof, 4), "frac": round(t_roof / t_iter, 4),
-                              "flops_per_sample": wl.flops_per_sample, "bytes_per_sample": wl.bytes_per_sample,
-                              "note": "summed stage-compute roofline: B*(F/P_sustained + bytes/BW_hbm)/N vs measured step"},
-            "bubble": {"measured": round(bubble, 4), "busy_ms_per_gpu": round(busy_sum / world, 4),
-                       "model": round(sim.bubble_fraction, 4),
-                       "note": "1 - sum over ranks of kernel busy time / (N * step time); busy from events around "
-                               "every kernel call in eager iterations"},
-            "sim": {"iteration_ms_model": round(sim.iteration_ms, 4), "bubble_fraction_model": round(sim.bubble_fraction, 4)},
-            "spp": spp,
-        }
-        if cpu:
-            line["cpu_baseline"] = cpu
-        print(json.dumps(line), flush=True)
-        if os.environ.get("GPP_BENCH_DETAIL"):
-            print(json.dumps({"gemm_by_shape": summ.get("by_shape", {})}), file=sys.stderr)
+        head = results[names[0]]
+        if len(names) > 1:
+            head["sub_results"] = {n: results[n] for n in names[1:]}
+        print(json.dumps(head), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

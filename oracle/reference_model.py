@@ -26,13 +26,23 @@ def _round(t, bf16: bool):
 
 
 class ReferenceModel:
-    def __init__(self, wl, seed: int = 0):
+    """``native_bf16``: the CPU BASELINE variant (bench.py cpu_baseline / --impl reference):
+    parameters, activations and GEMMs in bf16 directly (oneDNN / AMX on the host), no
+    rounding emulation — the fastest honest CPU training step of the workload, not the
+    parity oracle (which computes in fp32 and rounds where the device stores bf16)."""
+
+    def __init__(self, wl, seed: int = 0, native_bf16: bool = False):
         self.wl = wl
         self.bf16 = wl.dtype != "fp32"
+        self.native = native_bf16 and self.bf16
+        self.cd = torch.bfloat16 if self.native else torch.float32
         self.params: dict[tuple[int, str], torch.Tensor] = {}
         for o in wl.graph.topo_order:
             for name, t in init_params(wl.layers[o], o, seed):
-                self.params[(o, name)] = t.clone().requires_grad_(True)
+                self.params[(o, name)] = t.to(self.cd).clone().requires_grad_(True)
+
+    def _r(self, t):
+        return t if self.native else _round(t, self.bf16)
 
     def loss(self, batch: dict[str, torch.Tensor], relu_masks: dict | None = None) -> torch.Tensor:
         """``relu_masks`` (op -> bool [B, width], global sample order): take the ReLU
@@ -48,25 +58,25 @@ class ReferenceModel:
         for o in g.topo_order:
             spec = wl.layers[o]
             if spec.data_key is not None:
-                x = _round(batch[spec.data_key].float(), self.bf16)
+                x = self._r(batch[spec.data_key].to(self.cd))
             else:
                 preds = g.predecessors(o)
                 x = out[preds[0]] if len(preds) == 1 else None
             if spec.kind == "dense":
-                w = _round(P[(o, "w")], self.bf16)
+                w = self._r(P[(o, "w")])
                 z = x @ w.t() + P[(o, "b")]
                 if spec.act == "relu" and relu_masks is not None and o in relu_masks:
                     y = z * relu_masks[o].to(z.dtype)
                 else:
                     y = torch.relu(z) if spec.act == "relu" else (torch.nn.functional.gelu(z, approximate="tanh") if spec.act == "gelu" else z)
-                out[o] = _round(y, self.bf16)
+                out[o] = self._r(y)
             elif spec.kind == "concat":
                 out[o] = torch.cat([out[u] for u in g.predecessors(o)], dim=1)
             elif spec.kind == "mmt_layer":
                 out[o] = self._mmt_layer(o, spec, x)
             elif spec.kind == "embbag":
                 pooled = torch.nn.functional.embedding_bag(batch[spec.data_key], P[(o, "table")], mode="sum")
-                out[o] = _round(pooled, self.bf16)
+                out[o] = self._r(pooled)
             elif spec.kind == "interaction":
                 zz = torch.stack([out[u] for u in g.predecessors(o)], dim=1)  # [B, F, D]
                 F = zz.shape[1]
@@ -74,19 +84,19 @@ class ReferenceModel:
                 ii = torch.tensor([i for i in range(F) for j in range(i)])
                 jj = torch.tensor([j for i in range(F) for j in range(i)])
                 pad = spec.out_dim - zz.shape[2] - len(ii)
-                y = torch.cat([zz[:, 0], dots[:, ii, jj], torch.zeros(zz.shape[0], pad)], dim=1)
-                out[o] = _round(y, self.bf16)
+                y = torch.cat([zz[:, 0], dots[:, ii, jj], torch.zeros(zz.shape[0], pad, dtype=zz.dtype)], dim=1)
+                out[o] = self._r(y)
             elif spec.kind == "mse_head":
                 pred = x @ P[(o, "w")] + P[(o, "b")][0]
-                l = ((pred - batch[spec.label_key].float()) ** 2).sum() / B
+                l = ((pred - batch[spec.label_key].to(self.cd)) ** 2).sum() / B
                 total = l if total is None else total + l
             elif spec.kind == "bce_head":
                 z = x @ P[(o, "w")] + P[(o, "b")][0]
-                l = torch.nn.functional.binary_cross_entropy_with_logits(z, batch[spec.label_key].float(), reduction="sum") / B
+                l = torch.nn.functional.binary_cross_entropy_with_logits(z, batch[spec.label_key].to(self.cd), reduction="sum") / B
                 total = l if total is None else total + l
             elif spec.kind == "ce_head":
-                w = _round(P[(o, "w")], self.bf16)
-                logits = _round(x @ w.t() + P[(o, "b")], self.bf16)
+                w = self._r(P[(o, "w")])
+                logits = self._r(x @ w.t() + P[(o, "b")])
                 l = torch.nn.functional.cross_entropy(logits, batch[spec.label_key], reduction="sum") / B
                 total = l if total is None else total + l
             else:
@@ -96,9 +106,9 @@ class ReferenceModel:
     def _mmt_layer(self, o, spec, xflat):
         """Pre-LN encoder layer with the device path's bf16 rounding points."""
         S, d, H, ffn, pool = spec.extra
-        P, bf = self.params, self.bf16
-        R = lambda t: _round(t, bf)
-        W = lambda n: _round(P[(o, n)], bf)
+        P = self.params
+        R = self._r
+        W = lambda n: self._r(P[(o, n)])
         B = xflat.shape[0]
         x = xflat.reshape(B * S, d)
         h1 = R(torch.nn.functional.layer_norm(x, (d,), P[(o, "ln1_g")], P[(o, "ln1_b")], eps=1e-5))
@@ -120,7 +130,7 @@ class ReferenceModel:
         """Re-synchronise to another run's master weights (per-step parity without drift)."""
         with torch.no_grad():
             for k, p in self.params.items():
-                p.copy_(params[k].detach().float().cpu().reshape(p.shape))
+                p.copy_(params[k].detach().to(self.cd).cpu().reshape(p.shape))
 
     def step(self, batch, lr: float, relu_masks: dict | None = None):
         """loss, grads (dict) and the SGD update applied in place."""

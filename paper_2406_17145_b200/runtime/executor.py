@@ -664,7 +664,13 @@ class Executor:
         eager_sparse = step_optimizer and bool(self.tables) and self.d == 1
         fw_left = sum(1 for t in self.stage.schedule if t.direction == "fw")
         bw_done: list[int] = []
+        mark = getattr(self.be, "set_task", None)  # measured task trace (runtime/trace.py)
+        sid = self.stage.id
+        if mark:
+            mark(("iteration",))
         for t in self.stage.schedule:
+            if mark:
+                mark((sid, t.direction, t.index))
             if t.direction == "fw":
                 self._fw(t.index, batch)
                 fw_left -= 1
@@ -676,6 +682,8 @@ class Executor:
                 for j in bw_done:
                     self._sparse_update(batch, j)
                 bw_done = []
+        if mark:
+            mark((sid, "opt", 0))
         for key in list(self._send_works):
             self._wait_sends(key)
         if self.d > 1:
@@ -701,6 +709,8 @@ class Executor:
                     self.be.sgd_step(self.master[self.rest_off:], sh, self.grad[self.rest_off:], self.lr)
             else:
                 self.be.sgd_step(self.master, self.shadow, self.grad, self.lr)
+        if mark:
+            mark(None)
         return self.loss_acc
 
     def _sparse_update(self, batch, j: int) -> None:

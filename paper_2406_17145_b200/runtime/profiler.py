@@ -26,6 +26,7 @@ class _Rec:
     k: int
     start: torch.cuda.Event
     end: torch.cuda.Event
+    task: tuple | None = None  # (stage id, "fw" | "bw", micro-batch index) being executed
 
 
 GEMM_KINDS = ("fwd", "dgrad", "wgrad")
@@ -51,6 +52,8 @@ class TimedBackend(CudaBackend):
         self.enabled = True
         self.external = False  # graph capture: event-record nodes that keep their timestamps
         self.gemm_calls = None  # list -> record every dense GEMM call (replayable closure)
+        self.task = None  # set by the executor around each task (measured task trace)
+        self.t_origin = None  # event recorded at the start of the last iteration
         for name in _OTHER_CALLS:
             base = getattr(CudaBackend, name, None)
             if base is not None:
@@ -71,8 +74,36 @@ class TimedBackend(CudaBackend):
         s.record()
         r = fn()
         e.record()
-        self.records.append(_Rec(kind, 2.0 * m * n * k, m, n, k, s, e))
+        self.records.append(_Rec(kind, 2.0 * m * n * k, m, n, k, s, e, self.task))
         return r
+
+    def set_task(self, task) -> None:
+        """Executor hook: the kernels that follow belong to ``task`` = (stage, dir, index);
+        ``("iteration", ...)`` marks the start of an iteration (the trace's time origin)."""
+        if task is not None and task[0] == "iteration":
+            self.task = None
+            if self.enabled:
+                ev = torch.cuda.Event(enable_timing=True, external=self.external)
+                ev.record()
+                self.t_origin = ev
+            return
+        self.task = task
+
+    def task_times(self) -> dict:
+        """Measured {(stage, dir, index): (start_ms, end_ms, busy_ms)} of the recorded
+        iteration: first kernel start / last kernel end relative to the iteration's start
+        event, and the summed kernel time (waits for peers excluded).  Synchronises."""
+        torch.cuda.synchronize()
+        out: dict = {}
+        for r in self.records:
+            if r.task is None or self.t_origin is None:
+                continue
+            t0 = self.t_origin.elapsed_time(r.start)
+            t1 = self.t_origin.elapsed_time(r.end)
+            a = out.get(r.task)
+            d = r.start.elapsed_time(r.end)
+            out[r.task] = (t0, t1, d) if a is None else (min(a[0], t0), max(a[1], t1), a[2] + d)
+        return out
 
     def linear_fwd(self, y, x, w, bias, act, residual=None, pre=None):
         self._timed("fwd", x.shape[0], w.shape[0], x.shape[1],
