@@ -92,7 +92,10 @@ int gpp_linear_dgrad(void* dx, int64_t lddx, const void* dy, int64_t lddy, const
                      int64_t ldw, const void* saved, int64_t ldsaved, int64_t M, int64_t N,
                      int64_t K, int act, int dtype, void* stream);
 
-/* dw[N,K] (+)= dy[M,N]^T · x[M,K]  (fp32 out);  dbias[N] (+)= sum_m dy[m,:]. */
+/* dw[N,K] (+)= dy[M,N]^T · x[M,K]  (fp32 out);  dbias[N] (+)= sum_m dy[m,:].
+ * The bias column sums are read from the dy tiles the GEMM already stages in shared
+ * memory (an extra warp of the CTA-pair kernel) -- no second pass over dy -- except for
+ * split-K / single-CTA / fp32 launches, which add one column-sum kernel. */
 int gpp_linear_wgrad(float* dw, int64_t lddw, float* dbias, const void* dy, int64_t lddy,
                      const void* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
                      int accumulate, int dtype, void* stream);
@@ -105,7 +108,7 @@ int gpp_linear_wgrad(float* dw, int64_t lddw, float* dbias, const void* dy, int6
 int gpp_linear_wgrad_sgd(float* master, int64_t ldm, void* shadow, int64_t lds, float* grad,
                          int64_t ldg, float lr, int accumulate, int store_grad, const void* dy,
                          int64_t lddy, const void* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
-                         int dtype, void* stream);
+                         float* dbias, int dtype, void* stream);
 
 /* Generic C[M,N] = alpha * sum_k A(m,k) B(n,k) (+ beta*C).
  * a_mn / b_mn = 0: operand stored [rows][ld] with k contiguous (K-major);

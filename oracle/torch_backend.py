@@ -69,7 +69,9 @@ class TorchBackend:
             else:
                 db.copy_(s)
 
-    def linear_wgrad_sgd(self, master, shadow, grad, dy, x, lr, accumulate, store_grad):
+    def linear_wgrad_sgd(self, master, shadow, grad, dy, x, lr, accumulate, store_grad, dbias=None):
+        if dbias is not None:
+            self.colsum(dbias, dy, accumulate)
         g = dy.float().t() @ x.float()
         if accumulate:
             g = g + grad

@@ -31,6 +31,11 @@ struct EpiParams {
   int64_t split_stride;  // split-K: partial s is written at (float*)out + s * split_stride
   const void* pf_ptr;    // L2 prefetch hint: bytes another kernel will read next (or null)
   int64_t pf_bytes;
+  // wgrad (A = dy^T, MN-major): also colsum[m] (+)= sum_k A[m, k] -- the bias gradient,
+  // summed from the A tiles already staged in shared memory (or one column-sum kernel
+  // after the GEMM where that is not possible: split-K, 1-CTA tiles, fp32)
+  float* colsum;
+  int colsum_acc;
 };
 
 // One-shot L2 prefetch hint consumed by the next GEMM launched on this host thread.

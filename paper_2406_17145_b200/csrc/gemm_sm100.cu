@@ -562,8 +562,19 @@ __device__ __forceinline__ void read_aux_tile(const uint8_t* tile, int lane, flo
 //   single MMA thread commits (multicast) to both CTAs' empty / accum-full
 //   barriers; all 8 epilogue warps arrive on the leader's accum-empty barrier.
 // ------------------------------------------------------------------------
+// wgrad epilogues (A = dy^T, MN-major) carry one more warp: the bias-gradient column sums
+template <int EPI, bool A_MN>
+constexpr bool pair_colsum_epi() { return (EPI == EPI_F32 || EPI == EPI_SGD) && A_MN; }
+
+__device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS + 32, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
                         const __grid_constant__ CUtensorMap tma_b, EpiParams ep, int M, int N,
                         int K, int k_splits, int m_fast, const __grid_constant__ CUtensorMap tma_aux,
@@ -582,6 +593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;       // [2]
   uint64_t* tempty_bar = tfull_bar + 2;           // [2] (leader's copy is the live one)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* cs_bar = tempty_bar + 3;              // [STAGES] peer CTA: "leader saw this stage full"
   float* epi_stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);  // per warp 32 x 36 (x2 SGD)
   // bf16 epilogues: per-warp double-buffered 64B-swizzled 32 x 32 aux tiles filled by TMA
   uint64_t* aux_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + 512);
@@ -598,13 +610,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   const int num_units = m_tiles * n_tiles * k_splits;   // (tile, K-split) work units
   const int kb_total = (K + BK - 1) / BK;
   const int kb_per = (kb_total + k_splits - 1) / k_splits;
+  // fused bias gradient: a 12th warp per CTA sums this CTA's A tile of every stage over K
+  // (both CTAs: the leader's warp tells the peer's when the pair's TMA bytes landed) and
+  // releases the stage as a second arrival on its empty barrier
+  const bool cs = pair_colsum_epi<EPI, A_MN>() && ep.colsum != nullptr && k_splits == 1;
+  static_assert(3 * STAGES + 5 <= 32, "barrier block overflows its 256 bytes");
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], cs ? 2 : 1);
+      mbar_init(&cs_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -694,8 +712,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         umma_commit_pair(&tfull_bar[acc], 0x3);
       }
     }
+  } else if (warp >= 2 + PAIR_EPI_WARPS) {
+    // ---------------- bias-gradient column sums (wgrad: A = dy^T, MN-major) ----------------
+    // A stage holds this CTA's 128 m x 64 k as two 8 KB chunks of 64 k-rows x 64 m (128B
+    // swizzle); lane = (chunk, 16-byte unit, half): 4 m columns, summed over the 64 rows.
+    if (cs) {
+      const uint32_t peer_cs0 = mapa_shared(smem_u32(&cs_bar[0]), 1);
+      const int ch = lane >> 4, j = (lane & 15) >> 1, half = lane & 1;
+      uint32_t it = 0;
+      for (int u = cluster_id; u < num_units; u += num_clusters) {
+        const int m_blk = m_fast ? u % m_tiles : u / n_tiles;
+        const int n_blk = m_fast ? u / m_tiles : u % n_tiles;
+        const bool mine = n_blk == 0;  // one tile column sums each m block
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        for (int kb = 0; kb < kb_total; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          if (leader) {
+            mbar_wait(&full_bar[s], ph);
+            if (lane == 0) mbar_arrive_remote_release(peer_cs0 + s * 8);
+          } else {
+            mbar_wait_cluster(&cs_bar[s], ph);
+          }
+          if (mine) {
+            const uint8_t* base = smem + s * STAGE_BYTES + ch * 8192 + half * 8;
+#pragma unroll 16
+            for (int r = 0; r < 64; ++r) {
+              const uint2 v = *reinterpret_cast<const uint2*>(base + r * 128 + ((j ^ (r & 7)) << 4));
+              const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+              const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+              a0 += lo.x;
+              a1 += lo.y;
+              a2 += hi.x;
+              a3 += hi.y;
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_local(&empty_bar[s]);
+        }
+        if (mine) {
+          const int m = m_blk * 2 * BM + static_cast<int>(rank) * BM + ch * 64 + j * 8 + half * 4;
+          const float sums[4] = {a0, a1, a2, a3};
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (m + t < M) ep.colsum[m + t] = ep.colsum_acc ? ep.colsum[m + t] + sums[t] : sums[t];
+        }
+      }
+    }
   } else {
-    // ---------------- epilogue (warps 2..5 of both CTAs) ----------------
+    // ---------------- epilogue (warps 2..9 of both CTAs) ----------------
     const int q = warp & 3;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     uint32_t lt = 0, aux_it = 0;
@@ -986,8 +1051,9 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   const int64_t units = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * k_splits;
   int64_t clusters = num_sms() / 2;
   if (units < clusters) clusters = units;
+  constexpr int THREADS = PAIR_THREADS + (pair_colsum_epi<EPI, A_MN>() ? 32 : 0);
   gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(2 * clusters),
-                                                     PAIR_THREADS, SMEM, stream>>>(
+                                                     THREADS, SMEM, stream>>>(
       ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits, M < N ? 1 : 0, mx,
       aux_tma);
   cudaError_t e = cudaGetLastError();
@@ -1105,6 +1171,17 @@ static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
     slots = num_sms();
   }
   const int splits = choose_splits(tiles, slots, num_kb);
+  // bias gradient: fused into the pair kernel's A-tile reads when it runs unsplit; else
+  // one column-sum kernel over A ([K, M] row-major for the MN-major dy^T) after the GEMM
+  const bool fuse_cs = ep.colsum != nullptr && pair && splits == 1 && pair_colsum_epi<EPI, A_MN>();
+  if (ep.colsum != nullptr && !fuse_cs) {
+    GPP_ARG_CHECK(A_MN, "fused column sum needs the MN-major (wgrad) A operand");
+    EpiParams e2 = ep;
+    e2.colsum = nullptr;
+    int rc = dispatch_bn<A_MN, B_MN, EPI>(a, lda, b, ldb, e2, M, N, K, stream);
+    if (rc) return rc;
+    return gpp_colsum(ep.colsum, a, lda, K, M, ep.colsum_acc, GPP_BF16, stream);
+  }
 
   auto run = [&](auto epi_tag, const EpiParams& e, int ks) -> int {
     constexpr int E = decltype(epi_tag)::value;

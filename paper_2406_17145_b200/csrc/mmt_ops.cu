@@ -219,6 +219,179 @@ __global__ void __launch_bounds__(256) ln_fwd_vec_kernel(bf16* __restrict__ y, f
   }
 }
 
+// ---- LayerNorm, 16-byte vectors, two rows per warp (D % 256 == 0) -----------------------
+// Both rows' loads are issued before any reduction, so each warp keeps 2 x D x 2 B in
+// flight (the one-row kernel above was latency-bound: ~12 us for 32 MB at T=8192, D=1024).
+template <int PER>
+__global__ void __launch_bounds__(256) ln_fwd_vec2_kernel(bf16* __restrict__ y, float* __restrict__ mean,
+                                                          float* __restrict__ rstd, const bf16* __restrict__ x,
+                                                          const float* __restrict__ g, const float* __restrict__ b,
+                                                          int64_t T, int D, float eps) {
+  constexpr int NV = PER / 8;
+  const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5)) * 2;
+  const int lane = threadIdx.x & 31;
+  if (r0 >= T) return;
+  const bool two = r0 + 1 < T;
+  uint4 raw[2][NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) raw[0][i] = __ldg(reinterpret_cast<const uint4*>(x + r0 * D) + lane + 32 * i);
+  if (two) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) raw[1][i] = __ldg(reinterpret_cast<const uint4*>(x + (r0 + 1) * D) + lane + 32 * i);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (k == 1 && !two) break;
+    const int64_t r = r0 + k;
+    float v[PER];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) unpack8(raw[k][i], v + 8 * i);
+    float sm = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) sm += v[i];
+    const float mu = wsum(sm) / D;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) q += (v[i] - mu) * (v[i] - mu);
+    const float rs = rsqrtf(wsum(q) / D + eps);
+    uint4* yr = reinterpret_cast<uint4*>(y + r * D);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = 8 * (lane + 32 * i);
+      float gg[8], bb[8], o[8];
+      load8f(g + c, gg);
+      load8f(b + c, bb);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) o[t] = (v[8 * i + t] - mu) * rs * gg[t] + bb[t];
+      yr[lane + 32 * i] = pack8(o);
+    }
+    if (lane == 0) {
+      mean[r] = mu;
+      rstd[r] = rs;
+    }
+  }
+}
+
+// LayerNorm backward, 16-byte vectors (D % 256 == 0), register-lean so two 256-thread blocks
+// share an SM: the row's x / dy stay packed (uint4) and x-hat, g*dy are recomputed in the
+// second pass instead of being held as floats; gamma is staged in shared memory.
+//   dx = rstd * (g dy - mean(g dy) - xhat * mean(g dy xhat)) [+ dres]
+// per-block partials of dgamma = sum dy*xhat and dbeta = sum dy -> part[blockIdx.x][2*D].
+template <int PER, int ROWS>
+__global__ void __launch_bounds__(256, ROWS == 1 ? 2 : 1)
+    ln_bwd_vec_kernel(bf16* __restrict__ dx, float* __restrict__ part, const bf16* __restrict__ dy,
+                      const bf16* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
+                      const float* __restrict__ g, const bf16* __restrict__ dres, int64_t T, int D,
+                      int rows_per_block) {
+  constexpr int NV = PER / 8;
+  extern __shared__ float sm[];  // gamma [D] | red [8 warps][2 * D]
+  float* gs = sm;
+  float* red = sm + D;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = threadIdx.x; c < D; c += 256) gs[c] = g[c];
+  __syncthreads();
+  float dg[PER], db[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) dg[i] = db[i] = 0.f;
+  const int64_t rb = static_cast<int64_t>(blockIdx.x) * rows_per_block;
+  const int64_t re = min(T, rb + rows_per_block);
+  for (int64_t r0 = rb + ROWS * w; r0 < re; r0 += 8 * ROWS) {
+    // ROWS rows per warp: every row's x / dy loads issued before the first is processed
+    uint4 xr[ROWS][NV], dr[ROWS][NV];
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+      if (r0 + k >= re) break;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        xr[k][i] = __ldg(reinterpret_cast<const uint4*>(x + (r0 + k) * D) + lane + 32 * i);
+        dr[k][i] = __ldg(reinterpret_cast<const uint4*>(dy + (r0 + k) * D) + lane + 32 * i);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+      const int64_t r = r0 + k;
+      if (r >= re) break;
+      const float mu = __ldg(mean + r), rs = __ldg(rstd + r);
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        float xv[8], dv[8];
+        unpack8(xr[k][i], xv);
+        unpack8(dr[k][i], dv);
+        const int c = 8 * (lane + 32 * i);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float xh = (xv[t] - mu) * rs;
+          const float gy = dv[t] * gs[c + t];
+          dg[8 * i + t] = fmaf(dv[t], xh, dg[8 * i + t]);
+          db[8 * i + t] += dv[t];
+          s1 += gy;
+          s2 = fmaf(gy, xh, s2);
+        }
+      }
+      const float m1 = wsum(s1) / D, m2 = wsum(s2) / D;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        float xv[8], dv[8], o[8];
+        unpack8(xr[k][i], xv);
+        unpack8(dr[k][i], dv);
+        const int c = 8 * (lane + 32 * i);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float xh = (xv[t] - mu) * rs;
+          o[t] = rs * (dv[t] * gs[c + t] - m1 - xh * m2);
+        }
+        if (dres) {
+          float rv[8];
+          unpack8(__ldg(reinterpret_cast<const uint4*>(dres + r * D) + lane + 32 * i), rv);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) o[t] += rv[t];
+        }
+        reinterpret_cast<uint4*>(dx + r * D)[lane + 32 * i] = pack8(o);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = 8 * (lane + 32 * i);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      red[w * 2 * D + c + t] = dg[8 * i + t];
+      red[w * 2 * D + D + c + t] = db[8 * i + t];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 2 * D; c += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k * 2 * D + c];
+    part[static_cast<int64_t>(blockIdx.x) * 2 * D + c] = t;
+  }
+}
+
+// Column sums of the [nblocks, 2D] partials, 16 columns per block x 16 row groups (every
+// thread's loads independent and in flight together), fixed-order smem reduction.
+__global__ void __launch_bounds__(256) ln_bwd_final16_kernel(float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                             const float* __restrict__ part, int nblocks, int D,
+                                                             int accumulate) {
+  __shared__ float red[16][17];
+  const int cx = threadIdx.x & 15, ry = threadIdx.x >> 4;
+  const int c = blockIdx.x * 16 + cx;
+  float t = 0.f;
+  if (c < 2 * D) {
+#pragma unroll 8
+    for (int k = ry; k < nblocks; k += 16) t += __ldg(part + static_cast<int64_t>(k) * 2 * D + c);
+  }
+  red[ry][cx] = t;
+  __syncthreads();
+  if (ry == 0 && c < 2 * D) {
+#pragma unroll
+    for (int i = 1; i < 16; ++i) t += red[i][cx];
+    float* o = c < D ? dgamma + c : dbeta + (c - D);
+    *o = accumulate ? *o + t : t;
+  }
+}
+
 // ---- attention softmax: P = softmax(s) row-wise (fp32 scores, already scaled) ------------
 template <int PER>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(bf16* __restrict__ p,
@@ -357,8 +530,14 @@ int gpp_layernorm_fwd(void* y, float* mean, float* rstd, const void* x, const fl
   switch (D) {
     case 128: ln_fwd_kernel<4><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
     case 256: ln_fwd_vec_kernel<8><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
-    case 512: ln_fwd_vec_kernel<16><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
-    case 1024: ln_fwd_vec_kernel<32><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
+    case 512:
+      ln_fwd_vec2_kernel<16><<<static_cast<unsigned>((T + 15) / 16), 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd,
+                                                                                  static_cast<const bf16*>(x), gamma, beta, T, d, eps);
+      break;
+    case 1024:
+      ln_fwd_vec2_kernel<32><<<static_cast<unsigned>((T + 15) / 16), 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd,
+                                                                                  static_cast<const bf16*>(x), gamma, beta, T, d, eps);
+      break;
     default: set_error("layernorm: D must be 128/256/512/1024"); return GPP_ERR_UNSUPPORTED;
   }
   GPP_LAUNCH_CHECK();
@@ -370,6 +549,34 @@ int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, con
                       int64_t T, int64_t D, int accumulate, void* stream) {
   GPP_ARG_CHECK(dx && dgamma && dbeta && dy && x && mean && rstd && gamma && T > 0, "bad argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int d = static_cast<int>(D);
+  auto* dxp = static_cast<bf16*>(dx);
+  auto* dyp = static_cast<const bf16*>(dy);
+  auto* xp = static_cast<const bf16*>(x);
+  auto* drp = static_cast<const bf16*>(dres);
+  if ((D == 512 || D == 1024) && a16(dx) && a16(dy) && a16(x) && (!dres || a16(dres))) {
+    // D = 1024: one block per SM, two rows per warp in flight; D = 512: two blocks per SM,
+    // one row per warp.  Rows per block rounded up to the rows one pass of 8 warps covers.
+    const int per_sm = D == 1024 ? 1 : 2, rows = D == 1024 ? 16 : 8;
+    const int64_t nb0 = 148 * per_sm;
+    const int rpb = static_cast<int>(std::max<int64_t>(rows, ((T + nb0 - 1) / nb0 + rows - 1) / rows * rows));
+    const int nblk = static_cast<int>((T + rpb - 1) / rpb);
+    float* part = ln_scratch(static_cast<size_t>(nblk) * 2 * D, s);
+    if (!part) return GPP_ERR_CUDA;
+    const size_t smem = (D + 8 * 2 * D) * sizeof(float);
+    if (D == 1024) {
+      cudaFuncSetAttribute(ln_bwd_vec_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      ln_bwd_vec_kernel<32, 2><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb);
+    } else {
+      cudaFuncSetAttribute(ln_bwd_vec_kernel<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      ln_bwd_vec_kernel<16, 1><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb);
+    }
+    GPP_LAUNCH_CHECK();
+    ln_bwd_final16_kernel<<<static_cast<unsigned>((2 * D + 15) / 16), 256, 0, s>>>(dgamma, dbeta, part, nblk, d,
+                                                                                 accumulate);
+    GPP_LAUNCH_CHECK();
+    return GPP_OK;
+  }
   // one block per SM: rows per block = ceil(T / 148) rounded up to the 8 warps (T = 8192:
   // 56 rows, 147 blocks; 64 rows left 20 SMs idle)
   const int rpb = static_cast<int>(std::max<int64_t>(8, ((T + 147) / 148 + 7) / 8 * 8));
@@ -377,11 +584,6 @@ int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, con
   float* part = ln_scratch(static_cast<size_t>(nblk) * 2 * D, s);
   if (!part) return GPP_ERR_CUDA;
   const size_t smem = 8 * 2 * D * sizeof(float);
-  const int d = static_cast<int>(D);
-  auto* dxp = static_cast<bf16*>(dx);
-  auto* dyp = static_cast<const bf16*>(dy);
-  auto* xp = static_cast<const bf16*>(x);
-  auto* drp = static_cast<const bf16*>(dres);
   switch (D) {
     case 128: ln_bwd_kernel<4><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
     case 256: ln_bwd_kernel<8><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;

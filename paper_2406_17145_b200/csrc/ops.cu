@@ -526,7 +526,12 @@ static int gemm_any(int epi, const void* a, int64_t lda, int a_mn, const void* b
                     void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (dtype == GPP_BF16) return tc_gemm(epi, a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, s);
-  if (dtype == GPP_F32) return simt_gemm(epi, a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, s);
+  if (dtype == GPP_F32) {
+    const int rc = simt_gemm(epi, a, lda, a_mn, b, ldb, b_mn, ep, M, N, K, s);
+    if (rc || !ep.colsum) return rc;
+    GPP_ARG_CHECK(a_mn, "column sum needs the MN-major (wgrad) A operand");
+    return colsum_launch<float>(ep.colsum, static_cast<const float*>(a), lda, nullptr, K, M, ep.colsum_acc, s);
+  }
   set_error("unknown dtype");
   return GPP_ERR_ARG;
 }
@@ -555,20 +560,22 @@ int gpp_linear_wgrad(float* dw, int64_t lddw, float* dbias, const void* dy, int6
                      int accumulate, int dtype, void* stream) {
   GPP_ARG_CHECK(dw && dy && x, "null pointer");
   EpiParams ep{dw, lddw, nullptr, nullptr, 0, nullptr, 0, 1.f, accumulate ? 1.f : 0.f, 0, 0.f, nullptr, 0, 0, 0, nullptr, 0};
+  ep.colsum = dbias;  // dbias[n] = sum_m dy[m, n]: fused into the GEMM where possible
+  ep.colsum_acc = accumulate;
   // dw[N,K] = sum_m dy[m,n] x[m,k]: GEMM (N, K, M) with both operands MN-major.
-  int rc = gemm_any(EPI_F32, dy, lddy, 1, x, ldx, 1, ep, N, K, M, dtype, stream);
-  if (rc || !dbias) return rc;
-  return gpp_colsum(dbias, dy, lddy, M, N, accumulate, dtype, stream);
+  return gemm_any(EPI_F32, dy, lddy, 1, x, ldx, 1, ep, N, K, M, dtype, stream);
 }
 
 int gpp_linear_wgrad_sgd(float* master, int64_t ldm, void* shadow, int64_t lds, float* grad,
                          int64_t ldg, float lr, int accumulate, int store_grad, const void* dy,
                          int64_t lddy, const void* x, int64_t ldx, int64_t M, int64_t N, int64_t K,
-                         int dtype, void* stream) {
+                         float* dbias, int dtype, void* stream) {
   GPP_ARG_CHECK(master && grad && dy && x, "null pointer");
   GPP_ARG_CHECK(dtype == GPP_F32 || shadow, "bf16 path needs the shadow weights");
   EpiParams ep{master, ldm, nullptr, nullptr, 0, shadow, lds, 1.f, accumulate ? 1.f : 0.f, 0,
                lr, grad, ldg, store_grad, 0, nullptr, 0};
+  ep.colsum = dbias;  // the bias GRADIENT (applied later by the flat SGD), fused when possible
+  ep.colsum_acc = accumulate;
   return gemm_any(EPI_SGD, dy, lddy, 1, x, ldx, 1, ep, N, K, M, dtype, stream);
 }
 

@@ -39,8 +39,9 @@ class CudaBackend:
     def linear_wgrad(self, dw, db, dy, x, accumulate):
         lib.linear_wgrad(dw, db, dy, x, accumulate=accumulate)
 
-    def linear_wgrad_sgd(self, master, shadow, grad, dy, x, lr, accumulate, store_grad):
-        lib.linear_wgrad_sgd(master, shadow, grad, dy, x, lr, accumulate=accumulate, store_grad=store_grad)
+    def linear_wgrad_sgd(self, master, shadow, grad, dy, x, lr, accumulate, store_grad, dbias=None):
+        lib.linear_wgrad_sgd(master, shadow, grad, dy, x, lr, accumulate=accumulate, store_grad=store_grad,
+                             dbias=dbias)
 
     def colsum(self, out, x, accumulate):
         lib.colsum(out, x, accumulate=accumulate)

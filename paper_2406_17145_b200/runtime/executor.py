@@ -581,10 +581,11 @@ class Executor:
                     be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
                     self._ar_handles.append(self.tp.allreduce_async(self.G[(o, "w")]))
                 elif self.fuse and j == self.last_bw:
-                    # weight gradient + SGD in one epilogue; bias gradient -> flat SGD later
+                    # weight gradient + SGD in one epilogue, the bias gradient summed in the same
+                    # kernel (applied by the flat SGD later)
                     be.linear_wgrad_sgd(self.P[(o, "w")], self.W[(o, "w")] if self.shadow is not None else None,
-                                        self.G[(o, "w")], dz, x, self.lr, accumulate, self.keep_grads)
-                    be.colsum(self.G[(o, "b")], dz, accumulate)
+                                        self.G[(o, "w")], dz, x, self.lr, accumulate, self.keep_grads,
+                                        dbias=self.G[(o, "b")])
                 else:
                     be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
             elif spec.kind == "mmt_layer":

@@ -31,7 +31,7 @@ _SIGS = {
     "gpp_linear_fwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_linear_dgrad": ([_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_linear_wgrad": ([_vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
-    "gpp_linear_wgrad_sgd": ([_vp, _i64, _vp, _i64, _vp, _i64, _f32, _i32, _i32, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _vp], _i32),
+    "gpp_linear_wgrad_sgd": ([_vp, _i64, _vp, _i64, _vp, _i64, _f32, _i32, _i32, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp, _i32, _vp], _i32),
     "gpp_gemm_prefetch_hint": ([_vp, _i64], _i32),
     "gpp_gemm": ([_vp, _i64, _vp, _i64, _i32, _vp, _i64, _i32, _i64, _i64, _i64, _f32, _f32, _i32, _i32, _vp], _i32),
     "gpp_rowdot_fwd": ([_vp, _vp, _i64, _vp, _vp, _i64, _i64, _i32, _vp], _i32),
@@ -177,13 +177,15 @@ def linear_wgrad(dw, dbias, dy, x, accumulate=False, stream=None):
          M, N, K, int(bool(accumulate)), _dt(dy), _stream(stream))
 
 
-def linear_wgrad_sgd(master, shadow, grad, dy, x, lr, accumulate=False, store_grad=False, stream=None):
-    """Last-micro-batch wgrad with the SGD update fused into the epilogue."""
+def linear_wgrad_sgd(master, shadow, grad, dy, x, lr, accumulate=False, store_grad=False, dbias=None,
+                     stream=None):
+    """Last-micro-batch wgrad with the SGD update fused into the epilogue; ``dbias`` (optional)
+    receives the bias GRADIENT (+= with ``accumulate``), summed inside the same kernel."""
     M, N = dy.shape
     K = x.shape[1]
     call("gpp_linear_wgrad_sgd", _ptr(master), _ld(master), _ptr(shadow), _ld(shadow), _ptr(grad), _ld(grad),
          float(lr), int(bool(accumulate)), int(bool(store_grad)), _ptr(dy), _ld(dy), _ptr(x), _ld(x),
-         M, N, K, _dt(dy), _stream(stream))
+         M, N, K, _ptr(dbias), _dt(dy), _stream(stream))
 
 
 def gemm(c, a, b, a_mn=False, b_mn=False, alpha=1.0, beta=0.0, stream=None):

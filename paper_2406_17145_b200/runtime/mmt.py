@@ -120,8 +120,7 @@ class MMTLayer:
         o = self.o
         if ex.fuse and last:
             be.linear_wgrad_sgd(ex.P[(o, name)], ex.W[(o, name)] if ex.shadow is not None else None,
-                                ex.G[(o, name)], dz, xin, ex.lr, accumulate, ex.keep_grads)
-            be.colsum(ex.G[(o, bname)], dz, accumulate)
+                                ex.G[(o, name)], dz, xin, ex.lr, accumulate, ex.keep_grads, dbias=ex.G[(o, bname)])
         else:
             be.linear_wgrad(ex.G[(o, name)], ex.G[(o, bname)], dz, xin, accumulate)
             if ex.d > 1 and last:

@@ -117,10 +117,10 @@ class TimedBackend(CudaBackend):
         self._timed("wgrad", dy.shape[1], x.shape[1], dy.shape[0],
                     lambda: super(TimedBackend, self).linear_wgrad(dw, db, dy, x, accumulate))
 
-    def linear_wgrad_sgd(self, master, shadow, grad, dy, x, lr, accumulate, store_grad):
+    def linear_wgrad_sgd(self, master, shadow, grad, dy, x, lr, accumulate, store_grad, dbias=None):
         self._timed("wgrad", dy.shape[1], x.shape[1], dy.shape[0],
                     lambda: super(TimedBackend, self).linear_wgrad_sgd(master, shadow, grad, dy, x, lr,
-                                                                       accumulate, store_grad))
+                                                                       accumulate, store_grad, dbias))
 
     def time_gemms_alone(self, run_iteration, reps: int = 3) -> dict:
         """Record one iteration's dense GEMM launches (kind, FLOPs, closure), capture them
@@ -263,8 +263,7 @@ def profile_dense(din: int, dout: int, act: str, batches, device, dtype=torch.bf
             if has_dgrad:
                 be.linear_dgrad(dx, dz, w, x, act)
             if dtype == torch.bfloat16:
-                be.linear_wgrad_sgd(master, w, grad, dz, x, 0.0, False, False)
-                be.colsum(gb, dz, False)
+                be.linear_wgrad_sgd(master, w, grad, dz, x, 0.0, False, False, dbias=gb)
             else:
                 be.linear_wgrad(grad, gb, dz, x, False)
 

@@ -221,10 +221,14 @@ def test_wgrad_sgd_fused(cuda_lib, M, accumulate):
     shadow = torch.empty(N, K, device="cuda", dtype=torch.bfloat16)
     grad = torch.randn(N, K, device="cuda", generator=g)
     grad0, master0 = grad.clone(), master.clone()
-    cuda_lib.linear_wgrad_sgd(master, shadow, grad, dy, x, 0.01, accumulate=accumulate, store_grad=True)
+    db = torch.randn(N, device="cuda", generator=g)
+    db0 = db.clone()
+    cuda_lib.linear_wgrad_sgd(master, shadow, grad, dy, x, 0.01, accumulate=accumulate, store_grad=True, dbias=db)
     torch.cuda.synchronize()
     gref = dy.float().t() @ x.float() + (grad0 if accumulate else 0)
     assert _rel(grad, gref) < 1e-4
+    # bias gradient summed inside the GEMM (pair kernel at M = 1024, fallback kernel at 64)
+    assert torch.allclose(db, dy.float().sum(0) + (db0 if accumulate else 0), rtol=1e-4, atol=1e-3)
     assert torch.allclose(master, master0 - 0.01 * gref, rtol=1e-5, atol=1e-5)
     assert torch.equal(shadow, master.bfloat16())
 
@@ -239,11 +243,30 @@ def test_wgrad_sgd_fast_path(cuda_lib, N, K, M):
     shadow = torch.empty(N, K, device="cuda", dtype=torch.bfloat16)
     grad = torch.zeros(N, K, device="cuda")  # not touched (store_grad off)
     master0 = master.clone()
-    cuda_lib.linear_wgrad_sgd(master, shadow, grad, dy, x, 0.01)
+    db = torch.full((N,), float("nan"), device="cuda")
+    cuda_lib.linear_wgrad_sgd(master, shadow, grad, dy, x, 0.01, dbias=db)
     torch.cuda.synchronize()
     gref = dy.float().t() @ x.float()
     assert torch.allclose(master, master0 - 0.01 * gref, rtol=1e-5, atol=2e-5)
     assert torch.equal(shadow, master.bfloat16())
+    assert torch.allclose(db, dy.float().sum(0), rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 1024, 1024), (8192, 3072, 1024), (1024, 4096, 4096), (300, 520, 264)])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_wgrad_fused_bias_colsum(cuda_lib, M, N, K, accumulate):
+    """linear_wgrad's dbias: summed by the CTA-pair kernel's column-sum warp from the staged
+    dy tiles (unsplit launches) or by the column-sum kernel (split-K / small shapes)."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    dy = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    dw = torch.randn(N, K, device="cuda", generator=g)
+    db = torch.randn(N, device="cuda", generator=g)
+    dw0, db0 = dw.clone(), db.clone()
+    cuda_lib.linear_wgrad(dw, db, dy, x, accumulate=accumulate)
+    torch.cuda.synchronize()
+    assert _rel(dw, dy.float().t() @ x.float() + (dw0 if accumulate else 0)) < 1e-4
+    assert torch.allclose(db, dy.float().sum(0) + (db0 if accumulate else 0), rtol=1e-4, atol=2e-3)
 
 
 @pytest.mark.parametrize("F", [7, 26, 27])
