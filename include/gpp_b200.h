@@ -22,6 +22,7 @@
  *   gpp_sgd_step                fused optimizer over a stage's parameters
  *   gpp_layernorm_fwd / _bwd, gpp_softmax_fwd / _bwd, gpp_meanpool_fwd / _bwd,
  *   gpp_gemm_batched            MMT pre-LN transformer layer (attention as batched GEMMs)
+ *   gpp_flash_attn_fwd / _bwd         MMT attention, P recomputed (O + LSE forward; dQ, dK, dV backward)
  *   gpp_attn_fwd / gpp_attn_bwd       fused MMT attention (softmax + P.V / softmax-bwd + dS.K)
  *   gpp_attn_softmax / gpp_attn_softmax_bwd  attention scores with the softmax (or its
  *                               backward) fused into the tcgen05 epilogue (S <= 512)
@@ -218,6 +219,21 @@ int gpp_attn_fwd(const void* qkv, void* p, void* o, int64_t ldo, int64_t m, int6
                  float scale, void* stream);
 int gpp_attn_bwd(const void* qkv, const void* p, const void* o, int64_t ldo, const void* dout, int64_t lddo,
                  void* ds, void* dqkv, int64_t m, int64_t S, int64_t d, int64_t H, float scale, void* stream);
+
+/* Recompute-based (FlashAttention-style) MMT attention: nothing of size Z x S x S in HBM.
+ *   gpp_flash_attn_fwd: o[:, h*64..] = softmax(scale q k^T) v, and per (z, query row) the
+ *       base-2 log-sum-exp lse2 = scale log2(e) max + log2(sum) ([m*H, S] fp32).
+ *   gpp_flash_attn_bwd: dvec = rowsum(dout o o) (caller-owned [m*H, S] fp32 scratch), then
+ *       per (z, 128-key block) with P recomputed from q, k, lse2: the dK and dV blocks of
+ *       dqkv (summed over every query block in TMEM) and dQ (per-key-block partials summed
+ *       in a fixed order across a cluster of S/128 CTAs through distributed shared memory).
+ * Same layouts and requirements (d == 64 H, S in {128, 256, 384, 512}) as gpp_attn_*;
+ * they replace gpp_attn_fwd / gpp_attn_bwd and the two dV / dK batched GEMMs. */
+int gpp_flash_attn_fwd(const void* qkv, float* lse2, void* o, int64_t ldo, int64_t m, int64_t S, int64_t d,
+                       int64_t H, float scale, void* stream);
+int gpp_flash_attn_bwd(const void* qkv, const float* lse2, const void* o, int64_t ldo, const void* dout,
+                       int64_t lddo, float* dvec, void* dqkv, int64_t m, int64_t S, int64_t d, int64_t H,
+                       float scale, void* stream);
 
 /* ---- DLRM: embedding bags and the dot interaction ------------- */
 /* pooled[m, :D] = sum_b table[idx[m*ldi + b], :D]; fp32 table [rows, D], bf16 pooled, D = 64.

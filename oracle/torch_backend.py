@@ -216,6 +216,33 @@ class TorchBackend:
         """[m*S, >=col0+H*dh] head-interleaved columns -> [m*H, S, dh] fp32."""
         return t[:, col0:col0 + H * dh].float().reshape(m, S, H, dh).permute(0, 2, 1, 3).reshape(m * H, S, dh)
 
+    def flash_attn_fwd(self, qkv, lse2, o, m, S, d, H, scale):
+        """Emulates gpp_flash_attn_fwd: O = softmax(scale Q K^T) V (P rounded to bf16 as the
+        A operand of the P.V MMA), lse2 = base-2 log-sum-exp of the scaled scores."""
+        dh = d // H
+        q, k, v = (self._heads(qkv, m, S, H, c, dh) for c in (0, d, 2 * d))
+        s2 = scale * (q @ k.transpose(1, 2)) * 1.4426950408889634
+        l2 = torch.logsumexp(s2 * 0.6931471805599453, dim=2) * 1.4426950408889634
+        lse2.copy_(l2.reshape(-1))
+        pr = torch.exp2(s2 - l2[..., None]).to(o.dtype).float()
+        oz = pr @ v
+        o[:, :d].copy_(oz.reshape(m, H, S, dh).permute(0, 2, 1, 3).reshape(m * S, d))
+
+    def flash_attn_bwd(self, qkv, lse2, o, dout, dvec, dqkv, m, S, d, H, scale):
+        """Emulates gpp_flash_attn_bwd: P recomputed from lse2, D = rowsum(dO o O),
+        dS = scale P (dO V^T - D); dQ = dS K, dK = dS^T Q, dV = P^T dO (bf16 operands)."""
+        dh = d // H
+        q, k, v = (self._heads(qkv, m, S, H, c, dh) for c in (0, d, 2 * d))
+        g, oz = self._heads(dout, m, S, H, 0, dh), self._heads(o, m, S, H, 0, dh)
+        D = (g * oz).sum(2, keepdim=True)
+        dvec.copy_(D.reshape(-1))
+        s2 = scale * (q @ k.transpose(1, 2)) * 1.4426950408889634
+        pz = torch.exp2(s2 - lse2.reshape(m * H, S, 1))
+        dsz = scale * pz * (g @ v.transpose(1, 2) - D)
+        pb, dsb = pz.to(dqkv.dtype).float(), dsz.to(dqkv.dtype).float()
+        for col0, t in ((0, dsb @ k), (d, dsb.transpose(1, 2) @ q), (2 * d, pb.transpose(1, 2) @ g)):
+            dqkv[:, col0:col0 + d].copy_(t.reshape(m, H, S, dh).permute(0, 2, 1, 3).reshape(m * S, d))
+
     def attn_fwd(self, qkv, p, o, m, S, d, H, scale):
         """Emulates gpp_attn_fwd: P = softmax(scale Q K^T) (bf16, kept), O = bf16(P) V."""
         dh = d // H

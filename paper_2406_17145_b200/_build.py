@@ -17,7 +17,7 @@ CSRC = PKG_DIR / "csrc"
 INCLUDE = PKG_DIR.parent / "include"
 LIB_PATH = PKG_DIR / "libgpp_b200.so"
 
-SOURCES = ["gemm_sm100.cu", "gemm_simt.cu", "ops.cu", "comm.cu", "mmt_ops.cu", "dlrm_ops.cu", "attn_sm100.cu"]
+SOURCES = ["gemm_sm100.cu", "gemm_simt.cu", "ops.cu", "comm.cu", "mmt_ops.cu", "dlrm_ops.cu", "attn_sm100.cu", "attn_flash_sm100.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

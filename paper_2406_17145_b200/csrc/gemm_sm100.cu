@@ -569,9 +569,6 @@ constexpr bool pair_colsum_epi() { return (EPI == EPI_F32 || EPI == EPI_SGD) && 
 __device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
 
 template <int BN, int STAGES, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS + 32, 1)
@@ -728,11 +725,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS + 32, 1
         for (int kb = 0; kb < kb_total; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
+          // default (.release.cta) remote arrive + CTA-scope wait: a .release.cluster arrive
+          // costs a cluster-scope fence per stage (measured: 4x slower wgrad); the peer's A tile
+          // was written by the pair TMA before the leader's full barrier could complete
           if (leader) {
             mbar_wait(&full_bar[s], ph);
-            if (lane == 0) mbar_arrive_remote_release(peer_cs0 + s * 8);
+            if (lane == 0) mbar_arrive_cluster(peer_cs0 + s * 8);
           } else {
-            mbar_wait_cluster(&cs_bar[s], ph);
+            mbar_wait(&cs_bar[s], ph);
           }
           if (mine) {
             const uint8_t* base = smem + s * STAGE_BYTES + ch * 8192 + half * 8;
@@ -1173,7 +1173,8 @@ static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
   const int splits = choose_splits(tiles, slots, num_kb);
   // bias gradient: fused into the pair kernel's A-tile reads when it runs unsplit; else
   // one column-sum kernel over A ([K, M] row-major for the MN-major dy^T) after the GEMM
-  const bool fuse_cs = ep.colsum != nullptr && pair && splits == 1 && pair_colsum_epi<EPI, A_MN>();
+  static const bool cs_enabled = [] { const char* e = std::getenv("GPP_FUSED_COLSUM"); return !(e && e[0] == '0'); }();
+  const bool fuse_cs = cs_enabled && ep.colsum != nullptr && pair && splits == 1 && pair_colsum_epi<EPI, A_MN>();
   if (ep.colsum != nullptr && !fuse_cs) {
     GPP_ARG_CHECK(A_MN, "fused column sum needs the MN-major (wgrad) A operand");
     EpiParams e2 = ep;

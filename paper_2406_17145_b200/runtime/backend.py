@@ -110,6 +110,12 @@ class CudaBackend:
     def attn_softmax_bwd(self, ds, ldc, p, ldp, dout, ldo, o_rows, v, ldv, v_rows, M, N, K, scale, spec):
         lib.attn_softmax_bwd(ds, ldc, p, ldp, dout, ldo, o_rows, v, ldv, v_rows, M, N, K, scale, spec)
 
+    def flash_attn_fwd(self, qkv, lse2, o, m, S, d, H, scale):
+        lib.flash_attn_fwd(qkv, lse2, o, m, S, d, H, scale)
+
+    def flash_attn_bwd(self, qkv, lse2, o, dout, dvec, dqkv, m, S, d, H, scale):
+        lib.flash_attn_bwd(qkv, lse2, o, dout, dvec, dqkv, m, S, d, H, scale)
+
     def attn_fwd(self, qkv, p, o, m, S, d, H, scale):
         lib.attn_fwd(qkv, p, o, m, S, d, H, scale)
 

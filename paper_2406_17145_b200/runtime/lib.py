@@ -61,6 +61,8 @@ _SIGS = {
     "gpp_meanpool_fwd": ([_vp, _i64, _vp, _i64, _i64, _i64, _vp], _i32),
     "gpp_meanpool_bwd": ([_vp, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
     "gpp_gemm_batched": ([_vp, _i64, _vp, _i64, _i64, _i32, _vp, _i64, _i64, _i32, _i64, _i64, _i64, _f32, _f32, _i32, _vp, _vp], _i32),
+    "gpp_flash_attn_fwd": ([_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
+    "gpp_flash_attn_bwd": ([_vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_attn_fwd": ([_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_attn_bwd": ([_vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_attn_softmax": ([_vp, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp, _vp], _i32),
@@ -346,6 +348,19 @@ def attn_bwd(qkv, p, o, dout, ds, dqkv, m, S, d, H, scale, stream=None):
     Q block of dqkv = ds k (one tcgen05 kernel)."""
     call("gpp_attn_bwd", _ptr(qkv), _ptr(p), _ptr(o), _ld(o), _ptr(dout), _ld(dout), _ptr(ds), _ptr(dqkv), m, S, d,
          H, float(scale), _stream(stream))
+
+
+def flash_attn_fwd(qkv, lse2, o, m, S, d, H, scale, stream=None):
+    """MMT attention forward, P never stored: o[:, h*64..] = softmax(scale q k^T) v and the
+    base-2 row log-sum-exp lse2 [m*H, S] fp32 (packed qkv [m*S, 3d])."""
+    call("gpp_flash_attn_fwd", _ptr(qkv), _ptr(lse2), _ptr(o), _ld(o), m, S, d, H, float(scale), _stream(stream))
+
+
+def flash_attn_bwd(qkv, lse2, o, dout, dvec, dqkv, m, S, d, H, scale, stream=None):
+    """MMT attention backward with P recomputed from q, k and lse2: the Q, K and V blocks
+    of dqkv (dvec: [m*H, S] fp32 scratch for rowsum(dout o o))."""
+    call("gpp_flash_attn_bwd", _ptr(qkv), _ptr(lse2), _ptr(o), _ld(o), _ptr(dout), _ld(dout), _ptr(dvec),
+         _ptr(dqkv), m, S, d, H, float(scale), _stream(stream))
 
 
 def prefetch_hint(t):

@@ -6,17 +6,19 @@
 
 Every matrix product is a libgpp_b200 tcgen05 GEMM: the four projections with fused
 bias / GELU (+ pre-activation) / residual epilogues.  Attention with 64-wide heads and
-S in {128, ..., 512} is ONE kernel per direction (csrc/attn_sm100.cu): scores, softmax
-and P.V forward; dO.V^T, softmax backward and dS.K backward; the remaining dV = P^T dO
-and dK = dS^T Q are batched GEMMs (batch = sample x head, expressed as coordinate
-offsets into the packed QKV buffer).  Other shapes use the scores GEMM with the softmax
-in its epilogue plus batched GEMMs.  The fp32 score / dP matrices never reach HBM.
+S in {128, ..., 512} recomputes P (csrc/attn_flash_sm100.cu): the forward keeps only O
+and the row log-sum-exp; ONE backward kernel rebuilds P from Q, K and the LSE and
+produces dQ, dK and dV (dK/dV accumulated in TMEM, dQ partials summed across a CTA
+cluster) -- no [S x S] matrix of any kind reaches HBM.  (GPP_ATTN_IMPL=p selects the
+P-storing kernels of csrc/attn_sm100.cu plus dV / dK batched GEMMs.)  Other shapes use
+the scores GEMM with the softmax in its epilogue plus batched GEMMs.
 LayerNorm and mean-pool are warp-per-row kernels.  Rows of the executor's [m, S*d] buffers are viewed as [m*S, d] token matrices.
 """
 
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 
@@ -56,7 +58,6 @@ class MMTLayer:
         ring = ex._ring
         self.h1, self.h2, self.o_, self.y1 = ring((T, d)), ring((T, d)), ring((T, d)), ring((T, d))
         self.qkv = ring((T, 3 * d))
-        self.P = ring((Z * S, S))
         self.pre1, self.f = ring((T, f)), ring((T, f))
         self.y2 = ring((T, d)) if self.pool else None
         st = lambda: [torch.zeros(T, dtype=torch.float32, device=dev) for _ in range(ex.ell)]
@@ -67,9 +68,18 @@ class MMTLayer:
         # key row fits TMEM; else unfused GEMM + softmax kernels
         self.flash = S % 128 == 0 and S <= 512 and self.dh == 64 and dt == torch.bfloat16
         self.fused = S <= 512 and S % 32 == 0 and self.dh % 64 == 0 and dt == torch.bfloat16
+        # default for 64-wide heads: recompute attention (O + base-2 LSE forward, P rebuilt in
+        # the backward; csrc/attn_flash_sm100.cu) -- GPP_ATTN_IMPL=p keeps the P-storing kernels
+        self.recompute = self.flash and os.environ.get("GPP_ATTN_IMPL", "flash") != "p"
+        if self.recompute:
+            self.lse = [torch.zeros(Z * S, dtype=torch.float32, device=dev) for _ in range(ex.ell)]
+            self.dvec = torch.zeros(Z * S, dtype=torch.float32, device=dev)
+            self.P = None
+        else:
+            self.P = ring((Z * S, S))
         self.scores = None if self.fused else z((Z * S, S), torch.float32)
         self.dP = None if self.fused else z((Z * S, S), torch.float32)
-        self.dS = z((Z * S, S))
+        self.dS = None if self.recompute else z((Z * S, S))
         self.dy2 = z((T, d)) if self.pool else None
         self.df, self.dh2, self.dy1, self.do = z((T, f)), z((T, d)), z((T, d)), z((T, d))
         self.dqkv, self.dh1 = z((T, 3 * d)), z((T, d))
@@ -84,10 +94,13 @@ class MMTLayer:
 
     def forward(self, x2d: torch.Tensor, out: torch.Tensor, slot: int):
         be, S, d, H, dh, T, Z = self.ex.be, self.S, self.d, self.H, self.dh, self.T, self.Z
-        h1, qkv, P, o_ = self.h1[slot], self.qkv[slot], self.P[slot], self.o_[slot]
+        h1, qkv, o_ = self.h1[slot], self.qkv[slot], self.o_[slot]
+        P = self.P[slot] if self.P is not None else None
         be.layernorm_fwd(h1, self.mean1[slot], self.rstd1[slot], x2d, self._p("ln1_g"), self._p("ln1_b"))
         be.linear_fwd(qkv, h1, self._w("wqkv"), self._p("bqkv"), "none")
-        if self.flash:
+        if self.recompute:
+            be.flash_attn_fwd(qkv, self.lse[slot], o_, self.ex.m, S, d, H, self.scale)
+        elif self.flash:
             be.attn_fwd(qkv, P, o_, self.ex.m, S, d, H, self.scale)
         else:
             self._attention_fwd(qkv, P, o_)
@@ -144,7 +157,22 @@ class MMTLayer:
                          self.mean2[slot], self.rstd2[slot], self._p("ln2_g"), dres=dy2, accumulate=accumulate)
         be.linear_dgrad(self.do, self.dy1, self._w("wo"), None, "none")
         self._wgrad("wo", "bo", self.dy1, self.o_[slot], accumulate, last)
-        qkv, P = self.qkv[slot], self.P[slot]
+        qkv = self.qkv[slot]
+        if self.recompute:
+            # dQ, dK, dV in one kernel, P recomputed from Q, K and the forward's LSE
+            be.flash_attn_bwd(qkv, self.lse[slot], self.o_[slot], self.do, self.dvec, self.dqkv, ex.m, S, d, H,
+                              self.scale)
+        else:
+            self._attention_bwd_stored_p(qkv, self.P[slot], slot)
+        be.linear_dgrad(self.dh1, self.dqkv, self._w("wqkv"), None, "none")
+        self._wgrad("wqkv", "bqkv", self.dqkv, self.h1[slot], accumulate, last)
+        target = dx2d if dx2d is not None else self.dx_scratch
+        be.layernorm_bwd(target, G[(o, "ln1_g")], G[(o, "ln1_b")], self.dh1, x2d, self.mean1[slot],
+                         self.rstd1[slot], self._p("ln1_g"), dres=self.dy1, accumulate=accumulate)
+
+    def _attention_bwd_stored_p(self, qkv, P, slot):
+        ex, be = self.ex, self.ex.be
+        S, d, H, dh, T, Z = self.S, self.d, self.H, self.dh, self.T, self.Z
         # dV[z] = P_z^T dO_z
         be.gemm_batched(self.dqkv, 3 * d, P, S, Z * S, True, self.do, d, T, True, S, dh, S,
                         _spec(Z, H, a_k_hi=H * S, a_k_lo=S, b_n_lo=dh, b_k_hi=S, c0=2 * d, c_hi=S * 3 * d, c_lo=dh))
@@ -166,8 +194,3 @@ class MMTLayer:
         # dK[z] = dS_z^T Q_z
         be.gemm_batched(self.dqkv, 3 * d, self.dS, S, Z * S, True, qkv, 3 * d, T, True, S, dh, S,
                         _spec(Z, H, a_k_hi=H * S, a_k_lo=S, b_n_lo=dh, b_k_hi=S, c0=d, c_hi=S * 3 * d, c_lo=dh))
-        be.linear_dgrad(self.dh1, self.dqkv, self._w("wqkv"), None, "none")
-        self._wgrad("wqkv", "bqkv", self.dqkv, self.h1[slot], accumulate, last)
-        target = dx2d if dx2d is not None else self.dx_scratch
-        be.layernorm_bwd(target, G[(o, "ln1_g")], G[(o, "ln1_b")], self.dh1, x2d, self.mean1[slot],
-                         self.rstd1[slot], self._p("ln1_g"), dres=self.dy1, accumulate=accumulate)

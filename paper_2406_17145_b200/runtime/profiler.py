@@ -34,7 +34,8 @@ GEMM_KINDS = ("fwd", "dgrad", "wgrad")
 _OTHER_CALLS = ("colsum", "rowdot_fwd", "rowdot_bwd", "mse_loss", "bce_loss", "ce_loss", "copy_rows", "copy_rows_multi",
                 "sgd_step", "embbag_fwd", "embbag_sgd", "interaction_fwd", "interaction_bwd",
                 "layernorm_fwd", "layernorm_bwd", "softmax_fwd", "softmax_bwd", "meanpool_fwd",
-                "meanpool_bwd", "attn_softmax", "attn_softmax_bwd", "gemm_batched", "attn_fwd", "attn_bwd")
+                "meanpool_bwd", "attn_softmax", "attn_softmax_bwd", "gemm_batched", "attn_fwd", "attn_bwd",
+                "flash_attn_fwd", "flash_attn_bwd")
 
 
 class TimedBackend(CudaBackend):

@@ -64,6 +64,8 @@ def main():
     r["wgrad_sgd_us"] = timeit(lambda i: lib.linear_wgrad_sgd(master[i], shadow[i], grad[i], dy[i], x[i], 1e-6), L, args.reps)
     r["wgrad_sgd_acc_us"] = timeit(
         lambda i: lib.linear_wgrad_sgd(master[i], shadow[i], grad[i], dy[i], x[i], 1e-6, accumulate=True), L, args.reps)
+    r["wgrad_sgd_bias_us"] = timeit(
+        lambda i: lib.linear_wgrad_sgd(master[i], shadow[i], grad[i], dy[i], x[i], 1e-6, dbias=db), L, args.reps)
     r["wgrad_f32_us"] = timeit(lambda i: lib.linear_wgrad(grad[i], None, dy[i], x[i]), L, args.reps)
     r["colsum_us"] = timeit(lambda i: lib.colsum(db, dy[i]), L, args.reps)
     flops = 2.0 * O * W * B
