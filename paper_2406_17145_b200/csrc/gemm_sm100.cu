@@ -1173,7 +1173,11 @@ static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
   const int splits = choose_splits(tiles, slots, num_kb);
   // bias gradient: fused into the pair kernel's A-tile reads when it runs unsplit; else
   // one column-sum kernel over A ([K, M] row-major for the MN-major dy^T) after the GEMM
-  static const bool cs_enabled = [] { const char* e = std::getenv("GPP_FUSED_COLSUM"); return !(e && e[0] == '0'); }();
+  // Off by default (GPP_FUSED_COLSUM=1 enables it): measured at the MMT shapes the column-sum
+  // warp shares its SM sub-partition with the SGD epilogue warps and stretches the tiles it
+  // sums (wgrad+SGD 3072x1024x8192: 128 us fused vs 54 + 15 us GEMM + column-sum kernel;
+  // CANDLE 4096^2 x 1024: 54 vs 49 + 5 us) -- tools/bench_wgrad_sgd.py, DESIGN.md section 7b
+  static const bool cs_enabled = [] { const char* e = std::getenv("GPP_FUSED_COLSUM"); return e && e[0] == '1'; }();
   const bool fuse_cs = cs_enabled && ep.colsum != nullptr && pair && splits == 1 && pair_colsum_epi<EPI, A_MN>();
   if (ep.colsum != nullptr && !fuse_cs) {
     GPP_ARG_CHECK(A_MN, "fused column sum needs the MN-major (wgrad) A operand");
