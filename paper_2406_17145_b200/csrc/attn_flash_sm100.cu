@@ -498,13 +498,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         for (int i = 0; i < 64; ++i) acc[i] = 0.f;
         for (int rk = 0; rk < nq; ++rk) {  // fixed rank order: deterministic
           const uint32_t src = mapa_shared(part_local, static_cast<uint32_t>(rk));
+          float4 v[16];  // all 16 remote loads in flight before the first add
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = fa_ld_cluster_f4(src + 16 * i);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float4 v = fa_ld_cluster_f4(src + 16 * i);
-            acc[4 * i] += v.x;
-            acc[4 * i + 1] += v.y;
-            acc[4 * i + 2] += v.z;
-            acc[4 * i + 3] += v.w;
+            acc[4 * i] += v[i].x;
+            acc[4 * i + 1] += v[i].y;
+            acc[4 * i + 2] += v[i].z;
+            acc[4 * i + 3] += v[i].w;
           }
         }
         bf16* dst = dqkv + (static_cast<int64_t>(row0) + qb * 128 + r) * ld_dqkv + head * FA_DH;

@@ -116,12 +116,18 @@ class TimedBackend(CudaBackend):
 
     def linear_wgrad(self, dw, db, dy, x, accumulate):
         self._timed("wgrad", dy.shape[1], x.shape[1], dy.shape[0],
-                    lambda: super(TimedBackend, self).linear_wgrad(dw, db, dy, x, accumulate))
+                    lambda: super(TimedBackend, self).linear_wgrad(dw, None, dy, x, accumulate))
+        if db is not None:
+            self.colsum(db, dy, accumulate)
 
     def linear_wgrad_sgd(self, master, shadow, grad, dy, x, lr, accumulate, store_grad, dbias=None):
+        # the bias column sum is its own kernel (the GEMM-fused variant is off by default):
+        # timed apart so the GEMM family's roofline sees only the GEMM
         self._timed("wgrad", dy.shape[1], x.shape[1], dy.shape[0],
                     lambda: super(TimedBackend, self).linear_wgrad_sgd(master, shadow, grad, dy, x, lr,
-                                                                       accumulate, store_grad, dbias))
+                                                                       accumulate, store_grad, None))
+        if dbias is not None:
+            self.colsum(dbias, dy, accumulate)
 
     def time_gemms_alone(self, run_iteration, reps: int = 3) -> dict:
         """Record one iteration's dense GEMM launches (kind, FLOPs, closure), capture them
