@@ -325,7 +325,8 @@ def _attn_flops_per_launch(wl, ex) -> dict:
         if spec.kind == "mmt_layer":
             S, d, H, _, _ = spec.extra
             z = ex.m * H
-            return {"attn_fwd": 4.0 * S * S * (d // H) * z, "attn_bwd": 10.0 * S * S * (d // H) * z}
+            fw, bw = 4.0 * S * S * (d // H) * z, 10.0 * S * S * (d // H) * z
+            return {"attn_fwd": fw, "attn_bwd": bw, "flash_attn_fwd": fw, "flash_attn_bwd": bw}
     return {}
 
 

@@ -224,9 +224,9 @@ int gpp_attn_bwd(const void* qkv, const void* p, const void* o, int64_t ldo, con
  *   gpp_flash_attn_fwd: o[:, h*64..] = softmax(scale q k^T) v, and per (z, query row) the
  *       base-2 log-sum-exp lse2 = scale log2(e) max + log2(sum) ([m*H, S] fp32).
  *   gpp_flash_attn_bwd: dvec = rowsum(dout o o) (caller-owned [m*H, S] fp32 scratch), then
- *       per (z, 128-key block) with P recomputed from q, k, lse2: the dK and dV blocks of
- *       dqkv (summed over every query block in TMEM) and dQ (per-key-block partials summed
- *       in a fixed order across a cluster of S/128 CTAs through distributed shared memory).
+ *       with P recomputed from q, k, lse2: per (z, 128-key block) the dK and dV blocks of
+ *       dqkv (summed over every query block in TMEM), per (z, 128-query block) dQ (summed
+ *       over every key block in TMEM) -- three launches, deterministic.
  * Same layouts and requirements (d == 64 H, S in {128, 256, 384, 512}) as gpp_attn_*;
  * they replace gpp_attn_fwd / gpp_attn_bwd and the two dV / dK batched GEMMs. */
 int gpp_flash_attn_fwd(const void* qkv, float* lse2, void* o, int64_t ldo, int64_t m, int64_t S, int64_t d,

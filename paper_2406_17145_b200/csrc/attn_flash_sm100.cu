@@ -9,19 +9,23 @@
 //           lse2 = alpha log2e max + log2(sum),   P = exp2(alpha log2e s - lse2).
 //   attn_bwd_prep_kernel: D[q] = rowsum(dO o O) per (z, query) -- the FlashAttention
 //       identity rowsum(P o dP) = rowsum(dO o O).
-//   attn_bwd_kv_kernel  : one CTA per (z, 128-key block), a cluster of S/128 CTAs per z.
-//       For each 128-query block: S^T = K Q^T and dP^T = V dO^T (TMEM, lane = key), the
-//       epilogue warps recompute P^T = exp2(alpha log2e s - lse2[q]) and
-//       dS^T = alpha P^T o (dP^T - D[q]), write both as bf16 pairs back into TMEM (the A
-//       operands of dV += P^T dO and dK += dS^T Q, accumulated in TMEM over all query
-//       blocks) and dS^T into shared memory (the MN-major A operand of the partial
-//       dQ_kb = dS K_kb).  The S/128 partial dQ blocks are summed across the cluster in a
-//       fixed rank order through distributed shared memory (deterministic), by the CTA
-//       that owns that query block.  dK, dV go out once, at the end.
+//   attn_bwd_dkdv_kernel: one CTA per (z, 128-key block), looping over 64-query blocks:
+//       S^T = K Q^T and dP^T = V dO^T in TMEM (lane = key); the epilogue warps recompute
+//       P^T = exp2(alpha log2e s - lse2[q]) and dS^T = alpha P^T o (dP^T - D[q]) and write both
+//       as bf16 pairs back over the consumed columns -- the TMEM A operands of
+//       dV += P^T dO and dK += dS^T Q, accumulated in TMEM over every query block.
+//   attn_bwd_dq_kernel  : one CTA per (z, 128-query block), looping over 64-key blocks:
+//       S, dP recomputed (lane = query, lse2 / D are row constants), dS in place in TMEM,
+//       dQ += dS K.  (A single kernel reducing per-key-block dQ partials across a CTA
+//       cluster through DSMEM measured 363 us vs 149 us without the exchange: the exchange
+//       serialised the cluster; the recompute of S and dP here costs less.)
+//   Both hold 256 TMEM columns, so two CTAs share an SM and overlap their phases.
 //
 // Layout: packed QKV [m S, 3d] (Q | K | V, head h at columns h*64), o / dout [m S, d]
 // head-interleaved, lse2 / D [Z, S] fp32 with z = sample * H + head.
 #include <cuda.h>
+
+#include <cstdlib>
 
 #include "gemm.cuh"
 #include "tc_ptx.cuh"
@@ -232,306 +236,364 @@ __global__ void __launch_bounds__(FW_THREADS, 2)
   }
 }
 
-// D[z, s] = sum_c dO[row, head*64 + c] * O[row, head*64 + c]: one warp per (row, head),
-// 4 bytes per lane of each operand.
+// D[z, s] = sum_c dO[row, head*64 + c] * O[row, head*64 + c]: one thread per (row, head),
+// eight 16-byte loads of each operand in flight.
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(float* __restrict__ dvec, const bf16* __restrict__ o,
                                                             int64_t ldo, const bf16* __restrict__ dout, int64_t lddo,
                                                             int64_t T, int S, int H) {
-  const int64_t w = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (w >= T * H) return;
-  const int64_t row = w / H;
-  const int head = static_cast<int>(w % H);
-  const float2 a = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(o + row * ldo + head * FA_DH)[lane]);
-  const float2 b = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(dout + row * lddo + head * FA_DH)[lane]);
-  float v = fmaf(a.x, b.x, a.y * b.y);
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (t >= T * H) return;
+  const int64_t row = t / H;
+  const int head = static_cast<int>(t % H);
+  const uint4* a = reinterpret_cast<const uint4*>(o + row * ldo + head * FA_DH);
+  const uint4* b = reinterpret_cast<const uint4*>(dout + row * lddo + head * FA_DH);
+  uint4 va[8], vb[8];
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  if (lane == 0) {
-    const int64_t sample = row / S;
-    dvec[(sample * H + head) * S + row % S] = v;
+  for (int i = 0; i < 8; ++i) {
+    va[i] = __ldg(a + i);
+    vb[i] = __ldg(b + i);
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t* ua = reinterpret_cast<const uint32_t*>(&va[i]);
+    const uint32_t* ub = reinterpret_cast<const uint32_t*>(&vb[i]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ua[k]));
+      const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ub[k]));
+      acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+    }
+  }
+  const int64_t sample = row / S;
+  dvec[(sample * H + head) * S + row % S] = acc;
+}
+
+// ---------------------------------------------------------------------------------------
+// Backward: two kernels, no cross-CTA reduction, 256 TMEM columns each (two CTAs per SM, so
+// one CTA's softmax phase overlaps the other's loads and MMAs).  Blocks of 64 on the loop
+// dimension.  Warps: 0 TMA, 1 MMA (+ TMEM alloc), 2..9 two per TMEM lane quarter (one row
+// each), splitting the 64 columns of a block into two 32-column chunks.
+namespace {
+constexpr int BW_SMW = 8;
+constexpr int BW_THREADS = 64 + 32 * BW_SMW;
+constexpr int BW_STAGES = 3;
+constexpr uint32_t TILE64 = 64 * 128;    // 64 rows x 64 bf16 (128B-swizzled): 8 KB
+constexpr uint32_t TILE128 = 128 * 128;  // 16 KB
+
+__device__ __forceinline__ void fa_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 fp32 values -> bf16 -> 64 contiguous bytes
+__device__ __forceinline__ void fa_store_row32(bf16* dst, const uint32_t (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint4 pk;
+    pk.x = fa_pack(__uint_as_float(v[8 * i + 0]), __uint_as_float(v[8 * i + 1]));
+    pk.y = fa_pack(__uint_as_float(v[8 * i + 2]), __uint_as_float(v[8 * i + 3]));
+    pk.z = fa_pack(__uint_as_float(v[8 * i + 4]), __uint_as_float(v[8 * i + 5]));
+    pk.w = fa_pack(__uint_as_float(v[8 * i + 6]), __uint_as_float(v[8 * i + 7]));
+    *reinterpret_cast<uint4*>(dst + 8 * i) = pk;
   }
 }
 
-
-// ---------------------------------------------------------------------------------------
-// Backward, key-block major (see the file comment).  Warps: 0 TMA, 1 MMA (+ TMEM alloc),
-// 2..9 softmax-gradient warps (lane quarter q = warp % 4 = 32 keys, query half hf),
-// 10..13 dQ warps (lane quarter = 32 queries of the partial dQ).
-namespace {
-constexpr int BW_SM_WARPS = 8;
-constexpr int BW_DQ_WARPS = 4;
-constexpr int BW_THREADS = 64 + 32 * (BW_SM_WARPS + BW_DQ_WARPS);
-constexpr uint32_t BW_K = 0, BW_V = 16384;
-constexpr uint32_t BW_Q = 32768;      // [2] x 16 KB
-constexpr uint32_t BW_DO = 65536;     // [2] x 16 KB
-constexpr uint32_t BW_ADS = 98304;    // dS as the MN-major A of dQ = dS K: 2 chunks x 16 KB
-constexpr uint32_t BW_DQP = 131072;   // [2] partial dQ, 128 rows x DQ_LD fp32
-constexpr int DQ_LD = 68;             // floats per partial row (16-byte stores conflict-free)
-constexpr uint32_t DQP_BYTES = 128 * DQ_LD * 4;
-constexpr uint32_t BW_VEC = BW_DQP + 2 * DQP_BYTES;   // [2] x (lse2[128] | D[128])
-constexpr uint32_t BW_BAR = BW_VEC + 2 * 1024;
-constexpr int SMEM_BWKV = BW_BAR + 256 + 1024;
-// TMEM columns
-constexpr uint32_t T_ST = 0, T_DPT = 128, T_DV = 256, T_DK = 320, T_DQ = 384;  // T_DQ: [2] x 64
-
-__device__ __forceinline__ void fa_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ float4 fa_ld_cluster_f4(uint32_t cluster_addr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(cluster_addr)
-               : "memory");
-  return v;
-}
+// dK / dV smem: K, V (128 keys) | stages of [Q 64 rows | dO 64 rows | lse2[64] | D[64]]
+constexpr uint32_t KV_STAGE = 2 * TILE64 + 512;
+constexpr uint32_t KV_STAGE_STRIDE = (KV_STAGE + 1023) / 1024 * 1024;
+constexpr uint32_t KV_RING = 2 * TILE128;
+constexpr uint32_t KV_BAR = KV_RING + BW_STAGES * KV_STAGE_STRIDE;
+constexpr int SMEM_DKDV = KV_BAR + 256 + 1024;
+// dQ smem: Q, dO (128 queries) | stages of [K 64 rows | V 64 rows]
+constexpr uint32_t DQ_RING = 2 * TILE128;
+constexpr uint32_t DQ_BAR = DQ_RING + BW_STAGES * 2 * TILE64;
+constexpr int SMEM_DQ = DQ_BAR + 256 + 1024;
 }  // namespace
 
-__global__ void __launch_bounds__(BW_THREADS, 1)
-    attn_bwd_kv_kernel(const __grid_constant__ CUtensorMap m_qkv, const __grid_constant__ CUtensorMap m_do,
-                       const float* __restrict__ lse2, const float* __restrict__ dvec, bf16* __restrict__ dqkv,
-                       int64_t ld_dqkv, FaShape sh) {
-  constexpr uint32_t IDESC_ST = idesc_bf16<128, false, false>();   // S^T, dP^T: K-major A and B
-  constexpr uint32_t IDESC_DVK = idesc_bf16<FA_DH, false, true>(); // A = TMEM, B = MN-major tile
-  constexpr uint32_t IDESC_DQ = idesc_bf16<FA_DH, true, true>();   // A = dS (MN-major smem)
+// dK, dV of one (z, 128-key block), looping over the S/64 query blocks:
+//   S^T = K Q_j^T, dP^T = V dO_j^T (TMEM, lane = key, 64 query columns each);
+//   P^T = exp2(alpha log2e S^T - lse2[q]), dS^T = alpha P^T o (dP^T - D[q]) -> bf16 pairs in
+//   place (TMEM A operands);  dV += P^T dO_j, dK += dS^T Q_j (accumulated in TMEM).
+__global__ void __launch_bounds__(BW_THREADS, 2)
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap m_k128, const __grid_constant__ CUtensorMap m_q64,
+                         const __grid_constant__ CUtensorMap m_do64, const float* __restrict__ lse2,
+                         const float* __restrict__ dvec, bf16* __restrict__ dqkv, int64_t ld_dqkv, FaShape sh) {
+  constexpr uint32_t IDESC_ST = idesc_bf16<64, false, false>();
+  constexpr uint32_t IDESC_AC = idesc_bf16<FA_DH, false, true>();
+  constexpr uint32_t T_ST = 0, T_DPT = 64, T_DV = 128, T_DK = 192;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BW_BAR);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + KV_BAR);
   uint64_t* bar_kv = bar + 0;
-  uint64_t* bar_qfull = bar + 1;   // [2]
-  uint64_t* bar_qfree = bar + 3;   // [2]
-  uint64_t* bar_s = bar + 5;       // S^T, dP^T in TMEM
-  uint64_t* bar_p = bar + 6;       // P, dS in TMEM + dS in smem (8 softmax warps)
-  uint64_t* bar_mma2 = bar + 7;    // dV, dK, dQ MMAs of the query block done
-  uint64_t* bar_dqfree = bar + 8;  // dQ warps have read the dQ accumulator (4 warps)
-  uint64_t* bar_dqfull = bar + 9;  // [2] owner: every CTA's partial of the block is in place
-  uint64_t* bar_dqempty = bar + 11;  // [2] this CTA's partial buffer may be overwritten
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* bar_full = bar + 1;                 // [BW_STAGES]
+  uint64_t* bar_free = bar + 1 + BW_STAGES;     // [BW_STAGES]
+  uint64_t* bar_s = bar + 1 + 2 * BW_STAGES;    // S^T, dP^T in TMEM
+  uint64_t* bar_p = bar + 2 + 2 * BW_STAGES;    // P^T, dS^T (bf16) in TMEM (8 warps)
+  uint64_t* bar_done = bar + 3 + 2 * BW_STAGES; // every MMA done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4 + 2 * BW_STAGES);
 
   const int S = sh.S, d = sh.d, H = sh.H;
-  const int nq = S / 128;  // query blocks = key blocks = cluster size
+  const int nkb = S / 128, nq = S / 64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = static_cast<int>(blockIdx.x) % nq;  // == %cluster_ctarank
-  const int z = static_cast<int>(blockIdx.x) / nq;
+  const int z = static_cast<int>(blockIdx.x) / nkb;
+  const int kb = static_cast<int>(blockIdx.x) % nkb;
   const int sample = z / H, head = z % H;
   const int row0 = sample * S;
   const float sl2 = sh.alpha * 1.4426950408889634f;
 
   if (warp == 0 && lane == 0) {
     mbar_init(bar_kv, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar_qfull[i], 1);
-      mbar_init(&bar_qfree[i], 1);
-      mbar_init(&bar_dqfull[i], nq);
-      mbar_init(&bar_dqempty[i], 1);
+    for (int i = 0; i < BW_STAGES; ++i) {
+      mbar_init(&bar_full[i], 1);
+      mbar_init(&bar_free[i], 1);
     }
     mbar_init(bar_s, 1);
-    mbar_init(bar_p, BW_SM_WARPS);
-    mbar_init(bar_mma2, 1);
-    mbar_init(bar_dqfree, BW_DQ_WARPS);
+    mbar_init(bar_p, BW_SMW);
+    mbar_init(bar_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  cluster_sync();  // barriers of every CTA initialised before any remote arrive
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // K, V of this key block once; Q, dO per query block through a 2-stage ring
-      mbar_expect_tx(bar_kv, 2 * 16384);
-      tma_load_2d(smem + BW_K, &m_qkv, bar_kv, d + head * FA_DH, row0 + kb * 128);
-      tma_load_2d(smem + BW_V, &m_qkv, bar_kv, 2 * d + head * FA_DH, row0 + kb * 128);
-      for (int qb = 0; qb < nq; ++qb) {
-        const int st = qb & 1;
-        mbar_wait(&bar_qfree[st], ((qb >> 1) & 1) ^ 1);
-        mbar_expect_tx(&bar_qfull[st], 2 * 16384);
-        tma_load_2d(smem + BW_Q + st * 16384, &m_qkv, &bar_qfull[st], head * FA_DH, row0 + qb * 128);
-        tma_load_2d(smem + BW_DO + st * 16384, &m_do, &bar_qfull[st], head * FA_DH, row0 + qb * 128);
+      mbar_expect_tx(bar_kv, 2 * TILE128);
+      tma_load_2d(smem, &m_k128, bar_kv, d + head * FA_DH, row0 + kb * 128);
+      tma_load_2d(smem + TILE128, &m_k128, bar_kv, 2 * d + head * FA_DH, row0 + kb * 128);
+      const float* lz = lse2 + static_cast<int64_t>(z) * S;
+      const float* dz = dvec + static_cast<int64_t>(z) * S;
+      for (int j = 0; j < nq; ++j) {
+        const int st = j % BW_STAGES;
+        mbar_wait(&bar_free[st], ((j / BW_STAGES) & 1) ^ 1);
+        uint8_t* sb = smem + KV_RING + st * KV_STAGE_STRIDE;
+        mbar_expect_tx(&bar_full[st], 2 * TILE64 + 512);
+        tma_load_2d(sb, &m_q64, &bar_full[st], head * FA_DH, row0 + j * 64);
+        tma_load_2d(sb + TILE64, &m_do64, &bar_full[st], head * FA_DH, row0 + j * 64);
+        fa_bulk_load(sb + 2 * TILE64, lz + j * 64, 256, &bar_full[st]);
+        fa_bulk_load(sb + 2 * TILE64 + 256, dz + j * 64, 256, &bar_full[st]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t ka = smem_u32(smem + BW_K), va = smem_u32(smem + BW_V), dsa = smem_u32(smem + BW_ADS);
+      const uint32_t ka = smem_u32(smem), va = smem_u32(smem + TILE128);
       mbar_wait(bar_kv, 0);
-      for (int qb = 0; qb < nq; ++qb) {
-        const int st = qb & 1;
-        const uint32_t qa = smem_u32(smem + BW_Q + st * 16384), da = smem_u32(smem + BW_DO + st * 16384);
-        mbar_wait(&bar_qfull[st], (qb >> 1) & 1);
+      for (int j = 0; j < nq; ++j) {
+        const int st = j % BW_STAGES;
+        const uint32_t qa = smem_u32(smem + KV_RING + st * KV_STAGE_STRIDE), da = qa + TILE64;
+        mbar_wait(&bar_full[st], (j / BW_STAGES) & 1);
         tc_fence_after();
-        // S^T = K Q^T and dP^T = V dO^T (lane = key, column = query)
 #pragma unroll
         for (int k = 0; k < FA_DH / 16; ++k) {
           umma_bf16(tmem + T_ST, sdesc_sw128(ka + k * 32, 16, 1024), sdesc_sw128(qa + k * 32, 16, 1024), IDESC_ST, k != 0);
           umma_bf16(tmem + T_DPT, sdesc_sw128(va + k * 32, 16, 1024), sdesc_sw128(da + k * 32, 16, 1024), IDESC_ST, k != 0);
         }
         umma_commit(bar_s);
-        mbar_wait(bar_p, qb & 1);  // P^T, dS^T (bf16) in TMEM, dS in smem
-        if (qb > 0) mbar_wait(bar_dqfree, (qb - 1) & 1);  // dQ accumulator of qb-1 read out
+        mbar_wait(bar_p, j & 1);
         tc_fence_after();
-        const uint32_t dq = tmem + T_DQ + (qb & 1) * 64;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {  // K = 128 queries (dV, dK) / 128 keys (dQ), 16 per MMA
-          const uint32_t acol = (k >> 2) * 64 + (k & 3) * 8;  // packed pairs of query half k/4
-          const uint32_t acc = (qb | k) != 0;
-          fa_umma_ts(tmem + T_DV, tmem + T_ST + acol, sdesc_sw128(da + k * 2048, 8192, 1024), IDESC_DVK, acc);
-          fa_umma_ts(tmem + T_DK, tmem + T_DPT + acol, sdesc_sw128(qa + k * 2048, 8192, 1024), IDESC_DVK, acc);
-          umma_bf16(dq, sdesc_sw128(dsa + k * 2048, 16384, 1024), sdesc_sw128(ka + k * 2048, 8192, 1024), IDESC_DQ,
-                    k != 0);
+        for (int k = 0; k < 4; ++k) {  // K = 64 queries, 16 per MMA (8 packed columns)
+          const uint32_t acc = (j | k) != 0;
+          fa_umma_ts(tmem + T_DV, tmem + T_ST + k * 8, sdesc_sw128(da + k * 2048, 8192, 1024), IDESC_AC, acc);
+          fa_umma_ts(tmem + T_DK, tmem + T_DPT + k * 8, sdesc_sw128(qa + k * 2048, 8192, 1024), IDESC_AC, acc);
         }
-        umma_commit(bar_mma2);
-        umma_commit(&bar_qfree[st]);
+        umma_commit(&bar_free[st]);
       }
+      umma_commit(bar_done);
     }
-  } else if (warp < 2 + BW_SM_WARPS) {
-    // ---- softmax-gradient warps: key row lr (TMEM lane), queries [hf*64, hf*64 + 64) ----
-    const int q = warp & 3, hf = (warp - 2) / 4;
-    const int lr = q * 32 + lane;
-    const int tid = threadIdx.x - 64;  // 0..255
+  } else {
+    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 32-query chunk
+    const int lr = q * 32 + lane;  // key row
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    uint8_t* ads = smem + BW_ADS + hf * 16384 + lr * 128;
-    for (int qb = 0; qb < nq; ++qb) {
-      float* vec = reinterpret_cast<float*>(smem + BW_VEC + (qb & 1) * 1024);  // lse2[128] | D[128]
-      {
-        const int64_t base = static_cast<int64_t>(z) * S + qb * 128;
-        vec[tid] = tid < 128 ? __ldg(lse2 + base + tid) : __ldg(dvec + base + tid - 128);
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * BW_SM_WARPS) : "memory");
-      mbar_wait(bar_s, qb & 1);
-      if (qb > 0) mbar_wait(bar_mma2, (qb - 1) & 1);  // dQ MMA of qb-1 done reading smem dS
+    for (int j = 0; j < nq; ++j) {
+      const int st = j % BW_STAGES;
+      const float* vec = reinterpret_cast<const float*>(smem + KV_RING + st * KV_STAGE_STRIDE + 2 * TILE64);
+      mbar_wait(&bar_full[st], (j / BW_STAGES) & 1);  // lse2 / D of the stage (TMA-written)
+      mbar_wait(bar_s, j & 1);
       tc_fence_after();
+      uint32_t sv[32], pv[32];
+      tmem_ld32(trow + T_ST + c * 32, sv);
+      tmem_ld32(trow + T_DPT + c * 32, pv);
+      uint32_t pk[16], dk[16];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int q0 = hf * 64 + c * 32;  // first query of this 32-column chunk
-        uint32_t sv[32], pv[32];
-        tmem_ld32(trow + T_ST + q0, sv);
-        tmem_ld32(trow + T_DPT + q0, pv);
-        uint32_t pk[16], dk[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 ls = *reinterpret_cast<const float2*>(vec + q0 + 2 * j);
-          const float2 dd = *reinterpret_cast<const float2*>(vec + 128 + q0 + 2 * j);
-          const float p0 = exp2f(fmaf(__uint_as_float(sv[2 * j]), sl2, -ls.x));
-          const float p1 = exp2f(fmaf(__uint_as_float(sv[2 * j + 1]), sl2, -ls.y));
-          const float g0 = sh.alpha * p0 * (__uint_as_float(pv[2 * j]) - dd.x);
-          const float g1 = sh.alpha * p1 * (__uint_as_float(pv[2 * j + 1]) - dd.y);
-          pk[j] = fa_pack(p0, p1);
-          dk[j] = fa_pack(g0, g1);
-        }
-        // packed bf16 pairs over this chunk's own (consumed) columns: query pair j of the
-        // chunk at column hf*64 + c*16 + j -- the MMA reads A column (k>>2)*64 + (k&3)*8
-        fa_tmem_st16(trow + T_ST + hf * 64 + c * 16, pk);
-        fa_tmem_st16(trow + T_DPT + hf * 64 + c * 16, dk);
-        // dS^T row lr -> MN-major A of dQ: query chunk hf (64 queries), 16-byte units c*4..c*4+3
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int u = c * 4 + i;
-          *reinterpret_cast<uint4*>(ads + ((u ^ (lr & 7)) << 4)) = make_uint4(dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]);
-        }
+      for (int i = 0; i < 16; ++i) {
+        const float2 ls = *reinterpret_cast<const float2*>(vec + c * 32 + 2 * i);
+        const float2 dd = *reinterpret_cast<const float2*>(vec + 64 + c * 32 + 2 * i);
+        const float p0 = exp2f(fmaf(__uint_as_float(sv[2 * i]), sl2, -ls.x));
+        const float p1 = exp2f(fmaf(__uint_as_float(sv[2 * i + 1]), sl2, -ls.y));
+        pk[i] = fa_pack(p0, p1);
+        dk[i] = fa_pack(sh.alpha * p0 * (__uint_as_float(pv[2 * i]) - dd.x),
+                        sh.alpha * p1 * (__uint_as_float(pv[2 * i + 1]) - dd.y));
       }
+      // bf16 pairs: queries 32c + 2i, +1 -> column 16c + i.  Chunk 1's pairs land in chunk 0's
+      // columns, so both warps of the quarter must have read theirs first.
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      fa_tmem_st16(trow + T_ST + c * 16, pk);
+      fa_tmem_st16(trow + T_DPT + c * 16, dk);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) fa_mbar_arrive(bar_p);
     }
-    // dV (hf = 0) / dK (hf = 1) of key row lr: accumulated over every query block
-    mbar_wait(bar_mma2, (nq - 1) & 1);
+    mbar_wait(bar_done, 0);
     tc_fence_after();
     const int64_t krow = static_cast<int64_t>(row0) + kb * 128 + lr;
-    bf16* dst = dqkv + krow * ld_dqkv + (hf == 0 ? 2 * d : d) + head * FA_DH;
-    const uint32_t src = trow + (hf == 0 ? T_DV : T_DK);
+    // chunk-0 warps write dV, chunk-1 warps dK
+    const uint32_t src = trow + (c == 0 ? T_DV : T_DK);
+    bf16* dst = dqkv + krow * ld_dqkv + (c == 0 ? 2 * d : d) + head * FA_DH;
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
       uint32_t v[32];
       tmem_ld32(src + h2 * 32, v);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        uint4 pkd;
-        pkd.x = fa_pack(__uint_as_float(v[8 * i + 0]), __uint_as_float(v[8 * i + 1]));
-        pkd.y = fa_pack(__uint_as_float(v[8 * i + 2]), __uint_as_float(v[8 * i + 3]));
-        pkd.z = fa_pack(__uint_as_float(v[8 * i + 4]), __uint_as_float(v[8 * i + 5]));
-        pkd.w = fa_pack(__uint_as_float(v[8 * i + 6]), __uint_as_float(v[8 * i + 7]));
-        *reinterpret_cast<uint4*>(dst + h2 * 32 + 8 * i) = pkd;
-      }
-    }
-  } else {
-    // ---- dQ warps: partial dQ of query block qb (row = query r = 32q + lane) -> smem;
-    // the owner CTA (rank qb) sums every rank's partial in rank order -> dqkv ----
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    for (int qb = 0; qb < nq; ++qb) {
-      const int b = qb & 1;
-      float* part = reinterpret_cast<float*>(smem + BW_DQP + b * DQP_BYTES) + r * DQ_LD;
-      if (qb >= 2) mbar_wait(&bar_dqempty[b], ((qb >> 1) - 1) & 1);  // owner of qb-2 done reading
-      mbar_wait(bar_mma2, qb & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        uint32_t v[32];
-        tmem_ld32(trow + T_DQ + b * 64 + h2 * 32, v);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          *reinterpret_cast<float4*>(part + h2 * 32 + 4 * i) =
-              make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]), __uint_as_float(v[4 * i + 2]),
-                          __uint_as_float(v[4 * i + 3]));
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) fa_mbar_arrive(bar_dqfree);
-      asm volatile("bar.sync 3, %0;" ::"n"(32 * BW_DQ_WARPS) : "memory");
-      if (threadIdx.x == 64 + 32 * BW_SM_WARPS) {  // one arrival per CTA on the owner's barrier
-        fa_arrive_remote(mapa_shared(smem_u32(&bar_dqfull[b]), static_cast<uint32_t>(qb)));
-      }
-      if (qb == kb) {  // this CTA owns query block qb
-        mbar_wait_cluster(&bar_dqfull[b], 0);  // a CTA owns one query block: one phase
-        const uint32_t part_local = smem_u32(smem + BW_DQP + b * DQP_BYTES) + r * DQ_LD * 4;
-        float acc[64];
-#pragma unroll
-        for (int i = 0; i < 64; ++i) acc[i] = 0.f;
-        for (int rk = 0; rk < nq; ++rk) {  // fixed rank order: deterministic
-          const uint32_t src = mapa_shared(part_local, static_cast<uint32_t>(rk));
-          float4 v[16];  // all 16 remote loads in flight before the first add
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = fa_ld_cluster_f4(src + 16 * i);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            acc[4 * i] += v[i].x;
-            acc[4 * i + 1] += v[i].y;
-            acc[4 * i + 2] += v[i].z;
-            acc[4 * i + 3] += v[i].w;
-          }
-        }
-        bf16* dst = dqkv + (static_cast<int64_t>(row0) + qb * 128 + r) * ld_dqkv + head * FA_DH;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          uint4 pkd;
-          pkd.x = fa_pack(acc[8 * i + 0], acc[8 * i + 1]);
-          pkd.y = fa_pack(acc[8 * i + 2], acc[8 * i + 3]);
-          pkd.z = fa_pack(acc[8 * i + 4], acc[8 * i + 5]);
-          pkd.w = fa_pack(acc[8 * i + 6], acc[8 * i + 7]);
-          *reinterpret_cast<uint4*>(dst + 8 * i) = pkd;
-        }
-        asm volatile("bar.sync 3, %0;" ::"n"(32 * BW_DQ_WARPS) : "memory");  // all rows read
-        if (threadIdx.x == 64 + 32 * BW_SM_WARPS) {
-          for (int rk = 0; rk < nq; ++rk)  // every rank may now overwrite its buffer b
-            fa_arrive_remote(mapa_shared(smem_u32(&bar_dqempty[b]), static_cast<uint32_t>(rk)));
-        }
-      }
+      fa_store_row32(dst + h2 * 32, v);
     }
   }
   tc_fence_before();
-  cluster_sync();  // no CTA leaves while a peer may still read its partial dQ
+  __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  }
+}
+
+// dQ of one (z, 128-query block), looping over the S/64 key blocks:
+//   S = Q K_j^T, dP = dO V_j^T (TMEM, lane = query);  dS = alpha P o (dP - D[q]) with
+//   P = exp2(alpha log2e S - lse2[q]) (row constants in registers) -> bf16 pairs in place;
+//   dQ += dS K_j (A operand from TMEM).
+__global__ void __launch_bounds__(BW_THREADS, 2)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap m_q128, const __grid_constant__ CUtensorMap m_do128,
+                       const __grid_constant__ CUtensorMap m_k64, const float* __restrict__ lse2,
+                       const float* __restrict__ dvec, bf16* __restrict__ dqkv, int64_t ld_dqkv, FaShape sh) {
+  constexpr uint32_t IDESC_S = idesc_bf16<64, false, false>();
+  constexpr uint32_t IDESC_AC = idesc_bf16<FA_DH, false, true>();
+  constexpr uint32_t T_S = 0, T_DP = 64, T_DQ = 128;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + DQ_BAR);
+  uint64_t* bar_qo = bar + 0;
+  uint64_t* bar_full = bar + 1;
+  uint64_t* bar_free = bar + 1 + BW_STAGES;
+  uint64_t* bar_s = bar + 1 + 2 * BW_STAGES;
+  uint64_t* bar_p = bar + 2 + 2 * BW_STAGES;
+  uint64_t* bar_done = bar + 3 + 2 * BW_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4 + 2 * BW_STAGES);
+
+  const int S = sh.S, d = sh.d, H = sh.H;
+  const int nqb = S / 128, nk = S / 64;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int z = static_cast<int>(blockIdx.x) / nqb;
+  const int qb = static_cast<int>(blockIdx.x) % nqb;
+  const int sample = z / H, head = z % H;
+  const int row0 = sample * S;
+  const float sl2 = sh.alpha * 1.4426950408889634f;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(bar_qo, 1);
+    for (int i = 0; i < BW_STAGES; ++i) {
+      mbar_init(&bar_full[i], 1);
+      mbar_init(&bar_free[i], 1);
+    }
+    mbar_init(bar_s, 1);
+    mbar_init(bar_p, BW_SMW);
+    mbar_init(bar_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(bar_qo, 2 * TILE128);
+      tma_load_2d(smem, &m_q128, bar_qo, head * FA_DH, row0 + qb * 128);
+      tma_load_2d(smem + TILE128, &m_do128, bar_qo, head * FA_DH, row0 + qb * 128);
+      for (int j = 0; j < nk; ++j) {
+        const int st = j % BW_STAGES;
+        mbar_wait(&bar_free[st], ((j / BW_STAGES) & 1) ^ 1);
+        uint8_t* sb = smem + DQ_RING + st * 2 * TILE64;
+        mbar_expect_tx(&bar_full[st], 2 * TILE64);
+        tma_load_2d(sb, &m_k64, &bar_full[st], d + head * FA_DH, row0 + j * 64);
+        tma_load_2d(sb + TILE64, &m_k64, &bar_full[st], 2 * d + head * FA_DH, row0 + j * 64);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t qa = smem_u32(smem), da = smem_u32(smem + TILE128);
+      mbar_wait(bar_qo, 0);
+      for (int j = 0; j < nk; ++j) {
+        const int st = j % BW_STAGES;
+        const uint32_t ka = smem_u32(smem + DQ_RING + st * 2 * TILE64), va = ka + TILE64;
+        mbar_wait(&bar_full[st], (j / BW_STAGES) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < FA_DH / 16; ++k) {
+          umma_bf16(tmem + T_S, sdesc_sw128(qa + k * 32, 16, 1024), sdesc_sw128(ka + k * 32, 16, 1024), IDESC_S, k != 0);
+          umma_bf16(tmem + T_DP, sdesc_sw128(da + k * 32, 16, 1024), sdesc_sw128(va + k * 32, 16, 1024), IDESC_S, k != 0);
+        }
+        umma_commit(bar_s);
+        mbar_wait(bar_p, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // K = 64 keys, 16 per MMA; B = K_j as the MN-major (key rows) operand
+          fa_umma_ts(tmem + T_DQ, tmem + T_S + k * 8, sdesc_sw128(ka + k * 2048, 8192, 1024), IDESC_AC, (j | k) != 0);
+        umma_commit(&bar_free[st]);
+      }
+      umma_commit(bar_done);
+    }
+  } else {
+    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 32-key chunk
+    const int lr = q * 32 + lane;  // query row
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const int64_t zq = static_cast<int64_t>(z) * S + qb * 128 + lr;
+    const float mls = -__ldg(lse2 + zq), dq = __ldg(dvec + zq);
+    for (int j = 0; j < nk; ++j) {
+      mbar_wait(bar_s, j & 1);
+      tc_fence_after();
+      uint32_t sv[32], pv[32];
+      tmem_ld32(trow + T_S + c * 32, sv);
+      tmem_ld32(trow + T_DP + c * 32, pv);
+      uint32_t dk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float p0 = exp2f(fmaf(__uint_as_float(sv[2 * i]), sl2, mls));
+        const float p1 = exp2f(fmaf(__uint_as_float(sv[2 * i + 1]), sl2, mls));
+        dk[i] = fa_pack(sh.alpha * p0 * (__uint_as_float(pv[2 * i]) - dq),
+                        sh.alpha * p1 * (__uint_as_float(pv[2 * i + 1]) - dq));
+      }
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // chunk 0 read before chunk 1 lands
+      fa_tmem_st16(trow + T_S + c * 16, dk);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) fa_mbar_arrive(bar_p);
+    }
+    mbar_wait(bar_done, 0);
+    tc_fence_after();
+    const int64_t qrow = static_cast<int64_t>(row0) + qb * 128 + lr;
+    uint32_t v[32];
+    tmem_ld32(trow + T_DQ + c * 32, v);
+    fa_store_row32(dqkv + qrow * ld_dqkv + head * FA_DH + c * 32, v);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -586,39 +648,32 @@ int gpp_flash_attn_bwd(const void* qkv, const float* lse2, const void* o, int64_
                     (reinterpret_cast<uintptr_t>(dout) & 15) == 0, "16-byte alignment");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t T = m * S, Z = m * H;
-  tc::attn_bwd_prep_kernel<<<static_cast<unsigned>((T * H + 7) / 8), 256, 0, s>>>(
+  GPP_ARG_CHECK(ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(o) & 15) == 0, "16-byte aligned o");
+  tc::attn_bwd_prep_kernel<<<static_cast<unsigned>((T * H + 255) / 256), 256, 0, s>>>(
       dvec, static_cast<const bf16*>(o), ldo, static_cast<const bf16*>(dout), lddo, T, static_cast<int>(S),
       static_cast<int>(H));
   GPP_LAUNCH_CHECK();
-  CUtensorMap mqkv, mdo;
-  if ((rc = tc::make_map_bf16(&mqkv, qkv, 3 * d, T, 3 * d, 64, 128))) return rc;
-  if ((rc = tc::make_map_bf16(&mdo, dout, d, T, lddo, 64, 128))) return rc;
+  CUtensorMap mk128, mq64, mdo64, mq128, mdo128, mk64;
+  if ((rc = tc::make_map_bf16(&mk128, qkv, 3 * d, T, 3 * d, 64, 128))) return rc;
+  if ((rc = tc::make_map_bf16(&mq64, qkv, 3 * d, T, 3 * d, 64, 64))) return rc;
+  if ((rc = tc::make_map_bf16(&mdo64, dout, d, T, lddo, 64, 64))) return rc;
+  if ((rc = tc::make_map_bf16(&mdo128, dout, d, T, lddo, 64, 128))) return rc;
+  mq128 = mk128;  // same qkv map (box 64 x 128), Q block by coordinates
+  mk64 = mq64;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc::attn_bwd_kv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BWKV);
-    cudaFuncSetAttribute(tc::attn_bwd_kv_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(tc::attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_DKDV);
+    cudaFuncSetAttribute(tc::attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_DQ);
     attr = true;
   }
   tc::FaShape sh{static_cast<int>(S), static_cast<int>(d), static_cast<int>(H), scale};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(Z * (S / 128)));
-  cfg.blockDim = dim3(tc::BW_THREADS);
-  cfg.dynamicSmemBytes = tc::SMEM_BWKV;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = static_cast<unsigned>(S / 128);  // the key blocks of one (sample, head)
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc::attn_bwd_kv_kernel, mqkv, mdo, lse2, static_cast<const float*>(dvec),
-                                     static_cast<bf16*>(dqkv), 3 * d, sh);
-  if (e != cudaSuccess) {
-    set_error(std::string("attn_bwd_kv launch: ") + cudaGetErrorString(e));
-    return GPP_ERR_CUDA;
-  }
-  count_launch();
+  const unsigned grid = static_cast<unsigned>(Z * (S / 128));
+  tc::attn_bwd_dkdv_kernel<<<grid, tc::BW_THREADS, tc::SMEM_DKDV, s>>>(mk128, mq64, mdo64, lse2, dvec,
+                                                                      static_cast<bf16*>(dqkv), 3 * d, sh);
+  GPP_LAUNCH_CHECK();
+  tc::attn_bwd_dq_kernel<<<grid, tc::BW_THREADS, tc::SMEM_DQ, s>>>(mq128, mdo128, mk64, lse2, dvec,
+                                                                  static_cast<bf16*>(dqkv), 3 * d, sh);
+  GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
 

@@ -39,10 +39,79 @@ def twin(sg: StageGraph, cluster, graph):
     return simulate(sg, cluster, graph, sync_epilogue=True, op_granular=True, optimizer_bytes_per_param_byte=3.5)
 
 
+def refine_per_stage(sg: StageGraph, cluster, graph, mem_bytes: float | None = None, passes: int = 3,
+                     time_budget_s: float = 45.0) -> tuple[StageGraph, dict]:
+    """Per-stage (b, k) for a fixed partition: the runtime planner's kFkB mode (SPEC.md:320,
+    PAPER.md:747-749).
+
+    The exact per-stage search inside the SP-DP (``PartitionOptions.per_stage_schedules``)
+    enumerates every (b, k) pair at every stage boundary -- 464 s on MMT-4 at 4 GPUs.  Here
+    the partition, devices and edges of the uniform-b plan are kept and each stage's
+    micro-batch b (powers of two within 4x of its current b that divide B and the stage's DP
+    degree) and k (1, 2, 4) are improved by coordinate descent, every candidate rescheduled
+    with the Appendix-A in-flight calculus (``schedule_stage_graph`` with the ks pinned) and
+    scored by the executor's twin.  Returns (stage graph, info)."""
+    import time
+
+    from ..model import Stage
+    from ..sched import schedule_stage_graph
+
+    t0 = time.perf_counter()
+    B = sg.mini_batch
+    mem = mem_bytes if mem_bytes is not None else cluster.mem_per_device
+
+    def build_sg(bs: dict, ks: dict):
+        raw = StageGraph([Stage(st.id, st.op_ids, bs[st.id], st.devices) for st in sg.stages], sg.edges, B)
+        return schedule_stage_graph(raw, mem_limit=mem, g=graph, fixed_k=ks)
+
+    from ..sim import Deadlock
+
+    def score(cand):
+        if cand is None:
+            return None
+        try:
+            return twin(cand, cluster, graph).iteration_ms
+        except Deadlock:  # e.g. a k-block larger than a neighbour's in-flight window
+            return None
+
+    bs = {st.id: st.micro_batch for st in sg.stages}
+    ks = {st.id: (st.sched_cfg.k if st.sched_cfg else 1) for st in sg.stages}
+    best_sg = build_sg(bs, ks)
+    best = score(best_sg)
+    if best is None:
+        return sg, {"refined": False, "reason": "base plan infeasible under the memory cap"}
+    start, evals = best, 1
+    for _ in range(passes):
+        improved = False
+        for st in sg.stages:
+            d = st.dp_degree
+            b0 = bs[st.id]
+            cands_b = [b for b in (b0 // 4, b0 // 2, b0, 2 * b0, 4 * b0)
+                       if b >= d and b % d == 0 and B % b == 0 and b & (b - 1) == 0]
+            for b in cands_b:
+                for k in (1, 2, 4):
+                    if k > B // b or (b == bs[st.id] and k == ks[st.id]):
+                        continue
+                    if time.perf_counter() - t0 > time_budget_s:
+                        break
+                    tb, tk = dict(bs), dict(ks)
+                    tb[st.id], tk[st.id] = b, k
+                    cand = build_sg(tb, tk)
+                    t = score(cand)
+                    evals += 1
+                    if t is not None and t < best - 1e-9:
+                        best, best_sg, bs, ks, improved = t, cand, tb, tk, True
+        if not improved:
+            break
+    return best_sg, {"refined": True, "twin_ms_before": start, "twin_ms_after": best, "evals": evals,
+                     "seconds": round(time.perf_counter() - t0, 2),
+                     "b": {sid: bs[sid] for sid in sorted(bs)}, "k": {sid: ks[sid] for sid in sorted(ks)}}
+
+
 def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions | None = None,
          mem_bytes: float = 180e9, sweep: bool | None = None, min_microbatches: int = 1,
          max_microbatches: int = 32, costs: str = "measured", include_spp: bool | None = None,
-         info: dict | None = None) -> P.Strategy:
+         info: dict | None = None, per_stage: bool = False) -> P.Strategy:
     """Run the GPP (or SPP baseline) partitioner + scheduler for ``n_gpus`` B200s.
 
     The TPS objective (Eq. 1) is a steady-state measure: with launch overheads in the
@@ -60,6 +129,8 @@ def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions 
     SPP candidates join the GPP sweep and the twin picks; ``optimize`` itself is unchanged.
     ``info`` (a dict) receives the twin's iteration time of the pick, which arm produced
     it, and the best pure-``optimize`` (GraphPipe partitioner) candidate on its own.
+    ``per_stage``: then refine each stage's (b, k) on the picked partition
+    (``refine_per_stage``; GPP mode, N > 1).
     """
     from ..sim import simulate
     from ..workloads import with_measured_curves
@@ -106,6 +177,14 @@ def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions 
         if info is not None:
             info.update({"twin_ms": best_t, "picked_by": best_arm,
                          "gpp_partitioner": None if gbest is None else {"strategy": gbest, "twin_ms": gbest_t}})
+    if per_stage and mode == "gpp" and n_gpus > 1:
+        import dataclasses
+
+        refined, rinfo = refine_per_stage(st.stage_graph, cluster, wl.graph, mem_bytes)
+        if info is not None:
+            info["per_stage"] = rinfo
+        if rinfo.get("refined") and rinfo["twin_ms_after"] < rinfo["twin_ms_before"]:
+            st = dataclasses.replace(st, stage_graph=refined)
     rep = validate_strategy(wl.graph, cluster, st.stage_graph)
     if rep:
         raise RuntimeError(f"partitioner produced an invalid strategy: {rep}")
