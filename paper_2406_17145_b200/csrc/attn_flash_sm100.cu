@@ -236,28 +236,23 @@ __global__ void __launch_bounds__(FW_THREADS, 2)
   }
 }
 
-// D[z, s] = sum_c dO[row, head*64 + c] * O[row, head*64 + c]: one thread per (row, head),
-// eight 16-byte loads of each operand in flight.
+// D[z, s] = sum_c dO[row, head*64 + c] * O[row, head*64 + c]: eight lanes per (row, head),
+// one 16-byte vector of each operand per lane (every warp load is 512 contiguous bytes),
+// reduced with three shuffles.
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(float* __restrict__ dvec, const bf16* __restrict__ o,
                                                             int64_t ldo, const bf16* __restrict__ dout, int64_t lddo,
                                                             int64_t T, int S, int H) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
-  if (t >= T * H) return;
-  const int64_t row = t / H;
-  const int head = static_cast<int>(t % H);
-  const uint4* a = reinterpret_cast<const uint4*>(o + row * ldo + head * FA_DH);
-  const uint4* b = reinterpret_cast<const uint4*>(dout + row * lddo + head * FA_DH);
-  uint4 va[8], vb[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    va[i] = __ldg(a + i);
-    vb[i] = __ldg(b + i);
-  }
+  const int64_t pair = t >> 3;  // (row, head)
+  const int part = static_cast<int>(t & 7);
   float acc = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t* ua = reinterpret_cast<const uint32_t*>(&va[i]);
-    const uint32_t* ub = reinterpret_cast<const uint32_t*>(&vb[i]);
+  if (pair < T * H) {
+    const int64_t row = pair / H;
+    const int head = static_cast<int>(pair % H);
+    const uint4 va = __ldg(reinterpret_cast<const uint4*>(o + row * ldo + head * FA_DH) + part);
+    const uint4 vb = __ldg(reinterpret_cast<const uint4*>(dout + row * lddo + head * FA_DH) + part);
+    const uint32_t* ua = reinterpret_cast<const uint32_t*>(&va);
+    const uint32_t* ub = reinterpret_cast<const uint32_t*>(&vb);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ua[k]));
@@ -265,8 +260,14 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(float* __restrict__ 
       acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
     }
   }
-  const int64_t sample = row / S;
-  dvec[(sample * H + head) * S + row % S] = acc;
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  if (pair < T * H && part == 0) {
+    const int64_t row = pair / H;
+    const int head = static_cast<int>(pair % H);
+    dvec[(row / S * H + head) * S + row % S] = acc;
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -317,10 +318,10 @@ constexpr int SMEM_DQ = DQ_BAR + 256 + 1024;
 //   S^T = K Q_j^T, dP^T = V dO_j^T (TMEM, lane = key, 64 query columns each);
 //   P^T = exp2(alpha log2e S^T - lse2[q]), dS^T = alpha P^T o (dP^T - D[q]) -> bf16 pairs in
 //   place (TMEM A operands);  dV += P^T dO_j, dK += dS^T Q_j (accumulated in TMEM).
-__global__ void __launch_bounds__(BW_THREADS, 2)
-    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap m_k128, const __grid_constant__ CUtensorMap m_q64,
-                         const __grid_constant__ CUtensorMap m_do64, const float* __restrict__ lse2,
-                         const float* __restrict__ dvec, bf16* __restrict__ dqkv, int64_t ld_dqkv, FaShape sh) {
+__device__ __forceinline__ void attn_bwd_dkdv(const CUtensorMap& m_k128, const CUtensorMap& m_q64,
+                                              const CUtensorMap& m_do64, const float* __restrict__ lse2,
+                                              const float* __restrict__ dvec, bf16* __restrict__ dqkv,
+                                              int64_t ld_dqkv, const FaShape& sh, int cta) {
   constexpr uint32_t IDESC_ST = idesc_bf16<64, false, false>();
   constexpr uint32_t IDESC_AC = idesc_bf16<FA_DH, false, true>();
   constexpr uint32_t T_ST = 0, T_DPT = 64, T_DV = 128, T_DK = 192;
@@ -338,8 +339,8 @@ __global__ void __launch_bounds__(BW_THREADS, 2)
   const int S = sh.S, d = sh.d, H = sh.H;
   const int nkb = S / 128, nq = S / 64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int z = static_cast<int>(blockIdx.x) / nkb;
-  const int kb = static_cast<int>(blockIdx.x) % nkb;
+  const int z = cta / nkb;
+  const int kb = cta % nkb;
   const int sample = z / H, head = z % H;
   const int row0 = sample * S;
   const float sl2 = sh.alpha * 1.4426950408889634f;
@@ -469,10 +470,10 @@ __global__ void __launch_bounds__(BW_THREADS, 2)
 //   S = Q K_j^T, dP = dO V_j^T (TMEM, lane = query);  dS = alpha P o (dP - D[q]) with
 //   P = exp2(alpha log2e S - lse2[q]) (row constants in registers) -> bf16 pairs in place;
 //   dQ += dS K_j (A operand from TMEM).
-__global__ void __launch_bounds__(BW_THREADS, 2)
-    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap m_q128, const __grid_constant__ CUtensorMap m_do128,
-                       const __grid_constant__ CUtensorMap m_k64, const float* __restrict__ lse2,
-                       const float* __restrict__ dvec, bf16* __restrict__ dqkv, int64_t ld_dqkv, FaShape sh) {
+__device__ __forceinline__ void attn_bwd_dq(const CUtensorMap& m_q128, const CUtensorMap& m_do128,
+                                            const CUtensorMap& m_k64, const float* __restrict__ lse2,
+                                            const float* __restrict__ dvec, bf16* __restrict__ dqkv,
+                                            int64_t ld_dqkv, const FaShape& sh, int cta) {
   constexpr uint32_t IDESC_S = idesc_bf16<64, false, false>();
   constexpr uint32_t IDESC_AC = idesc_bf16<FA_DH, false, true>();
   constexpr uint32_t T_S = 0, T_DP = 64, T_DQ = 128;
@@ -490,8 +491,8 @@ __global__ void __launch_bounds__(BW_THREADS, 2)
   const int S = sh.S, d = sh.d, H = sh.H;
   const int nqb = S / 128, nk = S / 64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int z = static_cast<int>(blockIdx.x) / nqb;
-  const int qb = static_cast<int>(blockIdx.x) % nqb;
+  const int z = cta / nqb;
+  const int qb = cta % nqb;
   const int sample = z / H, head = z % H;
   const int row0 = sample * S;
   const float sl2 = sh.alpha * 1.4426950408889634f;
@@ -597,6 +598,20 @@ __global__ void __launch_bounds__(BW_THREADS, 2)
   }
 }
 
+// One launch for both backward halves: CTAs [0, n) compute dK / dV per key block, CTAs
+// [n, 2n) dQ per query block -- the two kinds share SMs (two CTAs each) and one tail.
+__global__ void __launch_bounds__(BW_THREADS, 2)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap m_qkv128, const __grid_constant__ CUtensorMap m_qkv64,
+                    const __grid_constant__ CUtensorMap m_do64, const __grid_constant__ CUtensorMap m_do128,
+                    const float* __restrict__ lse2, const float* __restrict__ dvec, bf16* __restrict__ dqkv,
+                    int64_t ld_dqkv, FaShape sh, int n) {
+  const int b = static_cast<int>(blockIdx.x);
+  if (b < n)
+    attn_bwd_dkdv(m_qkv128, m_qkv64, m_do64, lse2, dvec, dqkv, ld_dqkv, sh, b);
+  else
+    attn_bwd_dq(m_qkv128, m_do128, m_qkv64, lse2, dvec, dqkv, ld_dqkv, sh, b - n);
+}
+
 }  // namespace tc
 
 namespace {
@@ -649,30 +664,25 @@ int gpp_flash_attn_bwd(const void* qkv, const float* lse2, const void* o, int64_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t T = m * S, Z = m * H;
   GPP_ARG_CHECK(ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(o) & 15) == 0, "16-byte aligned o");
-  tc::attn_bwd_prep_kernel<<<static_cast<unsigned>((T * H + 255) / 256), 256, 0, s>>>(
+  tc::attn_bwd_prep_kernel<<<static_cast<unsigned>((T * H * 8 + 255) / 256), 256, 0, s>>>(
       dvec, static_cast<const bf16*>(o), ldo, static_cast<const bf16*>(dout), lddo, T, static_cast<int>(S),
       static_cast<int>(H));
   GPP_LAUNCH_CHECK();
-  CUtensorMap mk128, mq64, mdo64, mq128, mdo128, mk64;
+  CUtensorMap mk128, mq64, mdo64, mdo128;  // qkv maps serve Q, K and V by coordinates
   if ((rc = tc::make_map_bf16(&mk128, qkv, 3 * d, T, 3 * d, 64, 128))) return rc;
   if ((rc = tc::make_map_bf16(&mq64, qkv, 3 * d, T, 3 * d, 64, 64))) return rc;
   if ((rc = tc::make_map_bf16(&mdo64, dout, d, T, lddo, 64, 64))) return rc;
   if ((rc = tc::make_map_bf16(&mdo128, dout, d, T, lddo, 64, 128))) return rc;
-  mq128 = mk128;  // same qkv map (box 64 x 128), Q block by coordinates
-  mk64 = mq64;
   static bool attr = false;
+  constexpr int SMEM_BW = tc::SMEM_DKDV > tc::SMEM_DQ ? tc::SMEM_DKDV : tc::SMEM_DQ;
   if (!attr) {
-    cudaFuncSetAttribute(tc::attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_DKDV);
-    cudaFuncSetAttribute(tc::attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_DQ);
+    cudaFuncSetAttribute(tc::attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BW);
     attr = true;
   }
   tc::FaShape sh{static_cast<int>(S), static_cast<int>(d), static_cast<int>(H), scale};
-  const unsigned grid = static_cast<unsigned>(Z * (S / 128));
-  tc::attn_bwd_dkdv_kernel<<<grid, tc::BW_THREADS, tc::SMEM_DKDV, s>>>(mk128, mq64, mdo64, lse2, dvec,
-                                                                      static_cast<bf16*>(dqkv), 3 * d, sh);
-  GPP_LAUNCH_CHECK();
-  tc::attn_bwd_dq_kernel<<<grid, tc::BW_THREADS, tc::SMEM_DQ, s>>>(mq128, mdo128, mk64, lse2, dvec,
-                                                                  static_cast<bf16*>(dqkv), 3 * d, sh);
+  const int n = static_cast<int>(Z * (S / 128));
+  tc::attn_bwd_kernel<<<static_cast<unsigned>(2 * n), tc::BW_THREADS, SMEM_BW, s>>>(
+      mk128, mq64, mdo64, mdo128, lse2, dvec, static_cast<bf16*>(dqkv), 3 * d, sh, n);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
