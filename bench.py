@@ -330,15 +330,32 @@ def _attn_flops_per_launch(wl, ex) -> dict:
     return {}
 
 
+def _plan(wl, world, rank, mode, costs):
+    """Rank 0 loads (or plans) the strategy and broadcasts it as a StrategyFile document, so
+    N ranks never plan N times (and all run the identical StageGraph)."""
+    from paper_2406_17145_b200.cli import strategy_from_json, strategy_to_json
+    from paper_2406_17145_b200.runtime.api import plan_cached
+
+    if world == 1:
+        return plan_cached(wl, world, mode, costs=costs)
+    box = [None]
+    if rank == 0:
+        sg, meta = plan_cached(wl, world, mode, costs=costs)
+        box = [(strategy_to_json(sg, wl.graph), meta)]
+    dist.broadcast_object_list(box, src=0)
+    doc, meta = box[0]
+    return strategy_from_json(doc)[0], meta
+
+
 def bench_workload(name, args, rank, world, dev, peaks, peak_src, cpu_ok: bool) -> dict | None:
-    from paper_2406_17145_b200.runtime.api import execute, plan_cached, twin
+    from paper_2406_17145_b200.runtime.api import execute, twin
     from paper_2406_17145_b200.runtime.data import make_batch
     from paper_2406_17145_b200.runtime.trace import trace_diff
     from paper_2406_17145_b200.workloads import b200_cluster, with_measured_curves
 
     wl = _workload(name, world, args.per_gpu_batch, args.branches if name == "mmt" else None)
     cluster = b200_cluster(world)
-    sg, meta = plan_cached(wl, world, args.mode, costs=args.costs)
+    sg, meta = _plan(wl, world, rank, args.mode, args.costs)
     arm = _time_arm(wl, sg, world, rank, dev, args)
     ex, be, ms = arm["ex"], arm["be"], arm["ms"]
     launches, clk, graphed_flag = arm["launches"], arm["clocks"], arm["graphed"] is not None
@@ -399,7 +416,7 @@ def bench_workload(name, args, rank, world, dev, peaks, peak_src, cpu_ok: bool) 
 
         gc.collect()
         torch.cuda.empty_cache()
-        ssg, smeta = plan_cached(wl, world, "spp", costs=args.costs)
+        ssg, smeta = _plan(wl, world, rank, "spp", args.costs)
         sp = _time_arm(wl, ssg, world, rank, dev, args, clocks=False)
         spp_value = wl.mini_batch * args.steps / (sp["ms"] / 1e3)
         sp_sg = [(sorted(s.op_ids), s.micro_batch, s.sched_cfg.k if s.sched_cfg else None) for s in ssg.stages]

@@ -74,7 +74,35 @@ def _acyclic(n, edges):
     return seen == n
 
 
-def exhaustive_optimize(g: ComputationGraph, cluster: DeviceCluster, B: int, max_ops: int = 8) -> BruteResult | None:
+def sp_stage_candidates(g: ComputationGraph, cluster: DeviceCluster, B: int) -> set[frozenset]:
+    """Every op set the SP-DP of ``partition.optimize`` can make a stage of:
+    recorded from the DP's base case (Alg. 1 line "the whole node as one stage") while it
+    explores with an unbounded t_max, virtual junction ops stripped.  Restricting the brute
+    force to these blocks gives the optimum over SP-aligned partitions -- the space the
+    SPEC's DP searches -- against which optimize must match exactly (acceptance 4)."""
+    from paper_2406_17145_b200 import partition as P
+
+    seen: set[frozenset] = set()
+    orig = P._DP._base
+
+    def rec(self, node, c_f, c_b, d):
+        real = frozenset(o for o in node.ops if o not in self.virtual)
+        if real:
+            seen.add(real)
+        return orig(self, node, c_f, c_b, d)
+
+    P._DP._base = rec
+    try:
+        P.optimize(g, cluster, B, P.PartitionOptions(epsilon_mode="spec"))
+    finally:
+        P._DP._base = orig
+    return seen
+
+
+def exhaustive_optimize(g: ComputationGraph, cluster: DeviceCluster, B: int, max_ops: int = 8,
+                        allowed_blocks: set | None = None) -> BruteResult | None:
+    """``allowed_blocks``: only partitions whose every block is in the set (e.g.
+    ``sp_stage_candidates``)."""
     ops = [o.id for o in g.ops]
     if len(ops) > max_ops or cluster.num_devices > 4 or B > 16:
         raise BudgetExceeded(f"{len(ops)} ops / {cluster.num_devices} devices / B={B}")
@@ -82,6 +110,8 @@ def exhaustive_optimize(g: ComputationGraph, cluster: DeviceCluster, B: int, max
     for part in _set_partitions(ops):
         blocks = [frozenset(b) for b in part]
         if len(blocks) > cluster.num_devices:
+            continue
+        if allowed_blocks is not None and any(blk not in allowed_blocks for blk in blocks):
             continue
         if any(non_convex(g, blk) for blk in blocks):
             continue

@@ -108,6 +108,32 @@ def refine_per_stage(sg: StageGraph, cluster, graph, mem_bytes: float | None = N
                      "b": {sid: bs[sid] for sid in sorted(bs)}, "k": {sid: ks[sid] for sid in sorted(ks)}}
 
 
+def _plan_candidate(job):
+    """One sweep candidate: (strategy, twin iteration ms) or None if infeasible."""
+    fname, graph, cluster, B, o = job
+    f = getattr(P, fname)
+    try:
+        cand = f(graph, cluster, B, o)
+    except P.NoFeasibleStrategy:
+        return None
+    return cand, twin(cand.stage_graph, cluster, graph).iteration_ms
+
+
+def _map_candidates(jobs):
+    workers = min(len(jobs), int(os.environ.get("GPP_PLAN_WORKERS", os.cpu_count() or 1)))
+    if workers <= 1 or len(jobs) <= 1:
+        return [_plan_candidate(j) for j in jobs]
+    import multiprocessing as mp
+    import threading
+    from concurrent.futures import ProcessPoolExecutor
+
+    # fork: the candidates are pure Python (no CUDA in the children); serial otherwise
+    if "fork" not in mp.get_all_start_methods() or threading.current_thread() is not threading.main_thread():
+        return [_plan_candidate(j) for j in jobs]
+    with ProcessPoolExecutor(workers, mp_context=mp.get_context("fork")) as pool:
+        return list(pool.map(_plan_candidate, jobs))
+
+
 def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions | None = None,
          mem_bytes: float = 180e9, sweep: bool | None = None, min_microbatches: int = 1,
          max_microbatches: int = 32, costs: str = "measured", include_spp: bool | None = None,
@@ -151,25 +177,29 @@ def plan(wl: Workload, n_gpus: int, mode: str = "gpp", opts: P.PartitionOptions 
         # GPP also tries join-merging stages (PartitionOptions.merge_join); SPP stays the
         # paper's sequential baseline
         merges = (False, True) if mode == "gpp" and P.merge_join_applicable(wl.graph, opts) else (False,)
+        if include_spp is None:
+            include_spp = mode == "gpp"
+        jobs = []
         for b, _ in P.candidate_configs(B):
             if not (min_microbatches <= B // b <= max_microbatches):
                 continue
-            if include_spp is None:
-                include_spp = mode == "gpp"
             arms = [(fn, mj) for mj in merges] + ([(P.spp_optimize, False)] if include_spp and mode == "gpp" else [])
             for f, mj in arms:
                 o = P.PartitionOptions(**{**opts.__dict__, "micro_batches": (b,), "merge_join": mj,
                                           "rich_splits": f is P.optimize})
-                try:
-                    cand = f(wl.graph, cluster, B, o)
-                except P.NoFeasibleStrategy:
-                    continue
-                t = twin(cand.stage_graph, cluster, wl.graph).iteration_ms
-                if best_t is None or t < best_t:
-                    best, best_t = cand, t
-                    best_arm = "spp_optimize" if f is P.spp_optimize else "optimize"
-                if f is not P.spp_optimize and (gbest_t is None or t < gbest_t):
-                    gbest, gbest_t = cand, t
+                jobs.append((f.__name__, wl.graph, cluster, B, o))
+        # the sweep's candidates are independent: one process each (results consumed in the
+        # serial order, so the pick is identical to a serial sweep)
+        results = _map_candidates(jobs)
+        for (fname, *_), res in zip(jobs, results):
+            if res is None:
+                continue
+            cand, t = res
+            if best_t is None or t < best_t:
+                best, best_t = cand, t
+                best_arm = fname
+            if fname != "spp_optimize" and (gbest_t is None or t < gbest_t):
+                gbest, gbest_t = cand, t
         if best is None:
             st = fn(wl.graph, cluster, wl.mini_batch, opts)
         else:

