@@ -161,14 +161,23 @@ def test_live_against_reference_random_sp():
     """Hypothesis-style sweep against the live reference import (build container only)."""
     import random
 
-    sys.path.insert(0, REF)
+    # the repo's own `gpp` drop-in namespace (gpp/*.py aliases) shadows the reference's:
+    # import the reference's modules with only the reference on the path, then restore
+    saved = {k: sys.modules.pop(k) for k in list(sys.modules) if k == "gpp" or k.startswith("gpp.")}
+    old_path = sys.path[:]
+    sys.path[:] = [REF, HERE] + [p for p in old_path if os.path.abspath(p or ".") != os.path.dirname(HERE)
+                                 and p not in ("", ".")]
     try:
         from gpp import model as rm
         from gpp import spgraph as rs
+        assert rm.__file__.startswith(REF), rm.__file__
+        sys.modules.pop("golden.make_golden", None)
+        import golden.make_golden as mg  # binds the reference modules too
     finally:
-        sys.path.remove(REF)
-    sys.path.insert(0, HERE)
-    import golden.make_golden as mg  # noqa: E402
+        sys.path[:] = old_path
+        for k in [k for k in sys.modules if k == "gpp" or k.startswith("gpp.")]:
+            del sys.modules[k]
+        sys.modules.update(saved)
 
     rng = random.Random(7)
     for _ in range(150):
