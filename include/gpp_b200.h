@@ -130,6 +130,14 @@ int gpp_rowdot_bwd(void* dx, int64_t lddx, float* dw, float* dbias, const float*
                    const void* x, int64_t ldx, const float* w, const void* saved,
                    int64_t ldsaved, int act, int64_t M, int64_t K, int accumulate, int dtype,
                    void* stream);
+/* The N=1 head and its loss in ONE kernel: z[m] = dot(x[m,:K], w) + bias[0], then
+ * kind 0 (MSE): loss_acc[0] += scale sum (z-y)^2, dz = 2 scale (z-y);
+ * kind 1 (BCE-with-logits): loss_acc[0] += scale sum l(z,y), dz = scale (sigmoid(z)-y).
+ * Deterministic (fixed-order block partials).  Replaces gpp_rowdot_fwd + gpp_mse_loss /
+ * gpp_bce_loss on the executor's head stages. */
+int gpp_rowdot_loss(float* z, float* dz, float* loss_acc, const void* x, int64_t ldx, const float* w,
+                    const float* bias, const float* y, int64_t M, int64_t K, int kind, float scale, int dtype,
+                    void* stream);
 /* loss_acc[0] += scale * sum (pred-y)^2 ;  dpred = 2*scale*(pred - y). */
 int gpp_mse_loss(float* loss_acc, float* dpred, const float* pred, const float* y, int64_t M,
                  float scale, void* stream);

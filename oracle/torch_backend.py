@@ -81,6 +81,10 @@ class TorchBackend:
         if shadow is not None:
             shadow.copy_(master)
 
+    def rowdot_loss(self, z, dz, loss_acc, x, w, bias, y, kind, scale):
+        self.rowdot_fwd(z, x, w, bias)
+        (self.mse_loss if kind == "mse" else self.bce_loss)(loss_acc, dz, z, y, scale)
+
     def colsum(self, out, x, accumulate):
         s = x.float().sum(0)
         out.add_(s) if accumulate else out.copy_(s)

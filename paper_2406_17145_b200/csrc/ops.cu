@@ -92,6 +92,79 @@ __global__ void rowdot_fwd_kernel(float* out, const T* x, int64_t ldx, const flo
   if (lane == 0) out[row] = s + (bias ? bias[0] : 0.f);
 }
 
+// Fused N=1 head + loss: z[m] = dot(x[m,:K], w) + b, then MSE (kind 0: l = (z-y)^2,
+// dz = 2 scale (z-y)) or BCE-with-logits (kind 1: dz = scale (sigmoid(z) - y)); one warp per
+// row (16-byte bf16 loads when K % 256 == 0), per-block loss partials reduced in block
+// order by the last block to arrive (deterministic; the counter re-arms for graph replay).
+template <typename T>
+__global__ void __launch_bounds__(256) rowdot_loss_kernel(float* __restrict__ z, float* __restrict__ dz,
+                                                          float* __restrict__ loss_acc, float* __restrict__ part,
+                                                          unsigned* __restrict__ counter, const T* __restrict__ x,
+                                                          int64_t ldx, const float* __restrict__ w,
+                                                          const float* __restrict__ bias,
+                                                          const float* __restrict__ y, int64_t M, int64_t K,
+                                                          int kind, float scale) {
+  __shared__ float red[8];
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  float l = 0.f;
+  if (row < M) {
+    const T* xr = x + row * ldx;
+    float s = 0.f;
+    if constexpr (sizeof(T) == 2) {
+      if (K % 256 == 0 && ldx % 8 == 0) {
+        for (int64_t k = lane * 8; k < K; k += 256) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(xr + k));
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float2 f = __bfloat1622float2(h[t]);
+            s = fmaf(f.x, __ldg(w + k + 2 * t), fmaf(f.y, __ldg(w + k + 2 * t + 1), s));
+          }
+        }
+      } else {
+        for (int64_t k = lane; k < K; k += 32) s = fmaf(to_f<T>(xr[k]), w[k], s);
+      }
+    } else {
+      for (int64_t k = lane; k < K; k += 32) s = fmaf(to_f<T>(xr[k]), w[k], s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      const float zi = s + (bias ? bias[0] : 0.f), yi = y[row];
+      z[row] = zi;
+      if (kind == 0) {
+        const float d = zi - yi;
+        l = d * d;
+        dz[row] = 2.f * scale * d;
+      } else {
+        l = fmaxf(zi, 0.f) - zi * yi + log1pf(__expf(-fabsf(zi)));
+        dz[row] = scale * (1.f / (1.f + __expf(-zi)) - yi);
+      }
+    }
+  }
+  if (lane == 0) red[warp] = l;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i];
+    part[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  float t = 0.f;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) t += __ldcg(part + i);
+  t = block_sum(t);
+  if (threadIdx.x == 0) {
+    loss_acc[0] += scale * t;
+    *counter = 0;
+  }
+}
+
 template <typename T>
 __global__ void rowdot_dx_kernel(T* dx, int64_t lddx, const float* dout, const float* w,
                                  const T* saved, int64_t ldsaved, int act, int64_t M, int64_t K) {
@@ -634,6 +707,27 @@ int gpp_rowdot_bwd(void* dx, int64_t lddx, float* dw, float* dbias, const float*
     sum_kernel<<<1, 1024, 0, s>>>(dbias, dout, M, accumulate);
     GPP_LAUNCH_CHECK();
   }
+  return GPP_OK;
+}
+
+int gpp_rowdot_loss(float* z, float* dz, float* loss_acc, const void* x, int64_t ldx, const float* w,
+                    const float* bias, const float* y, int64_t M, int64_t K, int kind, float scale, int dtype,
+                    void* stream) {
+  GPP_ARG_CHECK(z && dz && loss_acc && x && w && y && M > 0 && K > 0, "bad argument");
+  GPP_ARG_CHECK(kind == 0 || kind == 1, "loss kind: 0 = MSE, 1 = BCE-with-logits");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t blocks = (M + 7) / 8;
+  GPP_ARG_CHECK(blocks <= kScratchFloats, "too many rows");
+  float* part = colsum_scratch();  // per-block partials + a re-arming arrival counter
+  if (!part) { set_error("loss scratch allocation failed"); return GPP_ERR_CUDA; }
+  unsigned* counter = reinterpret_cast<unsigned*>(part + kScratchFloats) + (kCounters - 1);
+  if (dtype == GPP_BF16)
+    rowdot_loss_kernel<bf16><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        z, dz, loss_acc, part, counter, static_cast<const bf16*>(x), ldx, w, bias, y, M, K, kind, scale);
+  else
+    rowdot_loss_kernel<float><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        z, dz, loss_acc, part, counter, static_cast<const float*>(x), ldx, w, bias, y, M, K, kind, scale);
+  GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
 

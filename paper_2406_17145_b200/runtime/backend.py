@@ -43,6 +43,9 @@ class CudaBackend:
         lib.linear_wgrad_sgd(master, shadow, grad, dy, x, lr, accumulate=accumulate, store_grad=store_grad,
                              dbias=dbias)
 
+    def rowdot_loss(self, z, dz, loss_acc, x, w, bias, y, kind, scale):
+        lib.rowdot_loss(z, dz, loss_acc, x, w, bias, y, kind, scale)
+
     def colsum(self, out, x, accumulate):
         lib.colsum(out, x, accumulate=accumulate)
 

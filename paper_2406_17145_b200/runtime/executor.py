@@ -510,10 +510,10 @@ class Executor:
                 be.copy_rows_multi(pdst, psrc)
             elif spec.kind in ("mse_head", "bce_head"):
                 x = self._input(o, j, slot, batch)
-                be.rowdot_fwd(self.pred[o][slot], x, self.P[(o, "w")], self.P[(o, "b")])
                 y = batch[spec.label_key][j * self.m:(j + 1) * self.m]
-                loss = be.mse_loss if spec.kind == "mse_head" else be.bce_loss
-                loss(self.loss_acc, self.dpred[o][slot], self.pred[o][slot], y, scale)
+                # head GEMV + loss + dLoss in one kernel
+                be.rowdot_loss(self.pred[o][slot], self.dpred[o][slot], self.loss_acc, x, self.P[(o, "w")],
+                               self.P[(o, "b")], y, "mse" if spec.kind == "mse_head" else "bce", scale)
             elif spec.kind == "mmt_layer":
                 x = self._input(o, j, slot, batch)
                 lay = self.mmt[o]

@@ -36,6 +36,7 @@ _SIGS = {
     "gpp_gemm": ([_vp, _i64, _vp, _i64, _i32, _vp, _i64, _i32, _i64, _i64, _i64, _f32, _f32, _i32, _i32, _vp], _i32),
     "gpp_rowdot_fwd": ([_vp, _vp, _i64, _vp, _vp, _i64, _i64, _i32, _vp], _i32),
     "gpp_rowdot_bwd": ([_vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _i64, _i64, _i32, _i32, _vp], _i32),
+    "gpp_rowdot_loss": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _i32, _f32, _i32, _vp], _i32),
     "gpp_mse_loss": ([_vp, _vp, _vp, _vp, _i64, _f32, _vp], _i32),
     "gpp_bce_loss": ([_vp, _vp, _vp, _vp, _i64, _f32, _vp], _i32),
     "gpp_ce_loss": ([_vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _f32, _i32, _vp], _i32),
@@ -222,6 +223,13 @@ def ce_loss(loss_acc, dlogits, logits, labels, scale: float, stream=None):
     M, C = logits.shape
     call("gpp_ce_loss", _ptr(loss_acc), _ptr(dlogits), _ld(dlogits), _ptr(logits), _ld(logits),
          _ptr(labels), M, C, float(scale), _dt(logits), _stream(stream))
+
+
+def rowdot_loss(z, dz, loss_acc, x, w, bias, y, kind: str, scale: float, stream=None):
+    """Fused N=1 head + loss (kind "mse" | "bce"): z = x.w + b, the loss into loss_acc, dz."""
+    M, K = x.shape
+    call("gpp_rowdot_loss", _ptr(z), _ptr(dz), _ptr(loss_acc), _ptr(x), _ld(x), _ptr(w), _ptr(bias), _ptr(y), M, K,
+         {"mse": 0, "bce": 1}[kind], float(scale), _dt(x), _stream(stream))
 
 
 def colsum(out, x, accumulate=False, stream=None):

@@ -628,3 +628,30 @@ def test_flash_attention_fwd_bwd(cuda_lib, m, S, H):
     cuda_lib.flash_attn_bwd(qkv, lse2, o, dout, dvec, again, m, S, d, H, scale)
     torch.cuda.synchronize()
     assert torch.equal(again, dqkv)
+
+
+@pytest.mark.parametrize("kind", ["mse", "bce"])
+@pytest.mark.parametrize("K,dt", [(1024, torch.bfloat16), (4096, torch.bfloat16), (300, torch.float32)])
+def test_rowdot_loss_fused(cuda_lib, kind, K, dt):
+    """Head GEMV + loss + dLoss in one kernel vs torch; deterministic across runs."""
+    g = torch.Generator(device="cuda").manual_seed(K)
+    M = 5000
+    x = torch.randn(M, K, device="cuda", generator=g).to(dt)
+    w = torch.randn(K, device="cuda", generator=g) / K ** 0.5
+    b = torch.randn(1, device="cuda", generator=g)
+    y = (torch.rand(M, device="cuda", generator=g) > 0.5).float() if kind == "bce" else torch.randn(M, device="cuda", generator=g)
+    z, dz, acc = torch.empty(M, device="cuda"), torch.empty(M, device="cuda"), torch.zeros(1, device="cuda")
+    scale = 1.0 / M
+    cuda_lib.rowdot_loss(z, dz, acc, x, w, b, y, kind, scale)
+    torch.cuda.synchronize()
+    zr = (x.float() @ w + b).requires_grad_(True)
+    lr = ((zr - y) ** 2).sum() * scale if kind == "mse" else \
+        torch.nn.functional.binary_cross_entropy_with_logits(zr, y, reduction="sum") * scale
+    lr.backward()
+    assert torch.allclose(z, zr.detach(), rtol=1e-4, atol=1e-4)
+    assert torch.allclose(dz, zr.grad, rtol=1e-4, atol=1e-7)
+    assert abs(acc.item() - lr.item()) <= 1e-4 * abs(lr.item())
+    acc2 = torch.zeros(1, device="cuda")
+    cuda_lib.rowdot_loss(z, dz, acc2, x, w, b, y, kind, scale)
+    torch.cuda.synchronize()
+    assert torch.equal(acc, acc2)
