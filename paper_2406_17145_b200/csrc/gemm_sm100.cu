@@ -1159,14 +1159,9 @@ static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
     // CTA-pair 256 x BN tiles; BN=128 when 256-wide tiles leave most pairs idle.
     const int64_t pairs256 = ((M + 255) / 256) * ((N + 255) / 256);
     bn = (N > 128 && pairs256 >= 48) ? 256 : 128;
-    // GPP_SGD_BN=128: 256 x 128 tiles for the fused wgrad + SGD (wave-quantisation experiment)
-    static const int sgd_bn = [] { const char* e = std::getenv("GPP_SGD_BN"); return e ? std::atoi(e) : 0; }();
-    if (EPI == EPI_SGD && sgd_bn == 128) bn = 128;
     // small output, long K: split-K fills the GPU anyway, and 256-wide tiles cut the
     // L2 -> SM operand traffic per FLOP by a third (the CANDLE tail: 1024 x 1024 x 28672)
-    if (bn == 128 && N > 128 && pairs256 * std::min<int64_t>(max_splits_env(), num_kb / 2) >= 48 &&
-        !(EPI == EPI_SGD && sgd_bn == 128))
-      bn = 256;
+    if (bn == 128 && N > 128 && pairs256 * std::min<int64_t>(max_splits_env(), num_kb / 2) >= 48) bn = 256;
     tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
     slots = num_sms() / 2;
   } else {
