@@ -316,6 +316,19 @@ def _time_arm(wl, sg, world, rank, dev, args, clocks=True):
             "be": be}
 
 
+def _dlrm_bf16_roof(wl, peaks, world, t_iter) -> dict:
+    """DLRM's tables are fp32 here (exact sparse SGD); SURVEY section
+    8(d) config 4 names bf16 tables.  The same roofline with the bf16 config's table bytes
+    (gather 2 B, read-modify-write 2 x 2 B per element) -- the stricter denominator."""
+    spec = next(s for s in wl.layers.values() if s.kind == "embbag")
+    tables = sum(1 for s in wl.layers.values() if s.kind == "embbag")
+    bag, emb = spec.extra[0], spec.out_dim
+    byts = tables * (3 * bag * emb * 2 + 2 * bag * 8 + 2 * emb * 2)
+    t = wl.mini_batch * (wl.flops_per_sample / (peaks["bf16_tflops_sustained"] * 1e12)
+                         + byts / (peaks["hbm_gbs"] * 1e9)) / world * 1e3
+    return {"bf16_table_config": {"bytes_per_sample": byts, "t_roof_ms": round(t, 4), "frac": round(t / t_iter, 4)}}
+
+
 def _attn_flops_per_launch(wl, ex) -> dict:
     """Algorithmic FLOPs of one attention launch on this rank (all heads of a micro-batch):
     fw = 2 GEMMs (QK^T, PV) = 4 S^2 dh per head; bw = 5 GEMM-equivalents with the
@@ -483,6 +496,7 @@ def bench_workload(name, args, rank, world, dev, peaks, peak_src, cpu_ok: bool) 
         "clocks": clk,
         "step_roofline": {"t_roof_ms": round(t_roof, 4), "frac": round(t_roof / t_iter, 4),
                           "flops_per_sample": wl.flops_per_sample, "bytes_per_sample": wl.bytes_per_sample,
+                          **(_dlrm_bf16_roof(wl, peaks, world, t_iter) if name == "dlrm" else {}),
                           "note": "summed stage-compute roofline: B*(F/P_sustained + bytes/BW_hbm)/N vs measured step"},
         "bubble": {"measured": round(bubble, 4), "model": round(sim.bubble_fraction, 4),
                    "note": "1 - sum over ranks of kernel busy time / (N * step time); kernel time from CUDA-event "
