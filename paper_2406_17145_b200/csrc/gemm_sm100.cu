@@ -101,14 +101,55 @@ __device__ __forceinline__ bool al16(const void* p) {
   return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
 }
 
+// Warp-collective bf16 store of a 32 x 32 chunk (lane = row) through a 2 KB smem tile in the
+// 64B-swizzled layout of the aux tiles: each lane writes its row's 64 B, then every store
+// instruction moves 8 rows x 64 contiguous bytes (4 lanes per row) instead of 32 rows x
+// 16 B -- a quarter of the L1/L2 store transactions.  Rows >= rows_valid are not stored.
+__device__ __forceinline__ void store_bf16x32_staged(bf16* base, int64_t ld, const float (&f)[32], uint8_t* stage,
+                                                     int lane, int rows_valid) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint4 pk;
+    const int j = 8 * u;
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(f[j + 0], f[j + 1]);
+    __nv_bfloat162 h1 = __floats2bfloat162_rn(f[j + 2], f[j + 3]);
+    __nv_bfloat162 h2 = __floats2bfloat162_rn(f[j + 4], f[j + 5]);
+    __nv_bfloat162 h3 = __floats2bfloat162_rn(f[j + 6], f[j + 7]);
+    pk.x = *reinterpret_cast<uint32_t*>(&h0);
+    pk.y = *reinterpret_cast<uint32_t*>(&h1);
+    pk.z = *reinterpret_cast<uint32_t*>(&h2);
+    pk.w = *reinterpret_cast<uint32_t*>(&h3);
+    *reinterpret_cast<uint4*>(stage + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = pk;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = (lane >> 2) + 8 * i, u = lane & 3;
+    const uint4 v = *reinterpret_cast<const uint4*>(stage + r * 64 + ((u ^ ((r >> 1) & 3)) << 4));
+    if (r < rows_valid) *reinterpret_cast<uint4*>(base + static_cast<int64_t>(r) * ld + u * 8) = v;
+  }
+  __syncwarp();
+}
+
 // Epilogue of one thread: 32 consecutive columns [col0, col0+32) of one row.
 // `aux` (residual / act'-saved, 32 values) is loaded by the caller BEFORE the TMEM
 // load so its global latency overlaps tcgen05.ld.
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const uint32_t (&v)[32],
                                                const float (&aux)[32], int row, int col0, int M,
-                                               int N) {
-  if (row >= M || col0 >= N) return;
+                                               int N, uint8_t* stage = nullptr, int lane = 0) {
+  // staged (warp-collective, coalesced) bf16 stores: whole 32-column chunks of a FWD / DGRAD
+  // epilogue with 16-byte-aligned rows; every lane of the warp takes part
+  const int row0 = row - lane;
+  bool staged = false;
+  if constexpr (EPI == EPI_FWD || EPI == EPI_DGRAD) {
+    staged = stage != nullptr && col0 + 32 <= N && row0 < M && ep.ldo % 8 == 0 &&
+             al16(static_cast<bf16*>(ep.out) + static_cast<int64_t>(row0) * ep.ldo + col0) &&
+             (ep.pre == nullptr || (ep.ldpre % 8 == 0 &&
+                                    al16(static_cast<bf16*>(ep.pre) + static_cast<int64_t>(row0) * ep.ldpre + col0)));
+  }
+  if (!staged && (row >= M || col0 >= N)) return;
+  const int rows_valid = M - row0 < 32 ? M - row0 : 32;
   const int n_valid = N - col0 < 32 ? N - col0 : 32;
   const bool full = n_valid == 32;
   float f[32];
@@ -187,8 +228,13 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const uint32
         }
       }
       if (ep.pre != nullptr) {
-        bf16* pre = static_cast<bf16*>(ep.pre) + static_cast<int64_t>(row) * ep.ldpre + col0;
-        store_bf16x32(pre, full && al16(pre), n_valid, f);
+        if (staged) {
+          store_bf16x32_staged(static_cast<bf16*>(ep.pre) + static_cast<int64_t>(row0) * ep.ldpre + col0, ep.ldpre, f,
+                               stage, lane, rows_valid);
+        } else {
+          bf16* pre = static_cast<bf16*>(ep.pre) + static_cast<int64_t>(row) * ep.ldpre + col0;
+          store_bf16x32(pre, full && al16(pre), n_valid, f);
+        }
       }
 #pragma unroll
       for (int j = 0; j < 32; ++j) f[j] = act_fwd(f[j], ep.act);
@@ -211,7 +257,12 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const uint32
         for (int j = 0; j < 32; ++j) f[j] += ep.beta * c[j];
       }
     }
-    store_bf16x32(out, full && al16(out), n_valid, f);
+    if (staged) {
+      store_bf16x32_staged(static_cast<bf16*>(ep.out) + static_cast<int64_t>(row0) * ep.ldo + col0, ep.ldo, f, stage,
+                           lane, rows_valid);
+    } else {
+      store_bf16x32(out, full && al16(out), n_valid, f);
+    }
   }
 }
 
@@ -826,18 +877,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS + 32, 1
                                       n_blk * BN + c * 32, M, N, lane);
         } else {
           float aux[32];
+          uint8_t* stage = nullptr;  // the chunk's store staging tile (2 KB of this warp's aux pair)
           if (AUX_TMA_EPI(EPI) && aux_tma) {
             const uint32_t b = aux_it & 1, ph = (aux_it >> 1) & 1;
             ++aux_it;
             if (c + GSTEP < BN / 32) issue_aux(c + GSTEP);  // into the other buffer (consumed)
             mbar_wait(&my_bar[b], ph);
             read_aux_tile(my_aux + b * 2048, lane, aux);
-            __syncwarp();  // every lane done with buffer b before it is refilled
+            __syncwarp();  // every lane done with buffer b before it is reused / refilled
+            stage = my_aux + b * 2048;  // free until the next chunk's TMA refills it
           } else {
             epilogue_aux<EPI>(epu, row, n_blk * BN + c * 32, M, N, aux);
+            if (AUX_TMA_EPI(EPI)) stage = my_aux;  // aux tiles unused by this launch
           }
           tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
-          epilogue_chunk<EPI>(epu, v, aux, row, n_blk * BN + c * 32, M, N);
+          epilogue_chunk<EPI>(epu, v, aux, row, n_blk * BN + c * 32, M, N, stage, lane);
+          if (stage != nullptr) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
       }
       tc_fence_before();
