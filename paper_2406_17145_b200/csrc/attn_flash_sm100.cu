@@ -271,21 +271,39 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(float* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------------------
-// Backward: two kernels, no cross-CTA reduction, 256 TMEM columns each (two CTAs per SM, so
-// one CTA's softmax phase overlaps the other's loads and MMAs).  Blocks of 64 on the loop
-// dimension.  Warps: 0 TMA, 1 MMA (+ TMEM alloc), 2..9 two per TMEM lane quarter (one row
-// each), splitting the 64 columns of a block into two 32-column chunks.
+// Backward: dK/dV per (z, 128-key block) and dQ per (z, 128-query block), both in one launch,
+// no cross-CTA reduction.  The loop dimension runs in blocks of BB = 32 with DOUBLE-BUFFERED
+// S / dP TMEM tiles: the MMA warp issues block j+1's S and dP while the softmax warps turn
+// block j's into P / dS, then block j's dV / dK (or dQ) MMAs -- the tensor pipe and the
+// softmax overlap inside a CTA.  256 TMEM columns (S[2], dP[2] 32 each, two 64-column
+// accumulators), so two CTAs still share an SM.  Warps: 0 TMA, 1 MMA (+ TMEM alloc), 2..9
+// two per TMEM lane quarter (one row each), splitting a block's 32 columns in halves of 16.
 namespace {
+constexpr int BB = 32;          // loop block (queries for dK/dV, keys for dQ)
 constexpr int BW_SMW = 8;
 constexpr int BW_THREADS = 64 + 32 * BW_SMW;
-constexpr int BW_STAGES = 3;
-constexpr uint32_t TILE64 = 64 * 128;    // 64 rows x 64 bf16 (128B-swizzled): 8 KB
+constexpr int BW_STAGES = 6;
+constexpr uint32_t TILEB = BB * 128;     // 32 rows x 64 bf16 (128B-swizzled): 4 KB
 constexpr uint32_t TILE128 = 128 * 128;  // 16 KB
 
 __device__ __forceinline__ void fa_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
                "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fa_tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void fa_tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                : "memory");
 }
 
@@ -302,42 +320,64 @@ __device__ __forceinline__ void fa_store_row32(bf16* dst, const uint32_t (&v)[32
   }
 }
 
-// dK / dV smem: K, V (128 keys) | stages of [Q 64 rows | dO 64 rows | lse2[64] | D[64]]
-constexpr uint32_t KV_STAGE = 2 * TILE64 + 512;
-constexpr uint32_t KV_STAGE_STRIDE = (KV_STAGE + 1023) / 1024 * 1024;
+// dK / dV smem: K, V (128 keys) | stages of [Q 32 rows | dO 32 rows | lse2[32] | D[32]]
+constexpr uint32_t KV_STAGE_STRIDE = 9 * 1024;  // 2 x 4 KB tiles + 256 B vectors, 1 KB aligned
 constexpr uint32_t KV_RING = 2 * TILE128;
 constexpr uint32_t KV_BAR = KV_RING + BW_STAGES * KV_STAGE_STRIDE;
 constexpr int SMEM_DKDV = KV_BAR + 256 + 1024;
-// dQ smem: Q, dO (128 queries) | stages of [K 64 rows | V 64 rows]
+// dQ smem: Q, dO (128 queries) | stages of [K 32 rows | V 32 rows]
 constexpr uint32_t DQ_RING = 2 * TILE128;
-constexpr uint32_t DQ_BAR = DQ_RING + BW_STAGES * 2 * TILE64;
+constexpr uint32_t DQ_BAR = DQ_RING + BW_STAGES * 2 * TILEB;
 constexpr int SMEM_DQ = DQ_BAR + 256 + 1024;
+// TMEM columns (both kernels): S[b] at 32b, dP[b] at 64 + 32b, accumulators at 128 / 192
+constexpr uint32_t T_S = 0, T_P = 64, T_A0 = 128, T_A1 = 192;
+
+// barrier block of both kernels
+struct BwBars {
+  uint64_t* first;                // K/V (dK/dV) or Q/dO (dQ) landed
+  uint64_t* full;                 // [BW_STAGES]
+  uint64_t* free_;                // [BW_STAGES]
+  uint64_t* s;                    // [2] S, dP of the buffer in TMEM
+  uint64_t* p;                    // [2] bf16 P / dS of the buffer in TMEM (8 warps)
+  uint64_t* done;                 // every MMA done
+  uint32_t* tmem_slot;
+};
+__device__ __forceinline__ BwBars bw_bars(uint8_t* base) {
+  uint64_t* b = reinterpret_cast<uint64_t*>(base);
+  return {b, b + 1, b + 1 + BW_STAGES, b + 1 + 2 * BW_STAGES, b + 3 + 2 * BW_STAGES, b + 5 + 2 * BW_STAGES,
+          reinterpret_cast<uint32_t*>(b + 6 + 2 * BW_STAGES)};
+}
+__device__ __forceinline__ void bw_init(const BwBars& br) {
+  mbar_init(br.first, 1);
+  for (int i = 0; i < BW_STAGES; ++i) {
+    mbar_init(&br.full[i], 1);
+    mbar_init(&br.free_[i], 1);
+  }
+  for (int i = 0; i < 2; ++i) {
+    mbar_init(&br.s[i], 1);
+    mbar_init(&br.p[i], BW_SMW);
+  }
+  mbar_init(br.done, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
 }  // namespace
 
-// dK, dV of one (z, 128-key block), looping over the S/64 query blocks:
-//   S^T = K Q_j^T, dP^T = V dO_j^T (TMEM, lane = key, 64 query columns each);
+// dK, dV of one (z, 128-key block), looping over the S/32 query blocks:
+//   S^T = K Q_j^T, dP^T = V dO_j^T (TMEM, lane = key, 32 query columns each);
 //   P^T = exp2(alpha log2e S^T - lse2[q]), dS^T = alpha P^T o (dP^T - D[q]) -> bf16 pairs in
 //   place (TMEM A operands);  dV += P^T dO_j, dK += dS^T Q_j (accumulated in TMEM).
-__device__ __forceinline__ void attn_bwd_dkdv(const CUtensorMap& m_k128, const CUtensorMap& m_q64,
-                                              const CUtensorMap& m_do64, const float* __restrict__ lse2,
+__device__ __forceinline__ void attn_bwd_dkdv(const CUtensorMap& m_k128, const CUtensorMap& m_qb,
+                                              const CUtensorMap& m_dob, const float* __restrict__ lse2,
                                               const float* __restrict__ dvec, bf16* __restrict__ dqkv,
                                               int64_t ld_dqkv, const FaShape& sh, int cta) {
-  constexpr uint32_t IDESC_ST = idesc_bf16<64, false, false>();
+  constexpr uint32_t IDESC_ST = idesc_bf16<BB, false, false>();
   constexpr uint32_t IDESC_AC = idesc_bf16<FA_DH, false, true>();
-  constexpr uint32_t T_ST = 0, T_DPT = 64, T_DV = 128, T_DK = 192;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + KV_BAR);
-  uint64_t* bar_kv = bar + 0;
-  uint64_t* bar_full = bar + 1;                 // [BW_STAGES]
-  uint64_t* bar_free = bar + 1 + BW_STAGES;     // [BW_STAGES]
-  uint64_t* bar_s = bar + 1 + 2 * BW_STAGES;    // S^T, dP^T in TMEM
-  uint64_t* bar_p = bar + 2 + 2 * BW_STAGES;    // P^T, dS^T (bf16) in TMEM (8 warps)
-  uint64_t* bar_done = bar + 3 + 2 * BW_STAGES; // every MMA done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4 + 2 * BW_STAGES);
+  const BwBars br = bw_bars(smem + KV_BAR);
 
   const int S = sh.S, d = sh.d, H = sh.H;
-  const int nkb = S / 128, nq = S / 64;
+  const int nkb = S / 128, nq = S / BB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int z = cta / nkb;
   const int kb = cta % nkb;
@@ -345,111 +385,110 @@ __device__ __forceinline__ void attn_bwd_dkdv(const CUtensorMap& m_k128, const C
   const int row0 = sample * S;
   const float sl2 = sh.alpha * 1.4426950408889634f;
 
-  if (warp == 0 && lane == 0) {
-    mbar_init(bar_kv, 1);
-    for (int i = 0; i < BW_STAGES; ++i) {
-      mbar_init(&bar_full[i], 1);
-      mbar_init(&bar_free[i], 1);
-    }
-    mbar_init(bar_s, 1);
-    mbar_init(bar_p, BW_SMW);
-    mbar_init(bar_done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  if (warp == 0 && lane == 0) bw_init(br);
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(br.tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *br.tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(bar_kv, 2 * TILE128);
-      tma_load_2d(smem, &m_k128, bar_kv, d + head * FA_DH, row0 + kb * 128);
-      tma_load_2d(smem + TILE128, &m_k128, bar_kv, 2 * d + head * FA_DH, row0 + kb * 128);
+      mbar_expect_tx(br.first, 2 * TILE128);
+      tma_load_2d(smem, &m_k128, br.first, d + head * FA_DH, row0 + kb * 128);
+      tma_load_2d(smem + TILE128, &m_k128, br.first, 2 * d + head * FA_DH, row0 + kb * 128);
       const float* lz = lse2 + static_cast<int64_t>(z) * S;
       const float* dz = dvec + static_cast<int64_t>(z) * S;
       for (int j = 0; j < nq; ++j) {
         const int st = j % BW_STAGES;
-        mbar_wait(&bar_free[st], ((j / BW_STAGES) & 1) ^ 1);
+        mbar_wait(&br.free_[st], ((j / BW_STAGES) & 1) ^ 1);
         uint8_t* sb = smem + KV_RING + st * KV_STAGE_STRIDE;
-        mbar_expect_tx(&bar_full[st], 2 * TILE64 + 512);
-        tma_load_2d(sb, &m_q64, &bar_full[st], head * FA_DH, row0 + j * 64);
-        tma_load_2d(sb + TILE64, &m_do64, &bar_full[st], head * FA_DH, row0 + j * 64);
-        fa_bulk_load(sb + 2 * TILE64, lz + j * 64, 256, &bar_full[st]);
-        fa_bulk_load(sb + 2 * TILE64 + 256, dz + j * 64, 256, &bar_full[st]);
+        mbar_expect_tx(&br.full[st], 2 * TILEB + 2 * BB * 4);
+        tma_load_2d(sb, &m_qb, &br.full[st], head * FA_DH, row0 + j * BB);
+        tma_load_2d(sb + TILEB, &m_dob, &br.full[st], head * FA_DH, row0 + j * BB);
+        fa_bulk_load(sb + 2 * TILEB, lz + j * BB, BB * 4, &br.full[st]);
+        fa_bulk_load(sb + 2 * TILEB + 128, dz + j * BB, BB * 4, &br.full[st]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t ka = smem_u32(smem), va = smem_u32(smem + TILE128);
-      mbar_wait(bar_kv, 0);
-      for (int j = 0; j < nq; ++j) {
-        const int st = j % BW_STAGES;
-        const uint32_t qa = smem_u32(smem + KV_RING + st * KV_STAGE_STRIDE), da = qa + TILE64;
-        mbar_wait(&bar_full[st], (j / BW_STAGES) & 1);
+      auto issue_sp = [&](int j) {  // S^T, dP^T of query block j into buffer j & 1
+        const int st = j % BW_STAGES, b = j & 1;
+        const uint32_t qa = smem_u32(smem + KV_RING + st * KV_STAGE_STRIDE), da = qa + TILEB;
+        mbar_wait(&br.full[st], (j / BW_STAGES) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < FA_DH / 16; ++k) {
-          umma_bf16(tmem + T_ST, sdesc_sw128(ka + k * 32, 16, 1024), sdesc_sw128(qa + k * 32, 16, 1024), IDESC_ST, k != 0);
-          umma_bf16(tmem + T_DPT, sdesc_sw128(va + k * 32, 16, 1024), sdesc_sw128(da + k * 32, 16, 1024), IDESC_ST, k != 0);
+          umma_bf16(tmem + T_S + b * BB, sdesc_sw128(ka + k * 32, 16, 1024), sdesc_sw128(qa + k * 32, 16, 1024), IDESC_ST,
+                    k != 0);
+          umma_bf16(tmem + T_P + b * BB, sdesc_sw128(va + k * 32, 16, 1024), sdesc_sw128(da + k * 32, 16, 1024), IDESC_ST,
+                    k != 0);
         }
-        umma_commit(bar_s);
-        mbar_wait(bar_p, j & 1);
+        umma_commit(&br.s[b]);
+      };
+      mbar_wait(br.first, 0);
+      issue_sp(0);
+      for (int j = 0; j < nq; ++j) {
+        const int st = j % BW_STAGES, b = j & 1;
+        if (j + 1 < nq) issue_sp(j + 1);  // overlaps block j's softmax
+        mbar_wait(&br.p[b], (j >> 1) & 1);
         tc_fence_after();
+        const uint32_t qa = smem_u32(smem + KV_RING + st * KV_STAGE_STRIDE), da = qa + TILEB;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // K = 64 queries, 16 per MMA (8 packed columns)
+        for (int k = 0; k < BB / 16; ++k) {  // K = 32 queries, 16 per MMA (8 packed columns)
           const uint32_t acc = (j | k) != 0;
-          fa_umma_ts(tmem + T_DV, tmem + T_ST + k * 8, sdesc_sw128(da + k * 2048, 8192, 1024), IDESC_AC, acc);
-          fa_umma_ts(tmem + T_DK, tmem + T_DPT + k * 8, sdesc_sw128(qa + k * 2048, 8192, 1024), IDESC_AC, acc);
+          fa_umma_ts(tmem + T_A0, tmem + T_S + b * BB + k * 8, sdesc_sw128(da + k * 2048, 8192, 1024), IDESC_AC, acc);
+          fa_umma_ts(tmem + T_A1, tmem + T_P + b * BB + k * 8, sdesc_sw128(qa + k * 2048, 8192, 1024), IDESC_AC, acc);
         }
-        umma_commit(&bar_free[st]);
+        umma_commit(&br.free_[st]);
       }
-      umma_commit(bar_done);
+      umma_commit(br.done);
     }
   } else {
-    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 32-query chunk
+    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 16-query half of a block
     const int lr = q * 32 + lane;  // key row
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
     for (int j = 0; j < nq; ++j) {
-      const int st = j % BW_STAGES;
-      const float* vec = reinterpret_cast<const float*>(smem + KV_RING + st * KV_STAGE_STRIDE + 2 * TILE64);
-      mbar_wait(&bar_full[st], (j / BW_STAGES) & 1);  // lse2 / D of the stage (TMA-written)
-      mbar_wait(bar_s, j & 1);
+      const int st = j % BW_STAGES, b = j & 1;
+      const float* vec = reinterpret_cast<const float*>(smem + KV_RING + st * KV_STAGE_STRIDE + 2 * TILEB);
+      mbar_wait(&br.full[st], (j / BW_STAGES) & 1);  // lse2 / D of the stage (TMA-written)
+      mbar_wait(&br.s[b], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t sv[32], pv[32];
-      tmem_ld32(trow + T_ST + c * 32, sv);
-      tmem_ld32(trow + T_DPT + c * 32, pv);
-      uint32_t pk[16], dk[16];
+      uint32_t sv[16], pv[16];
+      fa_tmem_ld16(trow + T_S + b * BB + c * 16, sv);
+      fa_tmem_ld16(trow + T_P + b * BB + c * 16, pv);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      uint32_t pk[8], dk[8];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float2 ls = *reinterpret_cast<const float2*>(vec + c * 32 + 2 * i);
-        const float2 dd = *reinterpret_cast<const float2*>(vec + 64 + c * 32 + 2 * i);
+      for (int i = 0; i < 8; ++i) {
+        const float2 ls = *reinterpret_cast<const float2*>(vec + c * 16 + 2 * i);
+        const float2 dd = *reinterpret_cast<const float2*>(vec + 32 + c * 16 + 2 * i);
         const float p0 = exp2f(fmaf(__uint_as_float(sv[2 * i]), sl2, -ls.x));
         const float p1 = exp2f(fmaf(__uint_as_float(sv[2 * i + 1]), sl2, -ls.y));
         pk[i] = fa_pack(p0, p1);
         dk[i] = fa_pack(sh.alpha * p0 * (__uint_as_float(pv[2 * i]) - dd.x),
                         sh.alpha * p1 * (__uint_as_float(pv[2 * i + 1]) - dd.y));
       }
-      // bf16 pairs: queries 32c + 2i, +1 -> column 16c + i.  Chunk 1's pairs land in chunk 0's
-      // columns, so both warps of the quarter must have read theirs first.
+      // bf16 pairs: queries 16c + 2i, +1 -> column 8c + i of the buffer.  Half 1's pairs land in
+      // half 0's columns, so both warps of the quarter must have read theirs first.
       asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-      fa_tmem_st16(trow + T_ST + c * 16, pk);
-      fa_tmem_st16(trow + T_DPT + c * 16, dk);
+      fa_tmem_st8(trow + T_S + b * BB + c * 8, pk);
+      fa_tmem_st8(trow + T_P + b * BB + c * 8, dk);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) fa_mbar_arrive(bar_p);
+      if (lane == 0) fa_mbar_arrive(&br.p[b]);
     }
-    mbar_wait(bar_done, 0);
+    mbar_wait(br.done, 0);
     tc_fence_after();
     const int64_t krow = static_cast<int64_t>(row0) + kb * 128 + lr;
-    // chunk-0 warps write dV, chunk-1 warps dK
-    const uint32_t src = trow + (c == 0 ? T_DV : T_DK);
+    // half-0 warps write dV, half-1 warps dK
+    const uint32_t src = trow + (c == 0 ? T_A0 : T_A1);
     bf16* dst = dqkv + krow * ld_dqkv + (c == 0 ? 2 * d : d) + head * FA_DH;
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
@@ -466,30 +505,22 @@ __device__ __forceinline__ void attn_bwd_dkdv(const CUtensorMap& m_k128, const C
   }
 }
 
-// dQ of one (z, 128-query block), looping over the S/64 key blocks:
+// dQ of one (z, 128-query block), looping over the S/32 key blocks:
 //   S = Q K_j^T, dP = dO V_j^T (TMEM, lane = query);  dS = alpha P o (dP - D[q]) with
 //   P = exp2(alpha log2e S - lse2[q]) (row constants in registers) -> bf16 pairs in place;
 //   dQ += dS K_j (A operand from TMEM).
 __device__ __forceinline__ void attn_bwd_dq(const CUtensorMap& m_q128, const CUtensorMap& m_do128,
-                                            const CUtensorMap& m_k64, const float* __restrict__ lse2,
+                                            const CUtensorMap& m_kb, const float* __restrict__ lse2,
                                             const float* __restrict__ dvec, bf16* __restrict__ dqkv,
                                             int64_t ld_dqkv, const FaShape& sh, int cta) {
-  constexpr uint32_t IDESC_S = idesc_bf16<64, false, false>();
+  constexpr uint32_t IDESC_S = idesc_bf16<BB, false, false>();
   constexpr uint32_t IDESC_AC = idesc_bf16<FA_DH, false, true>();
-  constexpr uint32_t T_S = 0, T_DP = 64, T_DQ = 128;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + DQ_BAR);
-  uint64_t* bar_qo = bar + 0;
-  uint64_t* bar_full = bar + 1;
-  uint64_t* bar_free = bar + 1 + BW_STAGES;
-  uint64_t* bar_s = bar + 1 + 2 * BW_STAGES;
-  uint64_t* bar_p = bar + 2 + 2 * BW_STAGES;
-  uint64_t* bar_done = bar + 3 + 2 * BW_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4 + 2 * BW_STAGES);
+  const BwBars br = bw_bars(smem + DQ_BAR);
 
   const int S = sh.S, d = sh.d, H = sh.H;
-  const int nqb = S / 128, nk = S / 64;
+  const int nqb = S / 128, nk = S / BB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int z = cta / nqb;
   const int qb = cta % nqb;
@@ -497,97 +528,98 @@ __device__ __forceinline__ void attn_bwd_dq(const CUtensorMap& m_q128, const CUt
   const int row0 = sample * S;
   const float sl2 = sh.alpha * 1.4426950408889634f;
 
-  if (warp == 0 && lane == 0) {
-    mbar_init(bar_qo, 1);
-    for (int i = 0; i < BW_STAGES; ++i) {
-      mbar_init(&bar_full[i], 1);
-      mbar_init(&bar_free[i], 1);
-    }
-    mbar_init(bar_s, 1);
-    mbar_init(bar_p, BW_SMW);
-    mbar_init(bar_done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  if (warp == 0 && lane == 0) bw_init(br);
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(br.tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *br.tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(bar_qo, 2 * TILE128);
-      tma_load_2d(smem, &m_q128, bar_qo, head * FA_DH, row0 + qb * 128);
-      tma_load_2d(smem + TILE128, &m_do128, bar_qo, head * FA_DH, row0 + qb * 128);
+      mbar_expect_tx(br.first, 2 * TILE128);
+      tma_load_2d(smem, &m_q128, br.first, head * FA_DH, row0 + qb * 128);
+      tma_load_2d(smem + TILE128, &m_do128, br.first, head * FA_DH, row0 + qb * 128);
       for (int j = 0; j < nk; ++j) {
         const int st = j % BW_STAGES;
-        mbar_wait(&bar_free[st], ((j / BW_STAGES) & 1) ^ 1);
-        uint8_t* sb = smem + DQ_RING + st * 2 * TILE64;
-        mbar_expect_tx(&bar_full[st], 2 * TILE64);
-        tma_load_2d(sb, &m_k64, &bar_full[st], d + head * FA_DH, row0 + j * 64);
-        tma_load_2d(sb + TILE64, &m_k64, &bar_full[st], 2 * d + head * FA_DH, row0 + j * 64);
+        mbar_wait(&br.free_[st], ((j / BW_STAGES) & 1) ^ 1);
+        uint8_t* sb = smem + DQ_RING + st * 2 * TILEB;
+        mbar_expect_tx(&br.full[st], 2 * TILEB);
+        tma_load_2d(sb, &m_kb, &br.full[st], d + head * FA_DH, row0 + j * BB);
+        tma_load_2d(sb + TILEB, &m_kb, &br.full[st], 2 * d + head * FA_DH, row0 + j * BB);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t qa = smem_u32(smem), da = smem_u32(smem + TILE128);
-      mbar_wait(bar_qo, 0);
-      for (int j = 0; j < nk; ++j) {
-        const int st = j % BW_STAGES;
-        const uint32_t ka = smem_u32(smem + DQ_RING + st * 2 * TILE64), va = ka + TILE64;
-        mbar_wait(&bar_full[st], (j / BW_STAGES) & 1);
+      auto issue_sp = [&](int j) {  // S, dP of key block j into buffer j & 1
+        const int st = j % BW_STAGES, b = j & 1;
+        const uint32_t ka = smem_u32(smem + DQ_RING + st * 2 * TILEB), va = ka + TILEB;
+        mbar_wait(&br.full[st], (j / BW_STAGES) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < FA_DH / 16; ++k) {
-          umma_bf16(tmem + T_S, sdesc_sw128(qa + k * 32, 16, 1024), sdesc_sw128(ka + k * 32, 16, 1024), IDESC_S, k != 0);
-          umma_bf16(tmem + T_DP, sdesc_sw128(da + k * 32, 16, 1024), sdesc_sw128(va + k * 32, 16, 1024), IDESC_S, k != 0);
+          umma_bf16(tmem + T_S + b * BB, sdesc_sw128(qa + k * 32, 16, 1024), sdesc_sw128(ka + k * 32, 16, 1024), IDESC_S,
+                    k != 0);
+          umma_bf16(tmem + T_P + b * BB, sdesc_sw128(da + k * 32, 16, 1024), sdesc_sw128(va + k * 32, 16, 1024), IDESC_S,
+                    k != 0);
         }
-        umma_commit(bar_s);
-        mbar_wait(bar_p, j & 1);
+        umma_commit(&br.s[b]);
+      };
+      mbar_wait(br.first, 0);
+      issue_sp(0);
+      for (int j = 0; j < nk; ++j) {
+        const int st = j % BW_STAGES, b = j & 1;
+        if (j + 1 < nk) issue_sp(j + 1);
+        mbar_wait(&br.p[b], (j >> 1) & 1);
         tc_fence_after();
+        const uint32_t ka = smem_u32(smem + DQ_RING + st * 2 * TILEB);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)  // K = 64 keys, 16 per MMA; B = K_j as the MN-major (key rows) operand
-          fa_umma_ts(tmem + T_DQ, tmem + T_S + k * 8, sdesc_sw128(ka + k * 2048, 8192, 1024), IDESC_AC, (j | k) != 0);
-        umma_commit(&bar_free[st]);
+        for (int k = 0; k < BB / 16; ++k)  // K = 32 keys, 16 per MMA; B = K_j as the MN-major (key rows) operand
+          fa_umma_ts(tmem + T_A0, tmem + T_S + b * BB + k * 8, sdesc_sw128(ka + k * 2048, 8192, 1024), IDESC_AC,
+                     (j | k) != 0);
+        umma_commit(&br.free_[st]);
       }
-      umma_commit(bar_done);
+      umma_commit(br.done);
     }
   } else {
-    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 32-key chunk
+    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 16-key half of a block
     const int lr = q * 32 + lane;  // query row
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const int64_t zq = static_cast<int64_t>(z) * S + qb * 128 + lr;
     const float mls = -__ldg(lse2 + zq), dq = __ldg(dvec + zq);
     for (int j = 0; j < nk; ++j) {
-      mbar_wait(bar_s, j & 1);
+      const int b = j & 1;
+      mbar_wait(&br.s[b], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t sv[32], pv[32];
-      tmem_ld32(trow + T_S + c * 32, sv);
-      tmem_ld32(trow + T_DP + c * 32, pv);
-      uint32_t dk[16];
+      uint32_t sv[16], pv[16];
+      fa_tmem_ld16(trow + T_S + b * BB + c * 16, sv);
+      fa_tmem_ld16(trow + T_P + b * BB + c * 16, pv);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      uint32_t dk[8];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < 8; ++i) {
         const float p0 = exp2f(fmaf(__uint_as_float(sv[2 * i]), sl2, mls));
         const float p1 = exp2f(fmaf(__uint_as_float(sv[2 * i + 1]), sl2, mls));
         dk[i] = fa_pack(sh.alpha * p0 * (__uint_as_float(pv[2 * i]) - dq),
                         sh.alpha * p1 * (__uint_as_float(pv[2 * i + 1]) - dq));
       }
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // chunk 0 read before chunk 1 lands
-      fa_tmem_st16(trow + T_S + c * 16, dk);
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // half 0 read before half 1 lands
+      fa_tmem_st8(trow + T_S + b * BB + c * 8, dk);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) fa_mbar_arrive(bar_p);
+      if (lane == 0) fa_mbar_arrive(&br.p[b]);
     }
-    mbar_wait(bar_done, 0);
+    mbar_wait(br.done, 0);
     tc_fence_after();
     const int64_t qrow = static_cast<int64_t>(row0) + qb * 128 + lr;
     uint32_t v[32];
-    tmem_ld32(trow + T_DQ + c * 32, v);
+    tmem_ld32(trow + T_A0 + c * 32, v);
     fa_store_row32(dqkv + qrow * ld_dqkv + head * FA_DH + c * 32, v);
   }
   tc_fence_before();
@@ -670,8 +702,8 @@ int gpp_flash_attn_bwd(const void* qkv, const float* lse2, const void* o, int64_
   GPP_LAUNCH_CHECK();
   CUtensorMap mk128, mq64, mdo64, mdo128;  // qkv maps serve Q, K and V by coordinates
   if ((rc = tc::make_map_bf16(&mk128, qkv, 3 * d, T, 3 * d, 64, 128))) return rc;
-  if ((rc = tc::make_map_bf16(&mq64, qkv, 3 * d, T, 3 * d, 64, 64))) return rc;
-  if ((rc = tc::make_map_bf16(&mdo64, dout, d, T, lddo, 64, 64))) return rc;
+  if ((rc = tc::make_map_bf16(&mq64, qkv, 3 * d, T, 3 * d, 64, tc::BB))) return rc;
+  if ((rc = tc::make_map_bf16(&mdo64, dout, d, T, lddo, 64, tc::BB))) return rc;
   if ((rc = tc::make_map_bf16(&mdo128, dout, d, T, lddo, 64, 128))) return rc;
   static bool attr = false;
   constexpr int SMEM_BW = tc::SMEM_DKDV > tc::SMEM_DQ ? tc::SMEM_DKDV : tc::SMEM_DQ;
