@@ -151,6 +151,11 @@ int gpp_ce_loss(float* loss_acc, void* dlogits, int64_t lddl, const void* logits
                 void* stream);
 
 /* colsum: out[n] (+)= sum_m x[m,n] (x in dtype, out fp32). */
+/* out_i[:N_i] (+)= column sums of x_i [M_i, N_i] for i < n, in as few launches as possible
+ * (the bias gradients of a whole backward task: one launch instead of one per layer).
+ * Host arrays; each sum is deterministic (fixed-order partials). */
+int gpp_colsum_multi(int n, const void* const* x, const int64_t* ldx, const int64_t* M, const int64_t* N,
+                     float* const* out, int accumulate, int dtype, void* stream);
 int gpp_colsum(float* out, const void* x, int64_t ldx, int64_t M, int64_t N, int accumulate,
                int dtype, void* stream);
 

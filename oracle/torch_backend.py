@@ -85,6 +85,10 @@ class TorchBackend:
         self.rowdot_fwd(z, x, w, bias)
         (self.mse_loss if kind == "mse" else self.bce_loss)(loss_acc, dz, z, y, scale)
 
+    def colsum_multi(self, outs, xs, accumulate):
+        for o, x in zip(outs, xs):
+            self.colsum(o, x, accumulate)
+
     def colsum(self, out, x, accumulate):
         s = x.float().sum(0)
         out.add_(s) if accumulate else out.copy_(s)

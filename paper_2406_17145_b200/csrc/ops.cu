@@ -303,18 +303,17 @@ __global__ void colsum_final_kernel(float* out, const float* part, int splits, i
 // arrive (per-range arrival counter) sums the partials in split order and writes out,
 // then re-arms its counter -- deterministic, and graph-replay safe.
 template <typename T>
-__global__ void __launch_bounds__(256) colsum_vec_kernel(float* out, float* part, unsigned* counters,
-                                                         const T* x, int64_t ldx, int64_t M,
-                                                         int64_t N, int64_t rows_per_split,
-                                                         int accumulate) {
+__device__ __forceinline__ void colsum_vec_body(float* out, float* part, unsigned* counters, const T* x,
+                                                int64_t ldx, int64_t M, int64_t N, int64_t rows_per_split,
+                                                int accumulate, unsigned bx, unsigned by, unsigned nsplit) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int CPB = 32 * VEC;
   constexpr int UNROLL = 8;
   __shared__ float red[8][CPB + 1];
   __shared__ bool is_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t col = static_cast<int64_t>(blockIdx.x) * CPB + lane * VEC;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_split;
+  const int64_t col = static_cast<int64_t>(bx) * CPB + lane * VEC;
+  const int64_t r0 = static_cast<int64_t>(by) * rows_per_split;
   const int64_t r1 = min(M, r0 + rows_per_split);
   float acc[VEC];
 #pragma unroll
@@ -347,25 +346,61 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(float* out, float* part
 #pragma unroll
   for (int j = 0; j < VEC; ++j) red[w][lane * VEC + j] = acc[j];
   __syncthreads();
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * CPB + threadIdx.x;
+  const int64_t c = static_cast<int64_t>(bx) * CPB + threadIdx.x;
   if (threadIdx.x < CPB && c < N) {
     float t = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) t += red[i][threadIdx.x];
-    part[static_cast<int64_t>(blockIdx.y) * N + c] = t;
+    part[static_cast<int64_t>(by) * N + c] = t;
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(&counters[blockIdx.x], 1u) == gridDim.y - 1;
+  if (threadIdx.x == 0) is_last = atomicAdd(&counters[bx], 1u) == nsplit - 1;
   __syncthreads();
   if (!is_last) return;
   __threadfence();
   if (threadIdx.x < CPB && c < N) {
     float t = 0.f;
-    for (unsigned s = 0; s < gridDim.y; ++s) t += __ldcg(part + static_cast<int64_t>(s) * N + c);
+    for (unsigned sp = 0; sp < nsplit; ++sp) t += __ldcg(part + static_cast<int64_t>(sp) * N + c);
     out[c] = accumulate ? out[c] + t : t;
   }
-  if (threadIdx.x == 0) counters[blockIdx.x] = 0;
+  if (threadIdx.x == 0) counters[bx] = 0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_vec_kernel(float* out, float* part, unsigned* counters,
+                                                         const T* x, int64_t ldx, int64_t M,
+                                                         int64_t N, int64_t rows_per_split,
+                                                         int accumulate) {
+  colsum_vec_body<T>(out, part, counters, x, ldx, M, N, rows_per_split, accumulate, blockIdx.x, blockIdx.y,
+                     gridDim.y);
+}
+
+// Several column sums in ONE launch (the bias gradients of a whole backward task): job i
+// owns blocks [blk0, blk0 + vb * splits) of the 1-D grid, its own partial / counter ranges.
+constexpr int kColsumJobs = 24;
+struct ColsumJob {
+  const void* x;
+  float* out;
+  int64_t ldx, M, N, rps;
+  int part_off, cnt_off, vb, splits, blk0, pad;
+};
+struct ColsumJobs {
+  ColsumJob j[kColsumJobs];
+  int n, accumulate;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_multi_kernel(float* part, unsigned* counters,
+                                                           const __grid_constant__ ColsumJobs jobs) {
+  const int b = static_cast<int>(blockIdx.x);
+  int i = 0;
+  while (i + 1 < jobs.n && b >= jobs.j[i + 1].blk0) ++i;
+  const ColsumJob& jb = jobs.j[i];
+  const int local = b - jb.blk0;
+  colsum_vec_body<T>(jb.out, part + jb.part_off, counters + jb.cnt_off, static_cast<const T*>(jb.x), jb.ldx, jb.M,
+                     jb.N, jb.rps, jobs.accumulate, static_cast<unsigned>(local % jb.vb),
+                     static_cast<unsigned>(local / jb.vb), static_cast<unsigned>(jb.splits));
 }
 
 // Persistent per-device scratch for the partial sums and the arrival counters
@@ -420,6 +455,63 @@ int colsum_launch(float* out, const T* x, int64_t ldx, const float* wts, int64_t
   colsum_final_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, s>>>(out, part, splits, N, accumulate);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
+}
+
+// colsum of several [M_i, N_i] tensors: vectorisable jobs share launches of <= kColsumJobs
+// (partial and counter ranges laid out per job); the rest go through colsum_launch.
+template <typename T>
+int colsum_multi_launch(int n, const void* const* xs, const int64_t* lds, const int64_t* Ms, const int64_t* Ns,
+                        float* const* outs, int accumulate, cudaStream_t s) {
+  constexpr int VEC = 16 / sizeof(T);
+  float* part = colsum_scratch();
+  if (!part) { set_error("colsum scratch allocation failed"); return GPP_ERR_CUDA; }
+  unsigned* counters = reinterpret_cast<unsigned*>(part + kScratchFloats);
+  ColsumJobs jobs{};
+  int64_t part_used = 0, cnt_used = 0, blocks = 0;
+  auto flush = [&]() -> int {
+    if (jobs.n == 0) return GPP_OK;
+    jobs.accumulate = accumulate;
+    colsum_multi_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, s>>>(part, counters, jobs);
+    GPP_LAUNCH_CHECK();
+    jobs.n = 0;
+    part_used = cnt_used = blocks = 0;
+    return GPP_OK;
+  };
+  for (int i = 0; i < n; ++i) {
+    const T* x = static_cast<const T*>(xs[i]);
+    const int64_t M = Ms[i], N = Ns[i], ld = lds[i];
+    GPP_ARG_CHECK(x && outs[i] && M > 0 && N > 0, "bad colsum job");
+    const int64_t vb = (N + 32 * VEC - 1) / (32 * VEC);
+    if (N % VEC != 0 || ld % VEC != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0 || vb > kCounters) {
+      const int rc = colsum_launch<T>(outs[i], x, ld, nullptr, M, N, accumulate, s);
+      if (rc) return rc;
+      continue;
+    }
+    int64_t splits = (148 * 4 + vb - 1) / vb;
+    if (splits > (M + 63) / 64) splits = (M + 63) / 64;
+    if (splits < 1) splits = 1;
+    while (splits > 1 && splits * N > kScratchFloats) --splits;
+    if (jobs.n == kColsumJobs || part_used + splits * N > kScratchFloats || cnt_used + vb > kCounters) {
+      const int rc = flush();
+      if (rc) return rc;
+    }
+    ColsumJob& jb = jobs.j[jobs.n++];
+    jb.x = x;
+    jb.out = outs[i];
+    jb.ldx = ld;
+    jb.M = M;
+    jb.N = N;
+    jb.rps = (M + splits - 1) / splits;
+    jb.part_off = static_cast<int>(part_used);
+    jb.cnt_off = static_cast<int>(cnt_used);
+    jb.vb = static_cast<int>(vb);
+    jb.splits = static_cast<int>(splits);
+    jb.blk0 = static_cast<int>(blocks);
+    part_used += splits * N;
+    cnt_used += vb;
+    blocks += vb * splits;
+  }
+  return flush();
 }
 
 // ---------------- losses (single block, deterministic reductions) ----------------
@@ -769,6 +861,14 @@ int gpp_colsum(float* out, const void* x, int64_t ldx, int64_t M, int64_t N, int
   return dtype == GPP_BF16
       ? colsum_launch<bf16>(out, static_cast<const bf16*>(x), ldx, nullptr, M, N, accumulate, s)
       : colsum_launch<float>(out, static_cast<const float*>(x), ldx, nullptr, M, N, accumulate, s);
+}
+
+int gpp_colsum_multi(int n, const void* const* x, const int64_t* ldx, const int64_t* M, const int64_t* N,
+                     float* const* out, int accumulate, int dtype, void* stream) {
+  GPP_ARG_CHECK(n >= 0 && (n == 0 || (x && ldx && M && N && out)), "bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return dtype == GPP_BF16 ? colsum_multi_launch<bf16>(n, x, ldx, M, N, out, accumulate, s)
+                           : colsum_multi_launch<float>(n, x, ldx, M, N, out, accumulate, s);
 }
 
 int gpp_sgd_step(float* master, void* shadow_bf16, const float* grad, int64_t n, float lr,

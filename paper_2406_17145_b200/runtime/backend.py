@@ -46,6 +46,9 @@ class CudaBackend:
     def rowdot_loss(self, z, dz, loss_acc, x, w, bias, y, kind, scale):
         lib.rowdot_loss(z, dz, loss_acc, x, w, bias, y, kind, scale)
 
+    def colsum_multi(self, outs, xs, accumulate):
+        lib.colsum_multi(outs, xs, accumulate=accumulate)
+
     def colsum(self, out, x, accumulate):
         lib.colsum(out, x, accumulate=accumulate)
 

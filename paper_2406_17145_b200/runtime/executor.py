@@ -163,6 +163,7 @@ class Executor:
         self.keep_grads = keep_grads
         self._fuse_req = fuse_optimizer
         self._transport_kind = transport
+        self.bias_queue: list = []  # (bias-gradient view, output gradient) of the running task
         # test hook: when a dict, every dense op's forward output is copied into it under
         # (op, task) -- the oracle takes the device's ReLU masks from these (tests only)
         self.tap: dict | None = None
@@ -575,19 +576,19 @@ class Executor:
                     saved, act = self._saved_for(u, x, slot)
                     be.linear_dgrad(self._dx_target(u, slot), dz, self.W[(o, "w")], saved, act)
 
+                self.bias_queue.append((self.G[(o, "b")], dz))  # bias grads: one launch per task
                 if self.d > 1 and j == self.last_bw:
                     # DP stage: this weight's gradient is final -> overlap its all-reduce
                     # with the rest of the backward pass (bucket = one layer's weight)
-                    be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
+                    be.linear_wgrad(self.G[(o, "w")], None, dz, x, accumulate)
                     self._ar_handles.append(self.tp.allreduce_async(self.G[(o, "w")]))
                 elif self.fuse and j == self.last_bw:
                     # weight gradient + SGD in one epilogue, the bias gradient summed in the same
                     # kernel (applied by the flat SGD later)
                     be.linear_wgrad_sgd(self.P[(o, "w")], self.W[(o, "w")] if self.shadow is not None else None,
-                                        self.G[(o, "w")], dz, x, self.lr, accumulate, self.keep_grads,
-                                        dbias=self.G[(o, "b")])
+                                        self.G[(o, "w")], dz, x, self.lr, accumulate, self.keep_grads)
                 else:
-                    be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dz, x, accumulate)
+                    be.linear_wgrad(self.G[(o, "w")], None, dz, x, accumulate)
             elif spec.kind == "mmt_layer":
                 lay = self.mmt[o]
                 x = self._input(o, j, slot, batch)
@@ -625,7 +626,8 @@ class Executor:
             elif spec.kind == "ce_head":
                 x = self._input(o, j, slot, batch)
                 dl = self.dpred[o][slot]
-                be.linear_wgrad(self.G[(o, "w")], self.G[(o, "b")], dl, x, accumulate)
+                be.linear_wgrad(self.G[(o, "w")], None, dl, x, accumulate)
+                self.bias_queue.append((self.G[(o, "b")], dl))
                 if needs_dx:
                     u = preds[0]
                     saved, act = self._saved_for(u, x, slot)
@@ -638,6 +640,7 @@ class Executor:
             if marked:
                 works += sends.flush(post)
         be.copy_rows_multi(emb_dst, emb_src)  # embedding-bag output grads -> the SGD scatter's rows
+        self._flush_bias(accumulate)
         for ws in pending.values():
             for w in ws:
                 w.wait()
@@ -645,6 +648,20 @@ class Executor:
         works += self._isend_many([(self.tok_tx, pc.producer) for pc in self.tok_in[j]])
         if works:
             self._send_works[("bw", slot)] = works
+
+    def _flush_bias(self, accumulate: bool) -> None:
+        """The task's queued bias gradients (column sums of each layer's output gradient) in
+        as few launches as possible (per dtype), before the next task reuses the rings."""
+        if not self.bias_queue:
+            return
+        by_dt: dict = {}
+        for out, dz in self.bias_queue:
+            by_dt.setdefault(dz.dtype, ([], []))
+            by_dt[dz.dtype][0].append(out)
+            by_dt[dz.dtype][1].append(dz)
+        for outs, xs in by_dt.values():
+            self.be.colsum_multi(outs, xs, accumulate)
+        self.bias_queue = []
 
     # ------------------------------------------------------------ iteration
     def run_iteration(self, batch: dict[str, torch.Tensor], step_optimizer: bool = True):

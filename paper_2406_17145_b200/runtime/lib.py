@@ -40,6 +40,7 @@ _SIGS = {
     "gpp_mse_loss": ([_vp, _vp, _vp, _vp, _i64, _f32, _vp], _i32),
     "gpp_bce_loss": ([_vp, _vp, _vp, _vp, _i64, _f32, _vp], _i32),
     "gpp_ce_loss": ([_vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _f32, _i32, _vp], _i32),
+    "gpp_colsum_multi": ([_i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp], _i32),
     "gpp_colsum": ([_vp, _vp, _i64, _i64, _i64, _i32, _i32, _vp], _i32),
     "gpp_sgd_step": ([_vp, _vp, _vp, _i64, _f32, _vp], _i32),
     "gpp_copy_rows": ([_vp, _i64, _vp, _i64, _i64, _i64, _i32, _vp], _i32),
@@ -230,6 +231,18 @@ def rowdot_loss(z, dz, loss_acc, x, w, bias, y, kind: str, scale: float, stream=
     M, K = x.shape
     call("gpp_rowdot_loss", _ptr(z), _ptr(dz), _ptr(loss_acc), _ptr(x), _ld(x), _ptr(w), _ptr(bias), _ptr(y), M, K,
          {"mse": 0, "bce": 1}[kind], float(scale), _dt(x), _stream(stream))
+
+
+def colsum_multi(outs, xs, accumulate=False, stream=None):
+    """out_i (+)= column sums of x_i (2-D, one dtype) for every pair, in as few launches as possible."""
+    n = len(xs)
+    if n == 0:
+        return
+    P = ctypes.c_void_p * n
+    I = ctypes.c_int64 * n
+    call("gpp_colsum_multi", n, P(*[_ptr(x) for x in xs]), I(*[_ld(x) for x in xs]), I(*[x.shape[0] for x in xs]),
+         I(*[x.shape[1] for x in xs]), P(*[_ptr(o) for o in outs]), int(bool(accumulate)), _dt(xs[0]),
+         _stream(stream))
 
 
 def colsum(out, x, accumulate=False, stream=None):

@@ -131,11 +131,12 @@ class MMTLayer:
     def _wgrad(self, name, bname, dz, xin, accumulate, last):
         ex, be = self.ex, self.ex.be
         o = self.o
+        ex.bias_queue.append((ex.G[(o, bname)], dz))  # summed with the task's other biases, one launch
         if ex.fuse and last:
             be.linear_wgrad_sgd(ex.P[(o, name)], ex.W[(o, name)] if ex.shadow is not None else None,
-                                ex.G[(o, name)], dz, xin, ex.lr, accumulate, ex.keep_grads, dbias=ex.G[(o, bname)])
+                                ex.G[(o, name)], dz, xin, ex.lr, accumulate, ex.keep_grads)
         else:
-            be.linear_wgrad(ex.G[(o, name)], ex.G[(o, bname)], dz, xin, accumulate)
+            be.linear_wgrad(ex.G[(o, name)], None, dz, xin, accumulate)
             if ex.d > 1 and last:
                 ex._ar_handles.append(ex.tp.allreduce_async(ex.G[(o, name)]))
 

@@ -655,3 +655,23 @@ def test_rowdot_loss_fused(cuda_lib, kind, K, dt):
     cuda_lib.rowdot_loss(z, dz, acc2, x, w, b, y, kind, scale)
     torch.cuda.synchronize()
     assert torch.equal(acc, acc2)
+
+
+def test_colsum_multi_matches_per_tensor(cuda_lib):
+    """Several bias-gradient column sums in one launch (shapes of an MMT layer + ragged /
+    unaligned ones that fall back), accumulate on and off, deterministic."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    shapes = [(8192, 1024), (8192, 4096), (8192, 3072), (300, 520), (777, 100), (64, 8)]
+    xs = [torch.randn(m, n, device="cuda", generator=g).bfloat16() for m, n in shapes]
+    for acc in (False, True):
+        outs = [torch.randn(n, device="cuda", generator=g) for _, n in shapes]
+        base = [o.clone() for o in outs]
+        cuda_lib.colsum_multi(outs, xs, accumulate=acc)
+        torch.cuda.synchronize()
+        for o, b, x in zip(outs, base, xs):
+            ref = x.float().sum(0) + (b if acc else 0)
+            assert torch.allclose(o, ref, rtol=1e-4, atol=2e-3)
+        again = [b.clone() for b in base]
+        cuda_lib.colsum_multi(again, xs, accumulate=acc)
+        torch.cuda.synchronize()
+        assert all(torch.equal(a, o) for a, o in zip(again, outs))
