@@ -25,6 +25,7 @@
 // head-interleaved, lse2 / D [Z, S] fp32 with z = sample * H + head.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "gemm.cuh"
@@ -271,20 +272,25 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(float* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------------------
-// Backward: dK/dV per (z, 128-key block) and dQ per (z, 128-query block), both in one launch,
-// no cross-CTA reduction.  The loop dimension runs in blocks of BB = 32 with DOUBLE-BUFFERED
-// S / dP TMEM tiles: the MMA warp issues block j+1's S and dP while the softmax warps turn
-// block j's into P / dS, then block j's dV / dK (or dQ) MMAs -- the tensor pipe and the
-// softmax overlap inside a CTA.  256 TMEM columns (S[2], dP[2] 32 each, two 64-column
-// accumulators), so two CTAs still share an SM.  Warps: 0 TMA, 1 MMA (+ TMEM alloc), 2..9
-// two per TMEM lane quarter (one row each), splitting a block's 32 columns in halves of 16.
+// Backward: a PERSISTENT launch of two CTA roles, no cross-CTA reduction.  CTAs [0, P) loop
+// over the dK/dV items (z, 128-key block), CTAs [P, 2P) over the dQ items (z, 128-query
+// block); one CTA of each role per SM (256 TMEM columns each).  Inside an item the loop
+// dimension runs in blocks of BB = 32 with double-buffered S / dP TMEM tiles (the MMA warp
+// issues block j+1's S and dP while the softmax warps turn block j's into P / dS, then block
+// j's accumulating MMAs).  Across items the 32 KB "first" tiles (K, V or Q, dO) are double
+// buffered, so the next item's load overlaps the current item, and the TMEM accumulators are
+// handed back by an mbarrier once the epilogue warps have read them out -- per-item launch,
+// barrier-init, TMEM-alloc and first-load latencies (~50 us of the non-persistent 2048-CTA
+// grid) are paid once per CTA.  Warps: 0 TMA, 1 MMA (+ TMEM alloc), 2..9 two per TMEM lane
+// quarter (one row each), splitting a block's 32 columns in halves of 16.
 namespace {
 constexpr int BB = 32;          // loop block (queries for dK/dV, keys for dQ)
 constexpr int BW_SMW = 8;
 constexpr int BW_THREADS = 64 + 32 * BW_SMW;
-constexpr int BW_STAGES = 6;
+constexpr int BW_STAGES = 4;
 constexpr uint32_t TILEB = BB * 128;     // 32 rows x 64 bf16 (128B-swizzled): 4 KB
 constexpr uint32_t TILE128 = 128 * 128;  // 16 KB
+constexpr uint32_t FIRST_BYTES = 2 * TILE128;  // K + V, or Q + dO
 
 __device__ __forceinline__ void fa_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -320,307 +326,237 @@ __device__ __forceinline__ void fa_store_row32(bf16* dst, const uint32_t (&v)[32
   }
 }
 
-// dK / dV smem: K, V (128 keys) | stages of [Q 32 rows | dO 32 rows | lse2[32] | D[32]]
-constexpr uint32_t KV_STAGE_STRIDE = 9 * 1024;  // 2 x 4 KB tiles + 256 B vectors, 1 KB aligned
-constexpr uint32_t KV_RING = 2 * TILE128;
-constexpr uint32_t KV_BAR = KV_RING + BW_STAGES * KV_STAGE_STRIDE;
-constexpr int SMEM_DKDV = KV_BAR + 256 + 1024;
-// dQ smem: Q, dO (128 queries) | stages of [K 32 rows | V 32 rows]
-constexpr uint32_t DQ_RING = 2 * TILE128;
-constexpr uint32_t DQ_BAR = DQ_RING + BW_STAGES * 2 * TILEB;
-constexpr int SMEM_DQ = DQ_BAR + 256 + 1024;
-// TMEM columns (both kernels): S[b] at 32b, dP[b] at 64 + 32b, accumulators at 128 / 192
+// smem: first tiles [2] x 32 KB | stages [BW_STAGES] of 9 KB (two 32-row tiles + 2 x 128 B of
+// per-query lse2 / D, used by the dK/dV role) | barriers
+constexpr uint32_t BW_STAGE_STRIDE = 9 * 1024;
+constexpr uint32_t BW_RING = 2 * FIRST_BYTES;
+constexpr uint32_t BW_BAR = BW_RING + BW_STAGES * BW_STAGE_STRIDE;
+constexpr int SMEM_BW = BW_BAR + 256 + 1024;
+// TMEM columns: S[b] at 32b, dP[b] at 64 + 32b, accumulators at 128 (dV | dQ) and 192 (dK)
 constexpr uint32_t T_S = 0, T_P = 64, T_A0 = 128, T_A1 = 192;
-
-// barrier block of both kernels
-struct BwBars {
-  uint64_t* first;                // K/V (dK/dV) or Q/dO (dQ) landed
-  uint64_t* full;                 // [BW_STAGES]
-  uint64_t* free_;                // [BW_STAGES]
-  uint64_t* s;                    // [2] S, dP of the buffer in TMEM
-  uint64_t* p;                    // [2] bf16 P / dS of the buffer in TMEM (8 warps)
-  uint64_t* done;                 // every MMA done
-  uint32_t* tmem_slot;
-};
-__device__ __forceinline__ BwBars bw_bars(uint8_t* base) {
-  uint64_t* b = reinterpret_cast<uint64_t*>(base);
-  return {b, b + 1, b + 1 + BW_STAGES, b + 1 + 2 * BW_STAGES, b + 3 + 2 * BW_STAGES, b + 5 + 2 * BW_STAGES,
-          reinterpret_cast<uint32_t*>(b + 6 + 2 * BW_STAGES)};
-}
-__device__ __forceinline__ void bw_init(const BwBars& br) {
-  mbar_init(br.first, 1);
-  for (int i = 0; i < BW_STAGES; ++i) {
-    mbar_init(&br.full[i], 1);
-    mbar_init(&br.free_[i], 1);
-  }
-  for (int i = 0; i < 2; ++i) {
-    mbar_init(&br.s[i], 1);
-    mbar_init(&br.p[i], BW_SMW);
-  }
-  mbar_init(br.done, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
 }  // namespace
 
-// dK, dV of one (z, 128-key block), looping over the S/32 query blocks:
-//   S^T = K Q_j^T, dP^T = V dO_j^T (TMEM, lane = key, 32 query columns each);
-//   P^T = exp2(alpha log2e S^T - lse2[q]), dS^T = alpha P^T o (dP^T - D[q]) -> bf16 pairs in
-//   place (TMEM A operands);  dV += P^T dO_j, dK += dS^T Q_j (accumulated in TMEM).
-__device__ __forceinline__ void attn_bwd_dkdv(const CUtensorMap& m_k128, const CUtensorMap& m_qb,
-                                              const CUtensorMap& m_dob, const float* __restrict__ lse2,
-                                              const float* __restrict__ dvec, bf16* __restrict__ dqkv,
-                                              int64_t ld_dqkv, const FaShape& sh, int cta) {
-  constexpr uint32_t IDESC_ST = idesc_bf16<BB, false, false>();
-  constexpr uint32_t IDESC_AC = idesc_bf16<FA_DH, false, true>();
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const BwBars br = bw_bars(smem + KV_BAR);
-
-  const int S = sh.S, d = sh.d, H = sh.H;
-  const int nkb = S / 128, nq = S / BB;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int z = cta / nkb;
-  const int kb = cta % nkb;
-  const int sample = z / H, head = z % H;
-  const int row0 = sample * S;
-  const float sl2 = sh.alpha * 1.4426950408889634f;
-
-  if (warp == 0 && lane == 0) bw_init(br);
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(br.tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *br.tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(br.first, 2 * TILE128);
-      tma_load_2d(smem, &m_k128, br.first, d + head * FA_DH, row0 + kb * 128);
-      tma_load_2d(smem + TILE128, &m_k128, br.first, 2 * d + head * FA_DH, row0 + kb * 128);
-      const float* lz = lse2 + static_cast<int64_t>(z) * S;
-      const float* dz = dvec + static_cast<int64_t>(z) * S;
-      for (int j = 0; j < nq; ++j) {
-        const int st = j % BW_STAGES;
-        mbar_wait(&br.free_[st], ((j / BW_STAGES) & 1) ^ 1);
-        uint8_t* sb = smem + KV_RING + st * KV_STAGE_STRIDE;
-        mbar_expect_tx(&br.full[st], 2 * TILEB + 2 * BB * 4);
-        tma_load_2d(sb, &m_qb, &br.full[st], head * FA_DH, row0 + j * BB);
-        tma_load_2d(sb + TILEB, &m_dob, &br.full[st], head * FA_DH, row0 + j * BB);
-        fa_bulk_load(sb + 2 * TILEB, lz + j * BB, BB * 4, &br.full[st]);
-        fa_bulk_load(sb + 2 * TILEB + 128, dz + j * BB, BB * 4, &br.full[st]);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t ka = smem_u32(smem), va = smem_u32(smem + TILE128);
-      auto issue_sp = [&](int j) {  // S^T, dP^T of query block j into buffer j & 1
-        const int st = j % BW_STAGES, b = j & 1;
-        const uint32_t qa = smem_u32(smem + KV_RING + st * KV_STAGE_STRIDE), da = qa + TILEB;
-        mbar_wait(&br.full[st], (j / BW_STAGES) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < FA_DH / 16; ++k) {
-          umma_bf16(tmem + T_S + b * BB, sdesc_sw128(ka + k * 32, 16, 1024), sdesc_sw128(qa + k * 32, 16, 1024), IDESC_ST,
-                    k != 0);
-          umma_bf16(tmem + T_P + b * BB, sdesc_sw128(va + k * 32, 16, 1024), sdesc_sw128(da + k * 32, 16, 1024), IDESC_ST,
-                    k != 0);
-        }
-        umma_commit(&br.s[b]);
-      };
-      mbar_wait(br.first, 0);
-      issue_sp(0);
-      for (int j = 0; j < nq; ++j) {
-        const int st = j % BW_STAGES, b = j & 1;
-        if (j + 1 < nq) issue_sp(j + 1);  // overlaps block j's softmax
-        mbar_wait(&br.p[b], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t qa = smem_u32(smem + KV_RING + st * KV_STAGE_STRIDE), da = qa + TILEB;
-#pragma unroll
-        for (int k = 0; k < BB / 16; ++k) {  // K = 32 queries, 16 per MMA (8 packed columns)
-          const uint32_t acc = (j | k) != 0;
-          fa_umma_ts(tmem + T_A0, tmem + T_S + b * BB + k * 8, sdesc_sw128(da + k * 2048, 8192, 1024), IDESC_AC, acc);
-          fa_umma_ts(tmem + T_A1, tmem + T_P + b * BB + k * 8, sdesc_sw128(qa + k * 2048, 8192, 1024), IDESC_AC, acc);
-        }
-        umma_commit(&br.free_[st]);
-      }
-      umma_commit(br.done);
-    }
-  } else {
-    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 16-query half of a block
-    const int lr = q * 32 + lane;  // key row
-    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    for (int j = 0; j < nq; ++j) {
-      const int st = j % BW_STAGES, b = j & 1;
-      const float* vec = reinterpret_cast<const float*>(smem + KV_RING + st * KV_STAGE_STRIDE + 2 * TILEB);
-      mbar_wait(&br.full[st], (j / BW_STAGES) & 1);  // lse2 / D of the stage (TMA-written)
-      mbar_wait(&br.s[b], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sv[16], pv[16];
-      fa_tmem_ld16(trow + T_S + b * BB + c * 16, sv);
-      fa_tmem_ld16(trow + T_P + b * BB + c * 16, pv);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      uint32_t pk[8], dk[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float2 ls = *reinterpret_cast<const float2*>(vec + c * 16 + 2 * i);
-        const float2 dd = *reinterpret_cast<const float2*>(vec + 32 + c * 16 + 2 * i);
-        const float p0 = exp2f(fmaf(__uint_as_float(sv[2 * i]), sl2, -ls.x));
-        const float p1 = exp2f(fmaf(__uint_as_float(sv[2 * i + 1]), sl2, -ls.y));
-        pk[i] = fa_pack(p0, p1);
-        dk[i] = fa_pack(sh.alpha * p0 * (__uint_as_float(pv[2 * i]) - dd.x),
-                        sh.alpha * p1 * (__uint_as_float(pv[2 * i + 1]) - dd.y));
-      }
-      // bf16 pairs: queries 16c + 2i, +1 -> column 8c + i of the buffer.  Half 1's pairs land in
-      // half 0's columns, so both warps of the quarter must have read theirs first.
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-      fa_tmem_st8(trow + T_S + b * BB + c * 8, pk);
-      fa_tmem_st8(trow + T_P + b * BB + c * 8, dk);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) fa_mbar_arrive(&br.p[b]);
-    }
-    mbar_wait(br.done, 0);
-    tc_fence_after();
-    const int64_t krow = static_cast<int64_t>(row0) + kb * 128 + lr;
-    // half-0 warps write dV, half-1 warps dK
-    const uint32_t src = trow + (c == 0 ? T_A0 : T_A1);
-    bf16* dst = dqkv + krow * ld_dqkv + (c == 0 ? 2 * d : d) + head * FA_DH;
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      uint32_t v[32];
-      tmem_ld32(src + h2 * 32, v);
-      fa_store_row32(dst + h2 * 32, v);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
-  }
-}
-
-// dQ of one (z, 128-query block), looping over the S/32 key blocks:
-//   S = Q K_j^T, dP = dO V_j^T (TMEM, lane = query);  dS = alpha P o (dP - D[q]) with
-//   P = exp2(alpha log2e S - lse2[q]) (row constants in registers) -> bf16 pairs in place;
-//   dQ += dS K_j (A operand from TMEM).
-__device__ __forceinline__ void attn_bwd_dq(const CUtensorMap& m_q128, const CUtensorMap& m_do128,
-                                            const CUtensorMap& m_kb, const float* __restrict__ lse2,
-                                            const float* __restrict__ dvec, bf16* __restrict__ dqkv,
-                                            int64_t ld_dqkv, const FaShape& sh, int cta) {
+// DQ = false: dK, dV of items (z, 128-key block), looping over the S/32 query blocks:
+//   S^T = K Q_j^T, dP^T = V dO_j^T (lane = key); P^T = exp2(alpha log2e S^T - lse2[q]),
+//   dS^T = alpha P^T o (dP^T - D[q]) -> bf16 pairs in place; dV += P^T dO_j, dK += dS^T Q_j.
+// DQ = true: dQ of items (z, 128-query block), looping over the S/32 key blocks:
+//   S = Q K_j^T, dP = dO V_j^T (lane = query, lse2 / D row constants); dS in place;
+//   dQ += dS K_j.
+template <bool DQ>
+__device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const CUtensorMap& m_qkvb,
+                                              const CUtensorMap& m_do128, const CUtensorMap& m_dob,
+                                              const float* __restrict__ lse2, const float* __restrict__ dvec,
+                                              bf16* __restrict__ dqkv, int64_t ld_dqkv, const FaShape& sh,
+                                              int first_item, int item_step, int n_items) {
   constexpr uint32_t IDESC_S = idesc_bf16<BB, false, false>();
   constexpr uint32_t IDESC_AC = idesc_bf16<FA_DH, false, true>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const BwBars br = bw_bars(smem + DQ_BAR);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BW_BAR);
+  uint64_t* b_ffull = bar + 0;                    // [2] first tiles landed
+  uint64_t* b_ffree = bar + 2;                    // [2] first tiles free (item's MMAs done)
+  uint64_t* b_full = bar + 4;                     // [BW_STAGES]
+  uint64_t* b_free = bar + 4 + BW_STAGES;         // [BW_STAGES]
+  uint64_t* b_s = bar + 4 + 2 * BW_STAGES;        // [2] S, dP of the buffer in TMEM
+  uint64_t* b_p = bar + 6 + 2 * BW_STAGES;        // [2] bf16 P / dS of the buffer in TMEM
+  uint64_t* b_done = bar + 8 + 2 * BW_STAGES;     // the item's accumulators complete
+  uint64_t* b_acc = bar + 9 + 2 * BW_STAGES;      // accumulators read out (8 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10 + 2 * BW_STAGES);
 
   const int S = sh.S, d = sh.d, H = sh.H;
-  const int nqb = S / 128, nk = S / BB;
+  const int per_z = S / 128, nb = S / BB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int z = cta / nqb;
-  const int qb = cta % nqb;
-  const int sample = z / H, head = z % H;
-  const int row0 = sample * S;
   const float sl2 = sh.alpha * 1.4426950408889634f;
+  // my items: first_item, first_item + item_step, ... < n_items
+  const int my_items = first_item < n_items ? (n_items - 1 - first_item) / item_step + 1 : 0;
 
-  if (warp == 0 && lane == 0) bw_init(br);
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&b_ffull[i], 1);
+      mbar_init(&b_ffree[i], 1);
+      mbar_init(&b_s[i], 1);
+      mbar_init(&b_p[i], BW_SMW);
+    }
+    for (int i = 0; i < BW_STAGES; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_free[i], 1);
+    }
+    mbar_init(b_done, 1);
+    mbar_init(b_acc, BW_SMW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(br.tmem_slot))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *br.tmem_slot;
+  const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(br.first, 2 * TILE128);
-      tma_load_2d(smem, &m_q128, br.first, head * FA_DH, row0 + qb * 128);
-      tma_load_2d(smem + TILE128, &m_do128, br.first, head * FA_DH, row0 + qb * 128);
-      for (int j = 0; j < nk; ++j) {
-        const int st = j % BW_STAGES;
-        mbar_wait(&br.free_[st], ((j / BW_STAGES) & 1) ^ 1);
-        uint8_t* sb = smem + DQ_RING + st * 2 * TILEB;
-        mbar_expect_tx(&br.full[st], 2 * TILEB);
-        tma_load_2d(sb, &m_kb, &br.full[st], d + head * FA_DH, row0 + j * BB);
-        tma_load_2d(sb + TILEB, &m_kb, &br.full[st], 2 * d + head * FA_DH, row0 + j * BB);
+      uint32_t g = 0;  // global stage counter (continues across items)
+      for (int it = 0; it < my_items; ++it) {
+        const int item = first_item + it * item_step;
+        const int z = item / per_z, blk = item % per_z;
+        const int row0 = (z / H) * S, head = z % H;
+        const int fb = it & 1;
+        mbar_wait(&b_ffree[fb], ((it >> 1) & 1) ^ 1);
+        uint8_t* first = smem + fb * FIRST_BYTES;
+        mbar_expect_tx(&b_ffull[fb], FIRST_BYTES);
+        if (DQ) {
+          tma_load_2d(first, &m_qkv128, &b_ffull[fb], head * FA_DH, row0 + blk * 128);
+          tma_load_2d(first + TILE128, &m_do128, &b_ffull[fb], head * FA_DH, row0 + blk * 128);
+        } else {
+          tma_load_2d(first, &m_qkv128, &b_ffull[fb], d + head * FA_DH, row0 + blk * 128);
+          tma_load_2d(first + TILE128, &m_qkv128, &b_ffull[fb], 2 * d + head * FA_DH, row0 + blk * 128);
+        }
+        const float* lz = lse2 + static_cast<int64_t>(z) * S;
+        const float* dz = dvec + static_cast<int64_t>(z) * S;
+        for (int j = 0; j < nb; ++j, ++g) {
+          const int st = g % BW_STAGES;
+          mbar_wait(&b_free[st], ((g / BW_STAGES) & 1) ^ 1);
+          uint8_t* sb = smem + BW_RING + st * BW_STAGE_STRIDE;
+          if (DQ) {
+            mbar_expect_tx(&b_full[st], 2 * TILEB);
+            tma_load_2d(sb, &m_qkvb, &b_full[st], d + head * FA_DH, row0 + j * BB);
+            tma_load_2d(sb + TILEB, &m_qkvb, &b_full[st], 2 * d + head * FA_DH, row0 + j * BB);
+          } else {
+            mbar_expect_tx(&b_full[st], 2 * TILEB + 2 * BB * 4);
+            tma_load_2d(sb, &m_qkvb, &b_full[st], head * FA_DH, row0 + j * BB);
+            tma_load_2d(sb + TILEB, &m_dob, &b_full[st], head * FA_DH, row0 + j * BB);
+            fa_bulk_load(sb + 2 * TILEB, lz + j * BB, BB * 4, &b_full[st]);
+            fa_bulk_load(sb + 2 * TILEB + 128, dz + j * BB, BB * 4, &b_full[st]);
+          }
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t qa = smem_u32(smem), da = smem_u32(smem + TILE128);
-      auto issue_sp = [&](int j) {  // S, dP of key block j into buffer j & 1
-        const int st = j % BW_STAGES, b = j & 1;
-        const uint32_t ka = smem_u32(smem + DQ_RING + st * 2 * TILEB), va = ka + TILEB;
-        mbar_wait(&br.full[st], (j / BW_STAGES) & 1);
-        tc_fence_after();
+      uint32_t g = 0;  // global block counter: stage g % BW_STAGES, TMEM buffer g & 1
+      for (int it = 0; it < my_items; ++it) {
+        const int fb = it & 1;
+        const uint32_t fa = smem_u32(smem + fb * FIRST_BYTES), fa2 = fa + TILE128;
+        mbar_wait(&b_ffull[fb], (it >> 1) & 1);
+        auto issue_sp = [&](uint32_t gg) {  // S / dP of block gg into buffer gg & 1
+          const int st = gg % BW_STAGES, b = gg & 1;
+          const uint32_t ta = smem_u32(smem + BW_RING + st * BW_STAGE_STRIDE), tb = ta + TILEB;
+          mbar_wait(&b_full[st], (gg / BW_STAGES) & 1);
+          tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < FA_DH / 16; ++k) {
-          umma_bf16(tmem + T_S + b * BB, sdesc_sw128(qa + k * 32, 16, 1024), sdesc_sw128(ka + k * 32, 16, 1024), IDESC_S,
-                    k != 0);
-          umma_bf16(tmem + T_P + b * BB, sdesc_sw128(da + k * 32, 16, 1024), sdesc_sw128(va + k * 32, 16, 1024), IDESC_S,
-                    k != 0);
+          for (int k = 0; k < FA_DH / 16; ++k) {
+            // dK/dV: S^T = K Q_j^T, dP^T = V dO_j^T;  dQ: S = Q K_j^T, dP = dO V_j^T
+            umma_bf16(tmem + T_S + b * BB, sdesc_sw128(fa + k * 32, 16, 1024), sdesc_sw128(ta + k * 32, 16, 1024),
+                      IDESC_S, k != 0);
+            umma_bf16(tmem + T_P + b * BB, sdesc_sw128(fa2 + k * 32, 16, 1024), sdesc_sw128(tb + k * 32, 16, 1024),
+                      IDESC_S, k != 0);
+          }
+          umma_commit(&b_s[b]);
+        };
+        issue_sp(g);
+        for (int j = 0; j < nb; ++j, ++g) {
+          const int st = g % BW_STAGES, b = g & 1;
+          if (j + 1 < nb) issue_sp(g + 1);  // overlaps block j's softmax
+          mbar_wait(&b_p[b], (g >> 1) & 1);
+          if (j == 0 && it > 0) mbar_wait(b_acc, (it - 1) & 1);  // previous item's accumulators read out
+          tc_fence_after();
+          const uint32_t ta = smem_u32(smem + BW_RING + st * BW_STAGE_STRIDE), tb = ta + TILEB;
+#pragma unroll
+          for (int k = 0; k < BB / 16; ++k) {  // K = 32 rows of the block, 16 per MMA (8 packed columns)
+            const uint32_t acc = (j | k) != 0;
+            if (DQ) {  // B = K_j as the MN-major (key rows) operand
+              fa_umma_ts(tmem + T_A0, tmem + T_S + b * BB + k * 8, sdesc_sw128(ta + k * 2048, 8192, 1024), IDESC_AC, acc);
+            } else {
+              fa_umma_ts(tmem + T_A0, tmem + T_S + b * BB + k * 8, sdesc_sw128(tb + k * 2048, 8192, 1024), IDESC_AC, acc);
+              fa_umma_ts(tmem + T_A1, tmem + T_P + b * BB + k * 8, sdesc_sw128(ta + k * 2048, 8192, 1024), IDESC_AC, acc);
+            }
+          }
+          umma_commit(&b_free[st]);
         }
-        umma_commit(&br.s[b]);
-      };
-      mbar_wait(br.first, 0);
-      issue_sp(0);
-      for (int j = 0; j < nk; ++j) {
-        const int st = j % BW_STAGES, b = j & 1;
-        if (j + 1 < nk) issue_sp(j + 1);
-        mbar_wait(&br.p[b], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t ka = smem_u32(smem + DQ_RING + st * 2 * TILEB);
-#pragma unroll
-        for (int k = 0; k < BB / 16; ++k)  // K = 32 keys, 16 per MMA; B = K_j as the MN-major (key rows) operand
-          fa_umma_ts(tmem + T_A0, tmem + T_S + b * BB + k * 8, sdesc_sw128(ka + k * 2048, 8192, 1024), IDESC_AC,
-                     (j | k) != 0);
-        umma_commit(&br.free_[st]);
+        umma_commit(b_done);
+        umma_commit(&b_ffree[fb]);
       }
-      umma_commit(br.done);
     }
   } else {
-    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 16-key half of a block
-    const int lr = q * 32 + lane;  // query row
+    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 16-column half of a block
+    const int lr = q * 32 + lane;                 // key row (dK/dV) or query row (dQ)
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const int64_t zq = static_cast<int64_t>(z) * S + qb * 128 + lr;
-    const float mls = -__ldg(lse2 + zq), dq = __ldg(dvec + zq);
-    for (int j = 0; j < nk; ++j) {
-      const int b = j & 1;
-      mbar_wait(&br.s[b], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sv[16], pv[16];
-      fa_tmem_ld16(trow + T_S + b * BB + c * 16, sv);
-      fa_tmem_ld16(trow + T_P + b * BB + c * 16, pv);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      uint32_t dk[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float p0 = exp2f(fmaf(__uint_as_float(sv[2 * i]), sl2, mls));
-        const float p1 = exp2f(fmaf(__uint_as_float(sv[2 * i + 1]), sl2, mls));
-        dk[i] = fa_pack(sh.alpha * p0 * (__uint_as_float(pv[2 * i]) - dq),
-                        sh.alpha * p1 * (__uint_as_float(pv[2 * i + 1]) - dq));
+    uint32_t g = 0;
+    for (int it = 0; it < my_items; ++it) {
+      const int item = first_item + it * item_step;
+      const int z = item / per_z, blk = item % per_z;
+      const int row0 = (z / H) * S, head = z % H;
+      float mls = 0.f, dq = 0.f;
+      if (DQ) {
+        const int64_t zq = static_cast<int64_t>(z) * S + blk * 128 + lr;
+        mls = -__ldg(lse2 + zq);
+        dq = __ldg(dvec + zq);
       }
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // half 0 read before half 1 lands
-      fa_tmem_st8(trow + T_S + b * BB + c * 8, dk);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) fa_mbar_arrive(&br.p[b]);
+      for (int j = 0; j < nb; ++j, ++g) {
+        const int st = g % BW_STAGES, b = g & 1;
+        const float* vec = reinterpret_cast<const float*>(smem + BW_RING + st * BW_STAGE_STRIDE + 2 * TILEB);
+        if (!DQ) mbar_wait(&b_full[st], (g / BW_STAGES) & 1);  // lse2 / D of the stage (TMA-written)
+        mbar_wait(&b_s[b], (g >> 1) & 1);
+        tc_fence_after();
+        uint32_t sv[16], pv[16];
+        fa_tmem_ld16(trow + T_S + b * BB + c * 16, sv);
+        fa_tmem_ld16(trow + T_P + b * BB + c * 16, pv);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint32_t pk[8], dk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float m0 = mls, m1 = mls, d0 = dq, d1 = dq;
+          if (!DQ) {
+            const float2 ls = *reinterpret_cast<const float2*>(vec + c * 16 + 2 * i);
+            const float2 dd = *reinterpret_cast<const float2*>(vec + 32 + c * 16 + 2 * i);
+            m0 = -ls.x;
+            m1 = -ls.y;
+            d0 = dd.x;
+            d1 = dd.y;
+          }
+          const float p0 = exp2f(fmaf(__uint_as_float(sv[2 * i]), sl2, m0));
+          const float p1 = exp2f(fmaf(__uint_as_float(sv[2 * i + 1]), sl2, m1));
+          pk[i] = fa_pack(p0, p1);
+          dk[i] = fa_pack(sh.alpha * p0 * (__uint_as_float(pv[2 * i]) - d0),
+                          sh.alpha * p1 * (__uint_as_float(pv[2 * i + 1]) - d1));
+        }
+        // bf16 pairs: rows 16c + 2i, +1 -> column 8c + i of the buffer.  Half 1's pairs land
+        // in half 0's columns, so both warps of the quarter must have read theirs first.
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        if (!DQ) fa_tmem_st8(trow + T_S + b * BB + c * 8, pk);
+        fa_tmem_st8(trow + (DQ ? T_S : T_P) + b * BB + c * 8, dk);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) fa_mbar_arrive(&b_p[b]);
+      }
+      // the item's accumulators -> bf16 rows of dqkv, then hand them back to the MMA warp
+      mbar_wait(b_done, it & 1);
+      tc_fence_after();
+      const int64_t row = static_cast<int64_t>(row0) + blk * 128 + lr;
+      if (DQ) {
+        uint32_t v[32];
+        tmem_ld32(trow + T_A0 + c * 32, v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) fa_mbar_arrive(b_acc);
+        fa_store_row32(dqkv + row * ld_dqkv + head * FA_DH + c * 32, v);
+      } else {
+        // half-0 warps write dV, half-1 warps dK
+        const uint32_t src = trow + (c == 0 ? T_A0 : T_A1);
+        uint32_t v0[32], v1[32];
+        tmem_ld32(src, v0);
+        tmem_ld32(src + 32, v1);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) fa_mbar_arrive(b_acc);
+        bf16* dst = dqkv + row * ld_dqkv + (c == 0 ? 2 * d : d) + head * FA_DH;
+        fa_store_row32(dst, v0);
+        fa_store_row32(dst + 32, v1);
+      }
     }
-    mbar_wait(br.done, 0);
-    tc_fence_after();
-    const int64_t qrow = static_cast<int64_t>(row0) + qb * 128 + lr;
-    uint32_t v[32];
-    tmem_ld32(trow + T_A0 + c * 32, v);
-    fa_store_row32(dqkv + qrow * ld_dqkv + head * FA_DH + c * 32, v);
   }
   tc_fence_before();
   __syncthreads();
@@ -630,18 +566,18 @@ __device__ __forceinline__ void attn_bwd_dq(const CUtensorMap& m_q128, const CUt
   }
 }
 
-// One launch for both backward halves: CTAs [0, n) compute dK / dV per key block, CTAs
-// [n, 2n) dQ per query block -- the two kinds share SMs (two CTAs each) and one tail.
+// Persistent backward: CTAs [0, P) the dK/dV role, [P, 2P) the dQ role, each striding over its
+// n items.
 __global__ void __launch_bounds__(BW_THREADS, 2)
-    attn_bwd_kernel(const __grid_constant__ CUtensorMap m_qkv128, const __grid_constant__ CUtensorMap m_qkv64,
-                    const __grid_constant__ CUtensorMap m_do64, const __grid_constant__ CUtensorMap m_do128,
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap m_qkv128, const __grid_constant__ CUtensorMap m_qkvb,
+                    const __grid_constant__ CUtensorMap m_do128, const __grid_constant__ CUtensorMap m_dob,
                     const float* __restrict__ lse2, const float* __restrict__ dvec, bf16* __restrict__ dqkv,
-                    int64_t ld_dqkv, FaShape sh, int n) {
+                    int64_t ld_dqkv, FaShape sh, int n, int P) {
   const int b = static_cast<int>(blockIdx.x);
-  if (b < n)
-    attn_bwd_dkdv(m_qkv128, m_qkv64, m_do64, lse2, dvec, dqkv, ld_dqkv, sh, b);
+  if (b < P)
+    attn_bwd_role<false>(m_qkv128, m_qkvb, m_do128, m_dob, lse2, dvec, dqkv, ld_dqkv, sh, b, P, n);
   else
-    attn_bwd_dq(m_qkv128, m_do128, m_qkv64, lse2, dvec, dqkv, ld_dqkv, sh, b - n);
+    attn_bwd_role<true>(m_qkv128, m_qkvb, m_do128, m_dob, lse2, dvec, dqkv, ld_dqkv, sh, b - P, P, n);
 }
 
 }  // namespace tc
@@ -706,15 +642,18 @@ int gpp_flash_attn_bwd(const void* qkv, const float* lse2, const void* o, int64_
   if ((rc = tc::make_map_bf16(&mdo64, dout, d, T, lddo, 64, tc::BB))) return rc;
   if ((rc = tc::make_map_bf16(&mdo128, dout, d, T, lddo, 64, 128))) return rc;
   static bool attr = false;
-  constexpr int SMEM_BW = tc::SMEM_DKDV > tc::SMEM_DQ ? tc::SMEM_DKDV : tc::SMEM_DQ;
   if (!attr) {
-    cudaFuncSetAttribute(tc::attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BW);
+    cudaFuncSetAttribute(tc::attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BW);
     attr = true;
   }
   tc::FaShape sh{static_cast<int>(S), static_cast<int>(d), static_cast<int>(H), scale};
   const int n = static_cast<int>(Z * (S / 128));
-  tc::attn_bwd_kernel<<<static_cast<unsigned>(2 * n), tc::BW_THREADS, SMEM_BW, s>>>(
-      mk128, mq64, mdo64, mdo128, lse2, dvec, static_cast<bf16*>(dqkv), 3 * d, sh, n);
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int P = std::min(n, sms > 0 ? sms : 148);  // one CTA of each role per SM
+  tc::attn_bwd_kernel<<<static_cast<unsigned>(2 * P), tc::BW_THREADS, tc::SMEM_BW, s>>>(
+      mk128, mq64, mdo128, mdo64, lse2, dvec, static_cast<bf16*>(dqkv), 3 * d, sh, n, P);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
