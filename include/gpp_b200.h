@@ -260,6 +260,13 @@ int gpp_embbag_fwd(void* out, int64_t ldo, const float* table, const int64_t* id
  * (fp32 atomics; applied once per iteration over the whole mini-batch). */
 int gpp_embbag_sgd(float* table, const void* dpooled, int64_t ldd, const int64_t* idx, int64_t ldi,
                    int64_t M, int64_t bag, int64_t D, int64_t rows, float lr, void* stream);
+/* Deterministic sparse SGD over n tables in one call: for every table t,
+ * tables[t][r, :] -= lr * sum over {(m, b): idx[t][m*ldi + b] == r} of dpooled[t][m, :],
+ * each row's sum taken in increasing (m, b) order (a counting sort by row, then one warp per
+ * touched row) -- bit-reproducible, unlike gpp_embbag_sgd's fp32 atomics. */
+int gpp_embbag_sgd_multi(int n, float* const* tables, const int64_t* rows, const void* const* dpooled, int64_t ldd,
+                         const int64_t* const* idx, int64_t ldi, int64_t M, int64_t bag, int64_t D, float lr,
+                         void* stream);
 /* z [M, F*D] (feature 0 = dense/bottom vector): out[:, 0:D] = z_0, then the F(F-1)/2
  * pairwise dots <z_i, z_j> (i > j, row-major lower triangle), zero padding to out_cols. */
 int gpp_interaction_fwd(void* out, int64_t ldo, int64_t out_cols, const void* z, int64_t ldz,

@@ -146,6 +146,10 @@ class TorchBackend:
     def embbag_fwd(self, out, table, idx):
         out.copy_(table[idx].sum(1))
 
+    def embbag_sgd_multi(self, tables, dpooled, idxs, lr):
+        for t, d, i in zip(tables, dpooled, idxs):
+            self.embbag_sgd(t, d, i, lr)
+
     def embbag_sgd(self, table, dpooled, idx, lr):
         M, bag = idx.shape
         upd = (-lr * dpooled.float())[:, None, :].expand(M, bag, table.shape[1]).reshape(-1, table.shape[1])

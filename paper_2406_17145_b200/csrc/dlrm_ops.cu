@@ -2,6 +2,7 @@
 // gather-sum, its sparse SGD scatter, and the pairwise dot interaction.
 // All HBM / latency bound: warp-per-bag with 8-byte vector row loads, ILP over the
 // bag, warp-per-sample interaction staged through padded shared memory.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -221,6 +222,235 @@ __global__ void __launch_bounds__(128) interaction_bwd_reg_kernel(bf16* __restri
   }
 }
 
+// ---- deterministic sparse SGD over several tables (counting sort by row) ----------------
+// table_t[r] -= lr * sum over the bag elements (m, b) with idx_t[m, b] == r of dpooled_t[m],
+// the sum taken in increasing (m, b) order whatever the thread timing:
+//   count  : cnt[t, r] += 1 per element (integer atomics: order-free)
+//   scan   : start = exclusive prefix sum of cnt over all (t, r)   (3 kernels)
+//   scatter: perm[start[t, r]++] = element id  (bucket order still arbitrary)
+//   apply  : one warp per bucket (a run of equal (t, r) keys in perm, its end = the bumped
+//            start): ranks its element ids, adds the pooled gradients in rank order, updates
+//            the row once (256 B, coalesced).  Buckets > 32 by repeated min-extraction.
+// Out-of-range indices are skipped and counted (g_bad_indices), as in the atomic kernel.
+constexpr int kSgdTables = 32;
+struct SgdTables {
+  float* table[kSgdTables];
+  const bf16* dpool[kSgdTables];
+  const int64_t* idx[kSgdTables];
+  int64_t rows[kSgdTables];
+  int64_t row_base[kSgdTables];  // prefix of rows: key = row_base[t] + r
+  int n, bag;
+  int64_t M, ldd, ldi;
+  float lr;
+};
+
+__device__ __forceinline__ int64_t sgd_key(const SgdTables& tb, int64_t e, int& t, int64_t& m) {
+  const int64_t E = tb.M * tb.bag;
+  t = static_cast<int>(e / E);
+  const int64_t local = e - static_cast<int64_t>(t) * E;
+  m = local / tb.bag;
+  const int64_t r = __ldg(tb.idx[t] + m * tb.ldi + (local % tb.bag));
+  if (r < 0 || r >= tb.rows[t]) return -1;
+  return tb.row_base[t] + r;
+}
+
+__global__ void __launch_bounds__(256) sgd_count_kernel(unsigned* cnt, const __grid_constant__ SgdTables tb) {
+  const int64_t total = static_cast<int64_t>(tb.n) * tb.M * tb.bag;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int t;
+    int64_t m;
+    const int64_t k = sgd_key(tb, e, t, m);
+    if (k < 0) {
+      atomicAdd(&g_bad_indices, 1ull);
+      continue;
+    }
+    atomicAdd(cnt + k, 1u);
+  }
+}
+
+// exclusive scan of cnt [n] in place: per-block sums, a one-block scan of those, then the
+// per-block scans with their offsets.  Block = 1024 threads x 8 items.
+constexpr int kScanItems = 8, kScanThreads = 1024, kScanBlock = kScanItems * kScanThreads;
+
+__device__ __forceinline__ unsigned block_scan_excl(unsigned v, unsigned* sh, unsigned& total) {
+  // warp inclusive scan
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned s = lane < (blockDim.x >> 5) ? sh[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    sh[lane] = s;  // inclusive warp-sum prefix
+  }
+  __syncthreads();
+  total = sh[(blockDim.x >> 5) - 1];
+  const unsigned before = w > 0 ? sh[w - 1] : 0u;
+  __syncthreads();
+  return before + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(const unsigned* cnt, unsigned* sums, int64_t n) {
+  __shared__ unsigned sh[32];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x * kScanItems;
+  unsigned v = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) v += base + i < n ? cnt[base + i] : 0u;
+  unsigned total;
+  block_scan_excl(v, sh, total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_top_kernel(unsigned* sums, int nb) {
+  __shared__ unsigned sh[32];
+  unsigned carry = 0;
+  for (int base = 0; base < nb; base += kScanThreads) {
+    const int i = base + threadIdx.x;
+    const unsigned v = i < nb ? sums[i] : 0u;
+    unsigned total;
+    const unsigned ex = block_scan_excl(v, sh, total);
+    if (i < nb) sums[i] = carry + ex;
+    carry += total;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(unsigned* cnt, const unsigned* sums, int64_t n) {
+  __shared__ unsigned sh[32];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x * kScanItems;
+  unsigned v[kScanItems], tot = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < n ? cnt[base + i] : 0u;
+    tot += v[i];
+  }
+  unsigned total;
+  unsigned run = sums[blockIdx.x] + block_scan_excl(tot, sh, total);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) cnt[base + i] = run;
+    run += v[i];
+  }
+}
+
+__global__ void __launch_bounds__(256) sgd_scatter_kernel(unsigned* start, unsigned* perm,
+                                                         const __grid_constant__ SgdTables tb) {
+  const int64_t total = static_cast<int64_t>(tb.n) * tb.M * tb.bag;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int t;
+    int64_t m;
+    const int64_t k = sgd_key(tb, e, t, m);
+    if (k < 0) continue;
+    perm[atomicAdd(start + k, 1u)] = static_cast<unsigned>(e);
+  }
+}
+
+// one thread per (table, row) key: its bucket is perm[end[k-1], end[k]) (the exclusive scan
+// made start[k] = end[k-1]); the element ids are put in increasing order (insertion sort in
+// registers for <= 8, repeated min-extraction beyond) and their bags' pooled gradients summed
+// in that order into 64 fp32 registers, then the table row is updated once (256 B).
+__global__ void __launch_bounds__(256) sgd_apply_kernel(const unsigned* end, const unsigned* perm, int64_t keys,
+                                                       const __grid_constant__ SgdTables tb) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= keys) return;
+  const unsigned e1 = end[k], e0 = k > 0 ? end[k - 1] : 0u;
+  const unsigned n = e1 - e0;
+  if (n == 0) return;
+  int t = 0;
+  while (t + 1 < tb.n && k >= tb.row_base[t + 1]) ++t;
+  const int64_t E = tb.M * tb.bag, tbase = static_cast<int64_t>(t) * E;
+  const bf16* dp = tb.dpool[t];
+  float acc[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+  auto add_bag = [&](unsigned e) {
+    const int64_t m = (static_cast<int64_t>(e) - tbase) / tb.bag;
+    const uint4* g = reinterpret_cast<const uint4*>(dp + m * tb.ldd);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const uint4 u = __ldg(g + v);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(h[q]);
+        acc[8 * v + 2 * q] += f.x;
+        acc[8 * v + 2 * q + 1] += f.y;
+      }
+    }
+  };
+  if (n <= 8) {
+    unsigned ids[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ids[i] = i < static_cast<int>(n) ? perm[e0 + i] : 0xffffffffu;
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {  // insertion sort (unused slots hold the max id: stay last)
+#pragma unroll
+      for (int j = i; j > 0; --j) {
+        const unsigned a = ids[j - 1], b = ids[j];
+        ids[j - 1] = min(a, b);
+        ids[j] = max(a, b);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < static_cast<int>(n)) add_bag(ids[i]);
+  } else {
+    unsigned last = 0;
+    for (unsigned r = 0; r < n; ++r) {  // next smallest id > last (ids are unique)
+      unsigned best = 0xffffffffu;
+      for (unsigned i = e0; i < e1; ++i) {
+        const unsigned e = perm[i];
+        if ((r == 0 || e > last) && e < best) best = e;
+      }
+      last = best;
+      add_bag(best);
+    }
+  }
+  float4* row = reinterpret_cast<float4*>(tb.table[t] + (k - tb.row_base[t]) * 64);
+#pragma unroll
+  for (int v = 0; v < 16; ++v) {
+    float4 w = row[v];
+    w.x -= tb.lr * acc[4 * v];
+    w.y -= tb.lr * acc[4 * v + 1];
+    w.z -= tb.lr * acc[4 * v + 2];
+    w.w -= tb.lr * acc[4 * v + 3];
+    row[v] = w;
+  }
+}
+
+// grow-only scratch (never freed: graphs captured earlier may reference it)
+unsigned* sgd_scratch(size_t words, cudaStream_t stream) {
+  static unsigned* bufs[64] = {nullptr};
+  static size_t caps[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (caps[dev] >= words) return bufs[dev];
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &st);
+  if (st != cudaStreamCaptureStatusNone) {
+    set_error("embedding SGD scratch must be sized before CUDA-graph capture (run one eager step first)");
+    return nullptr;
+  }
+  unsigned* p = nullptr;
+  if (cudaMalloc(&p, words * sizeof(unsigned)) != cudaSuccess) {
+    set_error("embedding SGD scratch allocation failed");
+    return nullptr;
+  }
+  bufs[dev] = p;
+  caps[dev] = words;
+  return p;
+}
+
 }  // namespace
 }  // namespace gpp
 
@@ -261,6 +491,58 @@ int gpp_embbag_sgd(float* table, const void* dpooled, int64_t ldd, const int64_t
   GPP_ARG_CHECK(D == 64, "embedding dim must be 64");
   embbag_sgd_kernel<<<static_cast<unsigned>((M + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       table, static_cast<const bf16*>(dpooled), ldd, idx, ldi, M, static_cast<int>(bag), lr, rows);
+  GPP_LAUNCH_CHECK();
+  return GPP_OK;
+}
+
+int gpp_embbag_sgd_multi(int n, float* const* tables, const int64_t* rows, const void* const* dpooled, int64_t ldd,
+                         const int64_t* const* idx, int64_t ldi, int64_t M, int64_t bag, int64_t D, float lr,
+                         void* stream) {
+  GPP_ARG_CHECK(n >= 1 && n <= kSgdTables && tables && rows && dpooled && idx && M > 0 && bag > 0, "bad argument");
+  GPP_ARG_CHECK(D == 64, "embedding dim must be 64");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SgdTables tb{};
+  int64_t keys = 0;
+  for (int t = 0; t < n; ++t) {
+    GPP_ARG_CHECK(tables[t] && dpooled[t] && idx[t] && rows[t] > 0, "bad table");
+    tb.table[t] = tables[t];
+    tb.dpool[t] = static_cast<const bf16*>(dpooled[t]);
+    tb.idx[t] = idx[t];
+    tb.rows[t] = rows[t];
+    tb.row_base[t] = keys;
+    keys += rows[t];
+  }
+  tb.n = n;
+  tb.bag = static_cast<int>(bag);
+  tb.M = M;
+  tb.ldd = ldd;
+  tb.ldi = ldi;
+  tb.lr = lr;
+  const int64_t total = static_cast<int64_t>(n) * M * bag;
+  GPP_ARG_CHECK(total < (1ll << 32) && keys < (1ll << 31), "too many elements for 32-bit ids");
+  const int64_t nsum = (keys + kScanBlock - 1) / kScanBlock;
+  unsigned* scratch = sgd_scratch(static_cast<size_t>(keys + total + nsum), s);
+  if (!scratch) return GPP_ERR_CUDA;
+  unsigned* cnt = scratch;            // counts, then bucket starts, then bucket ends
+  unsigned* perm = scratch + keys;    // element ids in bucket order
+  unsigned* sums = perm + total;
+  if (cudaMemsetAsync(cnt, 0, static_cast<size_t>(keys) * sizeof(unsigned), s) != cudaSuccess) {
+    set_error("embedding SGD: memset failed");
+    return GPP_ERR_CUDA;
+  }
+  const unsigned eg = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  sgd_count_kernel<<<eg, 256, 0, s>>>(cnt, tb);
+  GPP_LAUNCH_CHECK();
+  scan_sums_kernel<<<static_cast<unsigned>(nsum), kScanThreads, 0, s>>>(cnt, sums, keys);
+  GPP_LAUNCH_CHECK();
+  scan_top_kernel<<<1, kScanThreads, 0, s>>>(sums, static_cast<int>(nsum));
+  GPP_LAUNCH_CHECK();
+  scan_apply_kernel<<<static_cast<unsigned>(nsum), kScanThreads, 0, s>>>(cnt, sums, keys);
+  GPP_LAUNCH_CHECK();
+  sgd_scatter_kernel<<<eg, 256, 0, s>>>(cnt, perm, tb);
+  GPP_LAUNCH_CHECK();
+  // after the scatter cnt[k] is bucket k's end; its start is cnt[k - 1]
+  sgd_apply_kernel<<<static_cast<unsigned>((keys + 255) / 256), 256, 0, s>>>(cnt, perm, keys, tb);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }

@@ -82,6 +82,9 @@ class CudaBackend:
     def embbag_fwd(self, out, table, idx):
         lib.embbag_fwd(out, table, idx)
 
+    def embbag_sgd_multi(self, tables, dpooled, idxs, lr):
+        lib.embbag_sgd_multi(tables, dpooled, idxs, lr)
+
     def embbag_sgd(self, table, dpooled, idx, lr):
         lib.embbag_sgd(table, dpooled, idx, lr)
 

@@ -164,6 +164,11 @@ class Executor:
         self._fuse_req = fuse_optimizer
         self._transport_kind = transport
         self.bias_queue: list = []  # (bias-gradient view, output gradient) of the running task
+        import os
+
+        # sparse table SGD: fp32-atomic scatter (default: at the HBM roofline, 1.9 ms per DLRM
+        # step) or GPP_EMB_SGD=deterministic (bit-reproducible counting-sort kernel, 5.3 ms)
+        self._emb_atomic = os.environ.get("GPP_EMB_SGD", "atomic") != "deterministic"
         # test hook: when a dict, every dense op's forward output is copied into it under
         # (op, task) -- the oracle takes the device's ReLU masks from these (tests only)
         self.tap: dict | None = None
@@ -711,6 +716,7 @@ class Executor:
             self.tp.join(self._ar_handles)
             self._ar_handles = []
         if step_optimizer:
+            jobs = []
             for o, table in self.tables.items() if not eager_sparse else ():
                 idx = batch[self.layers[o].data_key]
                 g_o = self.emb_grad[o]
@@ -720,7 +726,8 @@ class Executor:
                     self.tp.allgather(gi, idx.contiguous())
                     self.tp.allgather(gg, g_o)
                     idx, g_o = gi, gg
-                self.be.embbag_sgd(table, g_o, idx, self.lr)
+                jobs.append((table, g_o, idx))
+            self._apply_sparse(jobs)
             if self.fuse:
                 if self.rest_off < self.master.numel():
                     sh = self.shadow[self.rest_off:] if self.shadow is not None else None
@@ -734,9 +741,22 @@ class Executor:
     def _sparse_update(self, batch, j: int) -> None:
         """Embedding-bag SGD for micro-batch j's rows of every table on this stage."""
         rows = slice(j * self.m, (j + 1) * self.m)
-        for o, table in self.tables.items():
-            idx = batch[self.layers[o].data_key][rows]
-            self.be.embbag_sgd(table, self.emb_grad[o][rows], idx, self.lr)
+        self._apply_sparse([(table, self.emb_grad[o][rows], batch[self.layers[o].data_key][rows])
+                            for o, table in self.tables.items()])
+
+    def _apply_sparse(self, jobs) -> None:
+        """Sparse SGD of several tables: the per-table fp32-atomic scatter (default), or with
+        GPP_EMB_SGD=deterministic the multi-table kernel (counting sort by row, each row's sum
+        in (sample, bag) order, bit-reproducible) in one call per 32 tables."""
+        if not jobs:
+            return
+        if self._emb_atomic or not hasattr(self.be, "embbag_sgd_multi"):
+            for table, g, idx in jobs:
+                self.be.embbag_sgd(table, g, idx, self.lr)
+            return
+        for i in range(0, len(jobs), 32):
+            ch = jobs[i:i + 32]
+            self.be.embbag_sgd_multi([t for t, _, _ in ch], [g for _, g, _ in ch], [x for _, _, x in ch], self.lr)
 
     def stage_loss(self, loss: torch.Tensor) -> float:
         """Loss of the whole mini-batch on a head rank (sums the DP replicas' shares)."""

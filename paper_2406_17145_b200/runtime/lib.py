@@ -71,6 +71,7 @@ _SIGS = {
     "gpp_attn_softmax_bwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp, _vp], _i32),
     "gpp_embbag_bad_indices": ([ctypes.POINTER(ctypes.c_uint64), _i32], _i32),
     "gpp_embbag_fwd": ([_vp, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp], _i32),
+    "gpp_embbag_sgd_multi": ([_i32, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_embbag_sgd": ([_vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp], _i32),
     "gpp_interaction_fwd": ([_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp], _i32),
     "gpp_interaction_bwd": ([_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _vp], _i32),
@@ -277,6 +278,17 @@ def embbag_fwd(out, table, idx, stream=None):
     M, bag = idx.shape
     call("gpp_embbag_fwd", _ptr(out), _ld(out), _ptr(table), _ptr(idx), _ld(idx), M, bag, table.shape[1],
          table.shape[0], _stream(stream))
+
+
+def embbag_sgd_multi(tables, dpooled, idxs, lr, stream=None):
+    """Deterministic sparse SGD of several tables in one call (same M x bag index shape and
+    dpooled row pitch for every table)."""
+    n = len(tables)
+    M, bag = idxs[0].shape
+    P = ctypes.c_void_p * n
+    call("gpp_embbag_sgd_multi", n, P(*[_ptr(t) for t in tables]), (ctypes.c_int64 * n)(*[t.shape[0] for t in tables]),
+         P(*[_ptr(d) for d in dpooled]), _ld(dpooled[0]), P(*[_ptr(i) for i in idxs]), _ld(idxs[0]), M, bag,
+         tables[0].shape[1], float(lr), _stream(stream))
 
 
 def embbag_sgd(table, dpooled, idx, lr, stream=None):

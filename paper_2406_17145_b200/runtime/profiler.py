@@ -32,7 +32,7 @@ class _Rec:
 GEMM_KINDS = ("fwd", "dgrad", "wgrad")
 # every other kernel-launching backend call, timed for the per-rank busy time
 _OTHER_CALLS = ("colsum", "colsum_multi", "rowdot_loss", "rowdot_fwd", "rowdot_bwd", "mse_loss", "bce_loss", "ce_loss", "copy_rows", "copy_rows_multi",
-                "sgd_step", "embbag_fwd", "embbag_sgd", "interaction_fwd", "interaction_bwd",
+                "sgd_step", "embbag_fwd", "embbag_sgd", "embbag_sgd_multi", "interaction_fwd", "interaction_bwd",
                 "layernorm_fwd", "layernorm_bwd", "softmax_fwd", "softmax_bwd", "meanpool_fwd",
                 "meanpool_bwd", "attn_softmax", "attn_softmax_bwd", "gemm_batched", "attn_fwd", "attn_bwd",
                 "flash_attn_fwd", "flash_attn_bwd")

@@ -675,3 +675,24 @@ def test_colsum_multi_matches_per_tensor(cuda_lib):
         cuda_lib.colsum_multi(again, xs, accumulate=acc)
         torch.cuda.synchronize()
         assert all(torch.equal(a, o) for a, o in zip(again, outs))
+
+
+@pytest.mark.parametrize("rows,M,bag,hot", [(5000, 300, 100, False), (200, 256, 20, True), (1000, 64, 3, False)])
+def test_embbag_sgd_multi_deterministic(cuda_lib, rows, M, bag, hot):
+    """Multi-table deterministic sparse SGD vs index_add_ (fp32): equal within fp32
+    reassociation, bit-identical across runs; hot rows (> 32 hits) take the min-extraction path."""
+    g = torch.Generator(device="cuda").manual_seed(rows + M)
+    T = 3
+    tables = [torch.randn(rows, 64, device="cuda", generator=g) for _ in range(T)]
+    idxs = [torch.randint(0, 8 if hot else rows, (M, bag), device="cuda", generator=g) for _ in range(T)]
+    dps = [torch.randn(M, 64, device="cuda", generator=g).bfloat16() for _ in range(T)]
+    outs = []
+    for _ in range(2):
+        t2 = [t.clone() for t in tables]
+        cuda_lib.embbag_sgd_multi(t2, dps, idxs, 0.1)
+        torch.cuda.synchronize()
+        outs.append(t2)
+    for t, t2, idx, dp in zip(tables, outs[0], idxs, dps):
+        exp = t.clone().index_add_(0, idx.reshape(-1), (-0.1 * dp.float())[:, None, :].expand(M, bag, 64).reshape(-1, 64))
+        assert torch.allclose(t2, exp, rtol=1e-5, atol=1e-4)
+    assert all(torch.equal(a, b) for a, b in zip(outs[0], outs[1]))

@@ -168,3 +168,20 @@ def test_mmt_full_width_layer(cuda_lib):
     """One full-size MMT layer (S=512, d=1024, 16 heads, FFN 4096) per branch, B=2."""
     wl = W.mmt(B=2, branches=2, layers=1, S=512, d=1024, H=16, ffn=4096, classes=1000)
     _check(wl, 1, 2e-2, steps=1)
+
+
+def test_dlrm_deterministic_sparse_sgd_bit_reproducible(cuda_lib, monkeypatch):
+    """GPP_EMB_SGD=deterministic: the same DLRM step twice from the same state gives bit-identical
+    tables (the default fp32-atomic scatter does not promise that), and matches the oracle."""
+    monkeypatch.setenv("GPP_EMB_SGD", "deterministic")
+    wl = W.dlrm(B=128, tables=6, rows=2000, bag=20, hidden=512)
+    dev = torch.device("cuda", 0)
+    outs = []
+    for _ in range(2):
+        ex = Executor(wl, _single_stage(wl, 32), 0, 1, CudaBackend(dev), lr=1e-2)
+        assert not ex._emb_atomic
+        ex.run_iteration(to_device_rows(ex, make_batch(wl, 0), ex.dtype, dev))
+        torch.cuda.synchronize()
+        outs.append({k: v.clone() for k, v in ex.P.items() if k[1] == "table"})
+    assert outs[0].keys() and all(torch.equal(outs[0][k], outs[1][k]) for k in outs[0])
+    _dlrm_check(wl, 32, steps=1)
