@@ -9,17 +9,19 @@
 //           lse2 = alpha log2e max + log2(sum),   P = exp2(alpha log2e s - lse2).
 //   attn_bwd_prep_kernel: D[q] = rowsum(dO o O) per (z, query) -- the FlashAttention
 //       identity rowsum(P o dP) = rowsum(dO o O).
-//   attn_bwd_dkdv_kernel: one CTA per (z, 128-key block), looping over 64-query blocks:
-//       S^T = K Q^T and dP^T = V dO^T in TMEM (lane = key); the epilogue warps recompute
-//       P^T = exp2(alpha log2e s - lse2[q]) and dS^T = alpha P^T o (dP^T - D[q]) and write both
-//       as bf16 pairs back over the consumed columns -- the TMEM A operands of
+//   attn_bwd_kernel     : ONE persistent launch, two CTA roles (one CTA of each per SM).
+//       dK/dV role, items (z, 128-key block), looping over 32-query blocks: S^T = K Q^T and
+//       dP^T = V dO^T in TMEM (lane = key); the softmax warps recompute
+//       P^T = exp2(alpha log2e s - lse2[q]) and dS^T = alpha P^T o (dP^T - D[q]) and write
+//       both as bf16 pairs back over the consumed columns -- the TMEM A operands of
 //       dV += P^T dO and dK += dS^T Q, accumulated in TMEM over every query block.
-//   attn_bwd_dq_kernel  : one CTA per (z, 128-query block), looping over 64-key blocks:
-//       S, dP recomputed (lane = query, lse2 / D are row constants), dS in place in TMEM,
-//       dQ += dS K.  (A single kernel reducing per-key-block dQ partials across a CTA
-//       cluster through DSMEM measured 363 us vs 149 us without the exchange: the exchange
-//       serialised the cluster; the recompute of S and dP here costs less.)
-//   Both hold 256 TMEM columns, so two CTAs share an SM and overlap their phases.
+//       dQ role, items (z, 128-query block), looping over 32-key blocks: S, dP recomputed
+//       (lane = query, lse2 / D row constants), dS in place, dQ += dS K.
+//       S / dP TMEM tiles double-buffered (block j+1's MMAs overlap block j's softmax), the
+//       32 KB first tiles double-buffered across items, 256 TMEM columns per CTA.
+//       (A single kernel reducing per-key-block dQ partials across a 4-CTA cluster through
+//       DSMEM measured 363 us vs 149 us without the exchange -- the owner-CTA reductions
+//       serialised the cluster; recomputing S and dP in the dQ role costs less.)
 //
 // Layout: packed QKV [m S, 3d] (Q | K | V, head h at columns h*64), o / dout [m S, d]
 // head-interleaved, lse2 / D [Z, S] fp32 with z = sample * H + head.
