@@ -219,29 +219,32 @@ __global__ void __launch_bounds__(256) ln_fwd_vec_kernel(bf16* __restrict__ y, f
   }
 }
 
-// ---- LayerNorm, 16-byte vectors, two rows per warp (D % 256 == 0) -----------------------
-// Both rows' loads are issued before any reduction, so each warp keeps 2 x D x 2 B in
-// flight (the one-row kernel above was latency-bound: ~12 us for 32 MB at T=8192, D=1024).
-template <int PER>
-__global__ void __launch_bounds__(256) ln_fwd_vec2_kernel(bf16* __restrict__ y, float* __restrict__ mean,
-                                                          float* __restrict__ rstd, const bf16* __restrict__ x,
-                                                          const float* __restrict__ g, const float* __restrict__ b,
-                                                          int64_t T, int D, float eps) {
+// ---- LayerNorm, 16-byte vectors, R rows per warp (D % 256 == 0) ---------------------------
+// All R rows' loads are issued before any reduction.  At T = 8192, D = 1024 with R = 4 the
+// 256 blocks fit in one wave (two per SM) with the whole 16.8 MB input in flight; R = 2 left
+// 512 blocks at 3 per SM = 1.15 waves (13 us cold, 1.3 TB/s).
+template <int PER, int R>
+__global__ void __launch_bounds__(256, R >= 4 ? 2 : 3) ln_fwd_vec2_kernel(bf16* __restrict__ y, float* __restrict__ mean,
+                                                                       float* __restrict__ rstd,
+                                                                       const bf16* __restrict__ x,
+                                                                       const float* __restrict__ g,
+                                                                       const float* __restrict__ b, int64_t T, int D,
+                                                                       float eps) {
   constexpr int NV = PER / 8;
-  const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5)) * 2;
+  const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5)) * R;
   const int lane = threadIdx.x & 31;
   if (r0 >= T) return;
-  const bool two = r0 + 1 < T;
-  uint4 raw[2][NV];
+  uint4 raw[R][NV];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) raw[0][i] = __ldg(reinterpret_cast<const uint4*>(x + r0 * D) + lane + 32 * i);
-  if (two) {
+  for (int k = 0; k < R; ++k) {
+    if (r0 + k < T) {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) raw[1][i] = __ldg(reinterpret_cast<const uint4*>(x + (r0 + 1) * D) + lane + 32 * i);
+      for (int i = 0; i < NV; ++i) raw[k][i] = __ldg(reinterpret_cast<const uint4*>(x + (r0 + k) * D) + lane + 32 * i);
+    }
   }
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    if (k == 1 && !two) break;
+  for (int k = 0; k < R; ++k) {
+    if (r0 + k >= T) break;
     const int64_t r = r0 + k;
     float v[PER];
 #pragma unroll
@@ -531,12 +534,12 @@ int gpp_layernorm_fwd(void* y, float* mean, float* rstd, const void* x, const fl
     case 128: ln_fwd_kernel<4><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
     case 256: ln_fwd_vec_kernel<8><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
     case 512:
-      ln_fwd_vec2_kernel<16><<<static_cast<unsigned>((T + 15) / 16), 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd,
-                                                                                  static_cast<const bf16*>(x), gamma, beta, T, d, eps);
+      ln_fwd_vec2_kernel<16, 4><<<static_cast<unsigned>((T + 31) / 32), 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd,
+                                                                                     static_cast<const bf16*>(x), gamma, beta, T, d, eps);
       break;
     case 1024:
-      ln_fwd_vec2_kernel<32><<<static_cast<unsigned>((T + 15) / 16), 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd,
-                                                                                  static_cast<const bf16*>(x), gamma, beta, T, d, eps);
+      ln_fwd_vec2_kernel<32, 4><<<static_cast<unsigned>((T + 31) / 32), 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd,
+                                                                                     static_cast<const bf16*>(x), gamma, beta, T, d, eps);
       break;
     default: set_error("layernorm: D must be 128/256/512/1024"); return GPP_ERR_UNSUPPORTED;
   }
@@ -559,7 +562,9 @@ int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, con
     // one row per warp.  Rows per block rounded up to the rows one pass of 8 warps covers.
     const int per_sm = D == 1024 ? 1 : 2, rows = D == 1024 ? 16 : 8;
     const int64_t nb0 = 148 * per_sm;
-    const int rpb = static_cast<int>(std::max<int64_t>(rows, ((T + nb0 - 1) / nb0 + rows - 1) / rows * rows));
+    // rows per block: ceil(T / (blocks per SM x SMs)) rounded to the 8 warps (T = 8192: 56 rows,
+    // 147 blocks; rounding to a whole 16-row pass left 20 SMs idle)
+    const int rpb = static_cast<int>(std::max<int64_t>(rows, ((T + nb0 - 1) / nb0 + 7) / 8 * 8));
     const int nblk = static_cast<int>((T + rpb - 1) / rpb);
     float* part = ln_scratch(static_cast<size_t>(nblk) * 2 * D, s);
     if (!part) return GPP_ERR_CUDA;
