@@ -12,11 +12,17 @@ CPU restatements used as oracles for the B200 stage executor:
 * ``brute``           — SPEC oracle module: min_inflight_search (Appendix A) and
                         exhaustive_optimize over convex partitions.
 
-Numerics parity is UNPINNED against the reference itself: the reference ships
-no runtime and no numerics; the torch-CPU model is
-the stated oracle.  Partitioner/scheduler parity IS pinned: the shipped
+* ``numpy_ref``       — an independent float64 numpy restatement of every workload's
+                        forward loss: the check on ``reference_model``.
+
+Partitioner/scheduler parity is pinned against the reference itself: the shipped
 reference modules (model/spgraph/cost) generate the golden fixtures under
-tests/golden/ (tests/golden/make_golden.py).
+tests/golden/ (tests/golden/make_golden.py).  Numerics cannot be pinned against the
+reference — it ships no runtime and no numerics — so
+the torch-CPU oracle is pinned instead (tests/test_oracle_pinning.py) against
+``numpy_ref`` (forward loss equal to 1e-11 on every layer kind), against central
+finite differences of that forward (every parameter tensor, float64), and its bf16
+rounding points against round-to-nearest-even.
 
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
 reference legs may import this package.
