@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#define GPP_PDL_CLASS 2  // programmatic-dependent-launch family: flash attention
 #include "gemm.cuh"
 #include "tc_ptx.cuh"
 
@@ -128,6 +129,8 @@ __global__ void __launch_bounds__(FW_THREADS, 2)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();  // qkv is the previous kernel's output
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -245,6 +248,8 @@ __global__ void __launch_bounds__(FW_THREADS, 2)
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(float* __restrict__ dvec, const bf16* __restrict__ o,
                                                             int64_t ldo, const bf16* __restrict__ dout, int64_t lddo,
                                                             int64_t T, int S, int H) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t t = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
   const int64_t pair = t >> 3;  // (row, head)
   const int part = static_cast<int>(t & 7);
@@ -396,6 +401,8 @@ __device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // prologue above overlaps the previous kernel's tail
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -617,8 +624,8 @@ int gpp_flash_attn_fwd(const void* qkv, float* lse2, void* o, int64_t ldo, int64
     attr = true;
   }
   tc::FaShape sh{static_cast<int>(S), static_cast<int>(d), static_cast<int>(H), scale};
-  tc::attn_fwd_lse_kernel<<<static_cast<unsigned>(Z * (S / 128)), tc::FW_THREADS, tc::SMEM_FWL,
-                            static_cast<cudaStream_t>(stream)>>>(mq, mk, mv, lse2, static_cast<bf16*>(o), ldo, sh);
+  launch_pdl(tc::attn_fwd_lse_kernel, dim3(static_cast<unsigned>(Z * (S / 128))), dim3(tc::FW_THREADS), tc::SMEM_FWL,
+             static_cast<cudaStream_t>(stream), mq, mk, mv, lse2, static_cast<bf16*>(o), ldo, sh);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -634,9 +641,9 @@ int gpp_flash_attn_bwd(const void* qkv, const float* lse2, const void* o, int64_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t T = m * S, Z = m * H;
   GPP_ARG_CHECK(ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(o) & 15) == 0, "16-byte aligned o");
-  tc::attn_bwd_prep_kernel<<<static_cast<unsigned>((T * H * 8 + 255) / 256), 256, 0, s>>>(
-      dvec, static_cast<const bf16*>(o), ldo, static_cast<const bf16*>(dout), lddo, T, static_cast<int>(S),
-      static_cast<int>(H));
+  launch_pdl(tc::attn_bwd_prep_kernel, dim3(static_cast<unsigned>((T * H * 8 + 255) / 256)), dim3(256), 0, s, dvec,
+             static_cast<const bf16*>(o), ldo, static_cast<const bf16*>(dout), lddo, T, static_cast<int>(S),
+             static_cast<int>(H));
   GPP_LAUNCH_CHECK();
   CUtensorMap mk128, mq64, mdo64, mdo128;  // qkv maps serve Q, K and V by coordinates
   if ((rc = tc::make_map_bf16(&mk128, qkv, 3 * d, T, 3 * d, 64, 128))) return rc;
@@ -654,8 +661,8 @@ int gpp_flash_attn_bwd(const void* qkv, const float* lse2, const void* o, int64_
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int P = std::min(n, sms > 0 ? sms : 148);  // one CTA of each role per SM
-  tc::attn_bwd_kernel<<<static_cast<unsigned>(2 * P), tc::BW_THREADS, tc::SMEM_BW, s>>>(
-      mk128, mq64, mdo128, mdo64, lse2, dvec, static_cast<bf16*>(dqkv), 3 * d, sh, n, P);
+  launch_pdl(tc::attn_bwd_kernel, dim3(static_cast<unsigned>(2 * P)), dim3(tc::BW_THREADS), tc::SMEM_BW, s, mk128,
+             mq64, mdo128, mdo64, lse2, dvec, static_cast<bf16*>(dqkv), 3 * d, sh, n, P);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }

@@ -66,4 +66,36 @@ __device__ __forceinline__ float act_bwd(float saved, int act) {
 
 inline int dtype_bytes(int dtype) { return dtype == GPP_BF16 ? 2 : 4; }
 
+// Programmatic dependent launch.  Kernels started by launch_pdl may begin while the
+// previous kernel of the stream drains (its CTAs have all issued pdl_trigger); they run
+// their prologue (barrier init, TMEM alloc, tensormap prefetch) and then block in
+// pdl_wait() until that kernel has completed and its writes are visible.  Every kernel
+// launched this way calls pdl_wait() before its first global access (and before any
+// early return), so completion stays transitive along the stream.  For a kernel launched
+// without the attribute both instructions are no-ops.  GPP_PDL (a bit mask over the kernel
+// families, GPP_PDL_CLASS of each translation unit; default all but 16) selects where it is used.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled(int family);
+#ifndef GPP_PDL_CLASS
+#define GPP_PDL_CLASS 0
+#endif
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_impl(int family, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                   cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled(family) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+#define launch_pdl(...) launch_pdl_impl(GPP_PDL_CLASS, __VA_ARGS__)
+
 }  // namespace gpp

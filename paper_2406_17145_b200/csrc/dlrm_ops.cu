@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#define GPP_PDL_CLASS 16  // programmatic-dependent-launch families: 16 embedding bags, 32 interaction, 64 sparse SGD
 #include "common.cuh"
 
 namespace gpp {
@@ -21,6 +22,8 @@ __global__ void __launch_bounds__(256) embbag_fwd_kernel(bf16* __restrict__ out,
                                                          const int64_t* __restrict__ idx,
                                                          int64_t ldi, int64_t M, int bag,
                                                          int64_t rows) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t m = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (m >= M) return;
@@ -63,6 +66,8 @@ __global__ void __launch_bounds__(256) embbag_sgd_kernel(float* __restrict__ tab
                                                          int64_t ldd, const int64_t* __restrict__ idx,
                                                          int64_t ldi, int64_t M, int bag, float lr,
                                                          int64_t rows) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t m = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (m >= M) return;
@@ -94,6 +99,8 @@ __global__ void __launch_bounds__(128) interaction_fwd_kernel(bf16* __restrict__
                                                               int64_t out_cols,
                                                               const bf16* __restrict__ z,
                                                               int64_t ldz, int64_t M, int F) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float zs[];  // 4 warps x F x ZLD
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = static_cast<int64_t>(blockIdx.x) * 4 + w;
@@ -134,6 +141,8 @@ __global__ void __launch_bounds__(128) interaction_bwd_kernel(bf16* __restrict__
                                                               const bf16* __restrict__ z,
                                                               int64_t ldz, int64_t M, int F,
                                                               int mask_first) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = static_cast<int64_t>(blockIdx.x) * 4 + w;
@@ -182,6 +191,8 @@ __global__ void __launch_bounds__(128) interaction_bwd_reg_kernel(bf16* __restri
                                                                   int64_t lddo,
                                                                   const bf16* __restrict__ z,
                                                                   int64_t ldz, int64_t M, int mask_first) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int P = F * (F - 1) / 2;
   __shared__ float dps[4][P + 1];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -255,6 +266,8 @@ __device__ __forceinline__ int64_t sgd_key(const SgdTables& tb, int64_t e, int& 
 }
 
 __global__ void __launch_bounds__(256) sgd_count_kernel(unsigned* cnt, const __grid_constant__ SgdTables tb) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = static_cast<int64_t>(tb.n) * tb.M * tb.bag;
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -301,6 +314,8 @@ __device__ __forceinline__ unsigned block_scan_excl(unsigned v, unsigned* sh, un
 }
 
 __global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(const unsigned* cnt, unsigned* sums, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned sh[32];
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x * kScanItems;
   unsigned v = 0;
@@ -312,6 +327,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(const unsigned*
 }
 
 __global__ void __launch_bounds__(kScanThreads) scan_top_kernel(unsigned* sums, int nb) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned sh[32];
   unsigned carry = 0;
   for (int base = 0; base < nb; base += kScanThreads) {
@@ -325,6 +342,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_top_kernel(unsigned* sums, 
 }
 
 __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(unsigned* cnt, const unsigned* sums, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned sh[32];
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x * kScanItems;
   unsigned v[kScanItems], tot = 0;
@@ -344,6 +363,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(unsigned* cnt,
 
 __global__ void __launch_bounds__(256) sgd_scatter_kernel(unsigned* start, unsigned* perm,
                                                          const __grid_constant__ SgdTables tb) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = static_cast<int64_t>(tb.n) * tb.M * tb.bag;
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -361,6 +382,8 @@ __global__ void __launch_bounds__(256) sgd_scatter_kernel(unsigned* start, unsig
 // in that order into 64 fp32 registers, then the table row is updated once (256 B).
 __global__ void __launch_bounds__(256) sgd_apply_kernel(const unsigned* end, const unsigned* perm, int64_t keys,
                                                        const __grid_constant__ SgdTables tb) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= keys) return;
   const unsigned e1 = end[k], e0 = k > 0 ? end[k - 1] : 0u;
@@ -479,8 +502,7 @@ int gpp_embbag_fwd(void* out, int64_t ldo, const float* table, const int64_t* id
   GPP_ARG_CHECK(out && table && idx && M > 0 && bag > 0, "bad argument");
   GPP_ARG_CHECK(D == 64, "embedding dim must be 64 (Appendix B DLRM)");
   GPP_ARG_CHECK((reinterpret_cast<uintptr_t>(table) & 7) == 0 && ldo % 2 == 0, "alignment");
-  embbag_fwd_kernel<<<static_cast<unsigned>((M + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<bf16*>(out), ldo, table, idx, ldi, M, static_cast<int>(bag), rows);
+  launch_pdl(embbag_fwd_kernel, dim3(static_cast<unsigned>((M + 7) / 8)), dim3(256), 0, static_cast<cudaStream_t>(stream), static_cast<bf16*>(out), ldo, table, idx, ldi, M, static_cast<int>(bag), rows);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -489,8 +511,7 @@ int gpp_embbag_sgd(float* table, const void* dpooled, int64_t ldd, const int64_t
                    int64_t M, int64_t bag, int64_t D, int64_t rows, float lr, void* stream) {
   GPP_ARG_CHECK(table && dpooled && idx && M > 0 && bag > 0, "bad argument");
   GPP_ARG_CHECK(D == 64, "embedding dim must be 64");
-  embbag_sgd_kernel<<<static_cast<unsigned>((M + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      table, static_cast<const bf16*>(dpooled), ldd, idx, ldi, M, static_cast<int>(bag), lr, rows);
+  launch_pdl(embbag_sgd_kernel, dim3(static_cast<unsigned>((M + 7) / 8)), dim3(256), 0, static_cast<cudaStream_t>(stream), table, static_cast<const bf16*>(dpooled), ldd, idx, ldi, M, static_cast<int>(bag), lr, rows);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -531,18 +552,18 @@ int gpp_embbag_sgd_multi(int n, float* const* tables, const int64_t* rows, const
     return GPP_ERR_CUDA;
   }
   const unsigned eg = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-  sgd_count_kernel<<<eg, 256, 0, s>>>(cnt, tb);
+  launch_pdl_impl(64, sgd_count_kernel, dim3(eg), dim3(256), 0, s, cnt, tb);
   GPP_LAUNCH_CHECK();
-  scan_sums_kernel<<<static_cast<unsigned>(nsum), kScanThreads, 0, s>>>(cnt, sums, keys);
+  launch_pdl_impl(64, scan_sums_kernel, dim3(static_cast<unsigned>(nsum)), dim3(kScanThreads), 0, s, cnt, sums, keys);
   GPP_LAUNCH_CHECK();
-  scan_top_kernel<<<1, kScanThreads, 0, s>>>(sums, static_cast<int>(nsum));
+  launch_pdl_impl(64, scan_top_kernel, dim3(1), dim3(kScanThreads), 0, s, sums, static_cast<int>(nsum));
   GPP_LAUNCH_CHECK();
-  scan_apply_kernel<<<static_cast<unsigned>(nsum), kScanThreads, 0, s>>>(cnt, sums, keys);
+  launch_pdl_impl(64, scan_apply_kernel, dim3(static_cast<unsigned>(nsum)), dim3(kScanThreads), 0, s, cnt, sums, keys);
   GPP_LAUNCH_CHECK();
-  sgd_scatter_kernel<<<eg, 256, 0, s>>>(cnt, perm, tb);
+  launch_pdl_impl(64, sgd_scatter_kernel, dim3(eg), dim3(256), 0, s, cnt, perm, tb);
   GPP_LAUNCH_CHECK();
   // after the scatter cnt[k] is bucket k's end; its start is cnt[k - 1]
-  sgd_apply_kernel<<<static_cast<unsigned>((keys + 255) / 256), 256, 0, s>>>(cnt, perm, keys, tb);
+  launch_pdl_impl(64, sgd_apply_kernel, dim3(static_cast<unsigned>((keys + 255) / 256)), dim3(256), 0, s, cnt, perm, keys, tb);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -552,8 +573,7 @@ int gpp_interaction_fwd(void* out, int64_t ldo, int64_t out_cols, const void* z,
   GPP_ARG_CHECK(out && z && M > 0 && F >= 2 && D == 64, "bad argument");
   GPP_ARG_CHECK(out_cols >= 64 + F * (F - 1) / 2 && out_cols <= ldo, "output too narrow");
   const size_t smem = 4 * F * ZLD * sizeof(float);
-  interaction_fwd_kernel<<<static_cast<unsigned>((M + 3) / 4), 128, smem, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<bf16*>(out), ldo, out_cols, static_cast<const bf16*>(z), ldz, M, static_cast<int>(F));
+  launch_pdl_impl(32, interaction_fwd_kernel, dim3(static_cast<unsigned>((M + 3) / 4)), dim3(128), smem, static_cast<cudaStream_t>(stream), static_cast<bf16*>(out), ldo, out_cols, static_cast<const bf16*>(z), ldz, M, static_cast<int>(F));
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -564,15 +584,13 @@ int gpp_interaction_bwd(void* dz, int64_t lddz, const void* dout, int64_t lddo, 
   // GPP_INTERACTION_GENERIC=1 forces the generic kernel (tests assert both are bit-identical)
   const char* gen = getenv("GPP_INTERACTION_GENERIC");
   if (F == 27 && !(gen && gen[0] == '1')) {  // DLRM: 26 tables + the bottom MLP
-    interaction_bwd_reg_kernel<27><<<static_cast<unsigned>((M + 3) / 4), 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<bf16*>(dz), lddz, static_cast<const bf16*>(dout), lddo, static_cast<const bf16*>(z), ldz, M,
+    launch_pdl_impl(32, interaction_bwd_reg_kernel<27>, dim3(static_cast<unsigned>((M + 3) / 4)), dim3(128), 0, static_cast<cudaStream_t>(stream), static_cast<bf16*>(dz), lddz, static_cast<const bf16*>(dout), lddo, static_cast<const bf16*>(z), ldz, M,
         mask_first);
     GPP_LAUNCH_CHECK();
     return GPP_OK;
   }
   const size_t smem = 4 * (F * ZLD + F * (F - 1) / 2 + 1) * sizeof(float);
-  interaction_bwd_kernel<<<static_cast<unsigned>((M + 3) / 4), 128, smem, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<bf16*>(dz), lddz, static_cast<const bf16*>(dout), lddo, static_cast<const bf16*>(z), ldz, M,
+  launch_pdl_impl(32, interaction_bwd_kernel, dim3(static_cast<unsigned>((M + 3) / 4)), dim3(128), smem, static_cast<cudaStream_t>(stream), static_cast<bf16*>(dz), lddz, static_cast<const bf16*>(dout), lddo, static_cast<const bf16*>(z), ldz, M,
       static_cast<int>(F), mask_first);
   GPP_LAUNCH_CHECK();
   return GPP_OK;

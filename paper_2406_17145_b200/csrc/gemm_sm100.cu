@@ -23,6 +23,7 @@
 #include <type_traits>
 #include <unordered_map>
 
+#define GPP_PDL_CLASS 1  // programmatic-dependent-launch family: tcgen05 GEMMs
 #include "gemm.cuh"
 #include "tc_ptx.cuh"
 
@@ -507,6 +508,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // prologue above overlaps the previous kernel's tail
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -691,6 +694,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS + 32, 1
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // prologue above overlaps the previous kernel's tail
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1020,10 +1025,10 @@ static int launch_tc(const void* a, int64_t lda, const void* b, int64_t ldb, con
     attr_set = true;
   }
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(tiles * k_splits * bs.nbatch),
-                                                NUM_THREADS, SMEM, stream>>>(
-      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits, bs);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPI>,
+                             dim3(static_cast<unsigned>(tiles * k_splits * bs.nbatch)), dim3(NUM_THREADS), SMEM,
+                             stream, ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
+                             k_splits, bs);
   if (e != cudaSuccess) {
     set_error(std::string("gemm_tc launch: ") + cudaGetErrorString(e));
     return GPP_ERR_CUDA;
@@ -1107,11 +1112,9 @@ static int launch_tc_pair(const void* a, int64_t lda, const void* b, int64_t ldb
   int64_t clusters = num_sms() / 2;
   if (units < clusters) clusters = units;
   constexpr int THREADS = PAIR_THREADS + (pair_colsum_epi<EPI, A_MN>() ? 32 : 0);
-  gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI><<<static_cast<unsigned>(2 * clusters),
-                                                     THREADS, SMEM, stream>>>(
-      ma, mb, ep, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), k_splits, M < N ? 1 : 0, mx,
-      aux_tma);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(gemm_tc_pair_kernel<BN, STAGES, A_MN, B_MN, EPI>, dim3(static_cast<unsigned>(2 * clusters)),
+                             dim3(THREADS), SMEM, stream, ma, mb, ep, static_cast<int>(M), static_cast<int>(N),
+                             static_cast<int>(K), k_splits, M < N ? 1 : 0, mx, aux_tma);
   if (e != cudaSuccess) {
     set_error(std::string("gemm_tc_pair launch: ") + cudaGetErrorString(e));
     return GPP_ERR_CUDA;
@@ -1180,6 +1183,8 @@ template <int EPI>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits,
                                                             int64_t stride, EpiParams ep, int M,
                                                             int N) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = static_cast<int64_t>(M) * N;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1270,9 +1275,8 @@ static int dispatch_bn(const void* a, int64_t lda, const void* b, int64_t ldb,
   const int64_t total = M * N;
   int64_t grid = (total + 255) / 256;
   if (grid > 148 * 8) grid = 148 * 8;
-  splitk_reduce_kernel<EPI><<<static_cast<unsigned>(grid), 256, 0, stream>>>(
-      ws, splits, M * N, ep, static_cast<int>(M), static_cast<int>(N));
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(splitk_reduce_kernel<EPI>, dim3(static_cast<unsigned>(grid)), dim3(256), 0, stream, ws,
+                             splits, M * N, ep, static_cast<int>(M), static_cast<int>(N));
   if (e != cudaSuccess) {
     set_error(std::string("splitk_reduce launch: ") + cudaGetErrorString(e));
     return GPP_ERR_CUDA;

@@ -4,6 +4,7 @@
 // registers only, fp32 statistics; deterministic column reductions via partial buffers.
 #include <algorithm>
 
+#define GPP_PDL_CLASS 4  // programmatic-dependent-launch family: LayerNorm / mean-pool
 #include "gemm.cuh"
 
 namespace gpp {
@@ -28,6 +29,8 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(bf16* __restrict__ y, float
                                                      const float* __restrict__ g,
                                                      const float* __restrict__ b, int64_t T, int D,
                                                      float eps) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= T) return;
@@ -72,6 +75,8 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(bf16* __restrict__ dx, floa
                                                      const float* __restrict__ g,
                                                      const bf16* __restrict__ dres, int64_t T, int D,
                                                      int rows_per_block) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float red[];  // [8 warps][2 * D]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float dg[PER], db[PER];
@@ -133,6 +138,8 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(bf16* __restrict__ dx, floa
 __global__ void __launch_bounds__(256) ln_bwd_final_kernel(float* __restrict__ dgamma, float* __restrict__ dbeta,
                                                            const float* __restrict__ part, int nblocks, int D,
                                                            int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
@@ -183,6 +190,8 @@ __global__ void __launch_bounds__(256) ln_fwd_vec_kernel(bf16* __restrict__ y, f
                                                          float* __restrict__ rstd, const bf16* __restrict__ x,
                                                          const float* __restrict__ g, const float* __restrict__ b,
                                                          int64_t T, int D, float eps) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NV = PER / 8;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -230,6 +239,8 @@ __global__ void __launch_bounds__(256, R >= 4 ? 2 : 3) ln_fwd_vec2_kernel(bf16* 
                                                                        const float* __restrict__ g,
                                                                        const float* __restrict__ b, int64_t T, int D,
                                                                        float eps) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NV = PER / 8;
   const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5)) * R;
   const int lane = threadIdx.x & 31;
@@ -286,6 +297,8 @@ __global__ void __launch_bounds__(256, ROWS == 1 ? 2 : 1)
                       const bf16* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
                       const float* __restrict__ g, const bf16* __restrict__ dres, int64_t T, int D,
                       int rows_per_block) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NV = PER / 8;
   extern __shared__ float sm[];  // gamma [D] | red [8 warps][2 * D]
   float* gs = sm;
@@ -377,6 +390,8 @@ __global__ void __launch_bounds__(256, ROWS == 1 ? 2 : 1)
 __global__ void __launch_bounds__(256) ln_bwd_final16_kernel(float* __restrict__ dgamma, float* __restrict__ dbeta,
                                                              const float* __restrict__ part, int nblocks, int D,
                                                              int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[16][17];
   const int cx = threadIdx.x & 15, ry = threadIdx.x >> 4;
   const int c = blockIdx.x * 16 + cx;
@@ -467,6 +482,8 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(bf16* __restrict__ ds,
 // ---- token mean-pool over S rows per sample (branch output of MMT) ------------------------
 __global__ void meanpool_fwd_kernel(bf16* __restrict__ out, int64_t ldo, const bf16* __restrict__ x,
                                     int64_t M, int S, int D) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t m = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M || c >= D) return;
@@ -478,6 +495,8 @@ __global__ void meanpool_fwd_kernel(bf16* __restrict__ out, int64_t ldo, const b
 
 __global__ void meanpool_bwd_kernel(bf16* __restrict__ dx, const bf16* __restrict__ dout,
                                     int64_t lddo, int64_t M, int S, int D) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t n = M * S * D;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -531,14 +550,14 @@ int gpp_layernorm_fwd(void* y, float* mean, float* rstd, const void* x, const fl
   const int d = static_cast<int>(D);
   GPP_ARG_CHECK(D == 128 || (a16(y) && a16(x) && a16(gamma) && a16(beta)), "16-byte aligned rows / affine params");
   switch (D) {
-    case 128: ln_fwd_kernel<4><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
-    case 256: ln_fwd_vec_kernel<8><<<grid, 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
+    case 128: launch_pdl(ln_fwd_kernel<4>, dim3(grid), dim3(256), 0, s, static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
+    case 256: launch_pdl(ln_fwd_vec_kernel<8>, dim3(grid), dim3(256), 0, s, static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
     case 512:
-      ln_fwd_vec2_kernel<16, 4><<<static_cast<unsigned>((T + 31) / 32), 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd,
+      launch_pdl(ln_fwd_vec2_kernel<16, 4>, dim3(static_cast<unsigned>((T + 31) / 32)), dim3(256), 0, s, static_cast<bf16*>(y), mean, rstd,
                                                                                      static_cast<const bf16*>(x), gamma, beta, T, d, eps);
       break;
     case 1024:
-      ln_fwd_vec2_kernel<32, 4><<<static_cast<unsigned>((T + 31) / 32), 256, 0, s>>>(static_cast<bf16*>(y), mean, rstd,
+      launch_pdl(ln_fwd_vec2_kernel<32, 4>, dim3(static_cast<unsigned>((T + 31) / 32)), dim3(256), 0, s, static_cast<bf16*>(y), mean, rstd,
                                                                                      static_cast<const bf16*>(x), gamma, beta, T, d, eps);
       break;
     default: set_error("layernorm: D must be 128/256/512/1024"); return GPP_ERR_UNSUPPORTED;
@@ -571,13 +590,13 @@ int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, con
     const size_t smem = (D + 8 * 2 * D) * sizeof(float);
     if (D == 1024) {
       cudaFuncSetAttribute(ln_bwd_vec_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      ln_bwd_vec_kernel<32, 2><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb);
+      launch_pdl(ln_bwd_vec_kernel<32, 2>, dim3(nblk), dim3(256), smem, s, dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb);
     } else {
       cudaFuncSetAttribute(ln_bwd_vec_kernel<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      ln_bwd_vec_kernel<16, 1><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb);
+      launch_pdl(ln_bwd_vec_kernel<16, 1>, dim3(nblk), dim3(256), smem, s, dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb);
     }
     GPP_LAUNCH_CHECK();
-    ln_bwd_final16_kernel<<<static_cast<unsigned>((2 * D + 15) / 16), 256, 0, s>>>(dgamma, dbeta, part, nblk, d,
+    launch_pdl(ln_bwd_final16_kernel, dim3(static_cast<unsigned>((2 * D + 15) / 16)), dim3(256), 0, s, dgamma, dbeta, part, nblk, d,
                                                                                  accumulate);
     GPP_LAUNCH_CHECK();
     return GPP_OK;
@@ -590,16 +609,16 @@ int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, con
   if (!part) return GPP_ERR_CUDA;
   const size_t smem = 8 * 2 * D * sizeof(float);
   switch (D) {
-    case 128: ln_bwd_kernel<4><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
-    case 256: ln_bwd_kernel<8><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
-    case 512: ln_bwd_kernel<16><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
+    case 128: launch_pdl(ln_bwd_kernel<4>, dim3(nblk), dim3(256), smem, s, dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
+    case 256: launch_pdl(ln_bwd_kernel<8>, dim3(nblk), dim3(256), smem, s, dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
+    case 512: launch_pdl(ln_bwd_kernel<16>, dim3(nblk), dim3(256), smem, s, dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
     case 1024:
       cudaFuncSetAttribute(ln_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      ln_bwd_kernel<32><<<nblk, 256, smem, s>>>(dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
+      launch_pdl(ln_bwd_kernel<32>, dim3(nblk), dim3(256), smem, s, dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d, rpb); break;
     default: set_error("layernorm: D must be 128/256/512/1024"); return GPP_ERR_UNSUPPORTED;
   }
   GPP_LAUNCH_CHECK();
-  ln_bwd_final_kernel<<<static_cast<unsigned>((2 * D + 31) / 32), 256, 0, s>>>(dgamma, dbeta, part, nblk, d, accumulate);
+  launch_pdl(ln_bwd_final_kernel, dim3(static_cast<unsigned>((2 * D + 31) / 32)), dim3(256), 0, s, dgamma, dbeta, part, nblk, d, accumulate);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -641,8 +660,7 @@ int gpp_meanpool_fwd(void* out, int64_t ldo, const void* x, int64_t M, int64_t S
                      void* stream) {
   GPP_ARG_CHECK(out && x && M > 0 && S > 0 && D > 0, "bad argument");
   dim3 grid(static_cast<unsigned>((D + 127) / 128), static_cast<unsigned>(M));
-  meanpool_fwd_kernel<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<bf16*>(out), ldo, static_cast<const bf16*>(x), M, static_cast<int>(S), static_cast<int>(D));
+  launch_pdl(meanpool_fwd_kernel, dim3(grid), dim3(128), 0, static_cast<cudaStream_t>(stream), static_cast<bf16*>(out), ldo, static_cast<const bf16*>(x), M, static_cast<int>(S), static_cast<int>(D));
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -653,8 +671,7 @@ int gpp_meanpool_bwd(void* dx, const void* dout, int64_t lddo, int64_t M, int64_
   int64_t n = M * S * D;
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
-  meanpool_bwd_kernel<<<static_cast<unsigned>(g), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<bf16*>(dx), static_cast<const bf16*>(dout), lddo, M, static_cast<int>(S), static_cast<int>(D));
+  launch_pdl(meanpool_bwd_kernel, dim3(static_cast<unsigned>(g)), dim3(256), 0, static_cast<cudaStream_t>(stream), static_cast<bf16*>(dx), static_cast<const bf16*>(dout), lddo, M, static_cast<int>(S), static_cast<int>(D));
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }

@@ -3,8 +3,10 @@
 // N=1 heads, fused losses, bias-grad column sums, the fused SGD step, casts and
 // strided row copies.  All memory-bound; vectorised where alignment allows.
 #include <atomic>
+#include <cstdlib>
 #include <string>
 
+#define GPP_PDL_CLASS 8  // programmatic-dependent-launch family: heads, column sums, SGD, copies
 #include "gemm.cuh"
 
 namespace gpp {
@@ -23,6 +25,12 @@ void take_prefetch_hint(EpiParams& ep) {
   g_pf_bytes = 0;
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// Default: every family except the embedding bags (16), measured 0.45 ms per DLRM step
+// slower with PDL (profiles/pdl_r2.json); GEMM / attention / LN / head kernels gain 1-4%.
+bool pdl_enabled(int family) {
+  static const long mask = [] { const char* e = std::getenv("GPP_PDL"); return e ? std::strtol(e, nullptr, 0) : ~16L; }();
+  return (mask & family) != 0;
+}
 
 namespace {
 
@@ -82,6 +90,8 @@ __device__ float block_max(float v) {
 template <typename T>
 __global__ void rowdot_fwd_kernel(float* out, const T* x, int64_t ldx, const float* w,
                                   const float* bias, int64_t M, int64_t K) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -104,6 +114,8 @@ __global__ void __launch_bounds__(256) rowdot_loss_kernel(float* __restrict__ z,
                                                           const float* __restrict__ bias,
                                                           const float* __restrict__ y, int64_t M, int64_t K,
                                                           int kind, float scale) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[8];
   __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -168,6 +180,8 @@ __global__ void __launch_bounds__(256) rowdot_loss_kernel(float* __restrict__ z,
 template <typename T>
 __global__ void rowdot_dx_kernel(T* dx, int64_t lddx, const float* dout, const float* w,
                                  const T* saved, int64_t ldsaved, int act, int64_t M, int64_t K) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t n = M * K;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -184,6 +198,8 @@ __global__ void __launch_bounds__(256) rowdot_dx_vec_kernel(bf16* dx, int64_t ld
                                                             const float* w, const bf16* saved,
                                                             int64_t ldsaved, int act, uint32_t M,
                                                             uint32_t K8) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t n = M * K8;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t m = i / K8, k = (i % K8) * 8;
@@ -207,6 +223,8 @@ __global__ void __launch_bounds__(256) rowdot_dx_vec_kernel(bf16* dx, int64_t ld
 
 // out[0] (+)= sum_m v[m]: one block, fixed-order (per-thread strided sums, then block_sum).
 __global__ void __launch_bounds__(1024) sum_kernel(float* out, const float* v, int64_t M, int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   float s = 0.f;
   for (int64_t m = threadIdx.x; m < M; m += blockDim.x) s += v[m];
   s = block_sum(s);
@@ -247,6 +265,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) colsum_part_kernel(float* part, const T* x, int64_t ldx,
                                                           const float* wts, int64_t M, int64_t N,
                                                           int64_t rows_per_split) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[8][65];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t col = static_cast<int64_t>(blockIdx.x) * 64 + lane * 2;
@@ -289,6 +309,8 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(float* part, const T* 
 
 __global__ void colsum_final_kernel(float* out, const float* part, int splits, int64_t N,
                                     int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= N) return;
   float t = 0.f;
@@ -372,6 +394,8 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(float* out, float* part
                                                          const T* x, int64_t ldx, int64_t M,
                                                          int64_t N, int64_t rows_per_split,
                                                          int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   colsum_vec_body<T>(out, part, counters, x, ldx, M, N, rows_per_split, accumulate, blockIdx.x, blockIdx.y,
                      gridDim.y);
 }
@@ -393,6 +417,8 @@ struct ColsumJobs {
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_multi_kernel(float* part, unsigned* counters,
                                                            const __grid_constant__ ColsumJobs jobs) {
+  pdl_wait();
+  pdl_trigger();
   const int b = static_cast<int>(blockIdx.x);
   int i = 0;
   while (i + 1 < jobs.n && b >= jobs.j[i + 1].blk0) ++i;
@@ -436,8 +462,7 @@ int colsum_launch(float* out, const T* x, int64_t ldx, const float* wts, int64_t
     float* part = colsum_scratch();
     if (!part) { set_error("colsum scratch allocation failed"); return GPP_ERR_CUDA; }
     const int64_t rps = (M + splits - 1) / splits;
-    colsum_vec_kernel<T><<<dim3(static_cast<unsigned>(vec_blocks), static_cast<unsigned>(splits)), 256, 0, s>>>(
-        out, part, reinterpret_cast<unsigned*>(part + kScratchFloats), x, ldx, M, N, rps, accumulate);
+    launch_pdl(colsum_vec_kernel<T>, dim3(dim3(static_cast<unsigned>(vec_blocks), static_cast<unsigned>(splits))), dim3(256), 0, s, out, part, reinterpret_cast<unsigned*>(part + kScratchFloats), x, ldx, M, N, rps, accumulate);
     GPP_LAUNCH_CHECK();
     return GPP_OK;
   }
@@ -450,9 +475,9 @@ int colsum_launch(float* out, const T* x, int64_t ldx, const float* wts, int64_t
   float* part = colsum_scratch();
   if (!part) { set_error("colsum scratch allocation failed"); return GPP_ERR_CUDA; }
   const int64_t rps = (M + splits - 1) / splits;
-  colsum_part_kernel<T><<<dim3(static_cast<unsigned>(col_blocks), splits), 256, 0, s>>>(part, x, ldx, wts, M, N, rps);
+  launch_pdl(colsum_part_kernel<T>, dim3(dim3(static_cast<unsigned>(col_blocks), splits)), dim3(256), 0, s, part, x, ldx, wts, M, N, rps);
   GPP_LAUNCH_CHECK();
-  colsum_final_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, s>>>(out, part, splits, N, accumulate);
+  launch_pdl(colsum_final_kernel, dim3(static_cast<unsigned>((N + 255) / 256)), dim3(256), 0, s, out, part, splits, N, accumulate);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -471,7 +496,7 @@ int colsum_multi_launch(int n, const void* const* xs, const int64_t* lds, const 
   auto flush = [&]() -> int {
     if (jobs.n == 0) return GPP_OK;
     jobs.accumulate = accumulate;
-    colsum_multi_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, s>>>(part, counters, jobs);
+    launch_pdl(colsum_multi_kernel<T>, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, part, counters, jobs);
     GPP_LAUNCH_CHECK();
     jobs.n = 0;
     part_used = cnt_used = blocks = 0;
@@ -517,6 +542,8 @@ int colsum_multi_launch(int n, const void* const* xs, const int64_t* lds, const 
 // ---------------- losses (single block, deterministic reductions) ----------------
 __global__ void mse_kernel(float* loss_acc, float* dpred, const float* pred, const float* y,
                            int64_t M, float scale) {
+  pdl_wait();
+  pdl_trigger();
   float s = 0.f;
   for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
     const float d = pred[i] - y[i];
@@ -529,6 +556,8 @@ __global__ void mse_kernel(float* loss_acc, float* dpred, const float* pred, con
 
 __global__ void bce_kernel(float* loss_acc, float* dz, const float* z, const float* y, int64_t M,
                            float scale) {
+  pdl_wait();
+  pdl_trigger();
   float s = 0.f;
   for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
     const float zi = z[i], yi = y[i];
@@ -543,6 +572,8 @@ __global__ void bce_kernel(float* loss_acc, float* dz, const float* z, const flo
 template <typename T>
 __global__ void ce_kernel(float* loss_acc, T* dl, int64_t lddl, const T* logits, int64_t ldl,
                           const int64_t* labels, int64_t C, float scale) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t row = blockIdx.x;
   const T* lr = logits + row * ldl;
   float mx = -INFINITY;
@@ -568,6 +599,8 @@ template <typename V, typename I>  // I: uint32_t index math when rows x cv < 2^
 __global__ void __launch_bounds__(256) copy_rows_kernel(V* __restrict__ dst, int64_t ldd,
                                                         const V* __restrict__ src, int64_t lds,
                                                         I cv, I n) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int U = 4;
   const I stride = static_cast<I>(gridDim.x) * blockDim.x;
   for (I base = static_cast<I>(blockIdx.x) * blockDim.x + threadIdx.x; base < n; base += stride * U) {
@@ -598,6 +631,8 @@ struct CopySlices {
 template <typename V>
 __global__ void __launch_bounds__(256) copy_slices_kernel(const __grid_constant__ CopySlices d,
                                                           uint32_t rows) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int U = 4;
   const int k = blockIdx.y;
   const uint32_t cv = d.cv[k], n = cv * rows;
@@ -622,6 +657,8 @@ __global__ void __launch_bounds__(256) copy_slices_kernel(const __grid_constant_
 // ---------------- optimizer ----------------
 __global__ void sgd_kernel(float* __restrict__ master, bf16* __restrict__ shadow,
                            const float* __restrict__ grad, int64_t n, float lr) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t n4 = n / 4;
   float4* m4 = reinterpret_cast<float4*>(master);
@@ -651,6 +688,8 @@ __global__ void sgd_kernel(float* __restrict__ master, bf16* __restrict__ shadow
 
 template <typename D, typename S>
 __global__ void cast_kernel(D* dst, const S* src, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     dst[i] = from_f<D>(to_f<S>(src[i]));
@@ -759,9 +798,9 @@ int gpp_rowdot_fwd(float* out, const void* x, int64_t ldx, const float* w, const
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int blocks = static_cast<int>((M + 7) / 8);
   if (dtype == GPP_BF16)
-    rowdot_fwd_kernel<bf16><<<blocks, 256, 0, s>>>(out, static_cast<const bf16*>(x), ldx, w, bias, M, K);
+    launch_pdl(rowdot_fwd_kernel<bf16>, dim3(blocks), dim3(256), 0, s, out, static_cast<const bf16*>(x), ldx, w, bias, M, K);
   else
-    rowdot_fwd_kernel<float><<<blocks, 256, 0, s>>>(out, static_cast<const float*>(x), ldx, w, bias, M, K);
+    launch_pdl(rowdot_fwd_kernel<float>, dim3(blocks), dim3(256), 0, s, out, static_cast<const float*>(x), ldx, w, bias, M, K);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -778,14 +817,13 @@ int gpp_rowdot_bwd(void* dx, int64_t lddx, float* dw, float* dbias, const float*
                      reinterpret_cast<uintptr_t>(dx) % 16 == 0 &&
                      (act == GPP_ACT_NONE || (ldsaved % 8 == 0 && reinterpret_cast<uintptr_t>(saved) % 16 == 0));
     if (vec)
-      rowdot_dx_vec_kernel<<<grid_for(M * K / 8, 256), 256, 0, s>>>(
-          static_cast<bf16*>(dx), lddx, dout, w, static_cast<const bf16*>(saved), ldsaved, act,
+      launch_pdl(rowdot_dx_vec_kernel, dim3(grid_for(M * K / 8, 256)), dim3(256), 0, s, static_cast<bf16*>(dx), lddx, dout, w, static_cast<const bf16*>(saved), ldsaved, act,
           static_cast<uint32_t>(M), static_cast<uint32_t>(K / 8));
     else if (dtype == GPP_BF16)
-      rowdot_dx_kernel<bf16><<<g, 256, 0, s>>>(static_cast<bf16*>(dx), lddx, dout, w,
+      launch_pdl(rowdot_dx_kernel<bf16>, dim3(g), dim3(256), 0, s, static_cast<bf16*>(dx), lddx, dout, w,
                                                static_cast<const bf16*>(saved), ldsaved, act, M, K);
     else
-      rowdot_dx_kernel<float><<<g, 256, 0, s>>>(static_cast<float*>(dx), lddx, dout, w,
+      launch_pdl(rowdot_dx_kernel<float>, dim3(g), dim3(256), 0, s, static_cast<float*>(dx), lddx, dout, w,
                                                 static_cast<const float*>(saved), ldsaved, act, M, K);
     GPP_LAUNCH_CHECK();
   }
@@ -796,7 +834,7 @@ int gpp_rowdot_bwd(void* dx, int64_t lddx, float* dw, float* dbias, const float*
     if (rc) return rc;
   }
   if (dbias) {
-    sum_kernel<<<1, 1024, 0, s>>>(dbias, dout, M, accumulate);
+    launch_pdl(sum_kernel, dim3(1), dim3(1024), 0, s, dbias, dout, M, accumulate);
     GPP_LAUNCH_CHECK();
   }
   return GPP_OK;
@@ -814,11 +852,9 @@ int gpp_rowdot_loss(float* z, float* dz, float* loss_acc, const void* x, int64_t
   if (!part) { set_error("loss scratch allocation failed"); return GPP_ERR_CUDA; }
   unsigned* counter = reinterpret_cast<unsigned*>(part + kScratchFloats) + (kCounters - 1);
   if (dtype == GPP_BF16)
-    rowdot_loss_kernel<bf16><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
-        z, dz, loss_acc, part, counter, static_cast<const bf16*>(x), ldx, w, bias, y, M, K, kind, scale);
+    launch_pdl(rowdot_loss_kernel<bf16>, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, z, dz, loss_acc, part, counter, static_cast<const bf16*>(x), ldx, w, bias, y, M, K, kind, scale);
   else
-    rowdot_loss_kernel<float><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
-        z, dz, loss_acc, part, counter, static_cast<const float*>(x), ldx, w, bias, y, M, K, kind, scale);
+    launch_pdl(rowdot_loss_kernel<float>, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, z, dz, loss_acc, part, counter, static_cast<const float*>(x), ldx, w, bias, y, M, K, kind, scale);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -826,7 +862,7 @@ int gpp_rowdot_loss(float* z, float* dz, float* loss_acc, const void* x, int64_t
 int gpp_mse_loss(float* loss_acc, float* dpred, const float* pred, const float* y, int64_t M,
                  float scale, void* stream) {
   GPP_ARG_CHECK(loss_acc && dpred && pred && y && M > 0, "bad argument");
-  mse_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(loss_acc, dpred, pred, y, M, scale);
+  launch_pdl(mse_kernel, dim3(1), dim3(1024), 0, static_cast<cudaStream_t>(stream), loss_acc, dpred, pred, y, M, scale);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -834,7 +870,7 @@ int gpp_mse_loss(float* loss_acc, float* dpred, const float* pred, const float* 
 int gpp_bce_loss(float* loss_acc, float* dlogit, const float* logit, const float* y, int64_t M,
                  float scale, void* stream) {
   GPP_ARG_CHECK(loss_acc && dlogit && logit && y && M > 0, "bad argument");
-  bce_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(loss_acc, dlogit, logit, y, M, scale);
+  launch_pdl(bce_kernel, dim3(1), dim3(1024), 0, static_cast<cudaStream_t>(stream), loss_acc, dlogit, logit, y, M, scale);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -845,10 +881,10 @@ int gpp_ce_loss(float* loss_acc, void* dlogits, int64_t lddl, const void* logits
   GPP_ARG_CHECK(loss_acc && dlogits && logits && labels && M > 0 && C > 0, "bad argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (dtype == GPP_BF16)
-    ce_kernel<bf16><<<static_cast<unsigned>(M), 256, 0, s>>>(loss_acc, static_cast<bf16*>(dlogits), lddl,
+    launch_pdl(ce_kernel<bf16>, dim3(static_cast<unsigned>(M)), dim3(256), 0, s, loss_acc, static_cast<bf16*>(dlogits), lddl,
                                                              static_cast<const bf16*>(logits), ldl, labels, C, scale);
   else
-    ce_kernel<float><<<static_cast<unsigned>(M), 256, 0, s>>>(loss_acc, static_cast<float*>(dlogits), lddl,
+    launch_pdl(ce_kernel<float>, dim3(static_cast<unsigned>(M)), dim3(256), 0, s, loss_acc, static_cast<float*>(dlogits), lddl,
                                                               static_cast<const float*>(logits), ldl, labels, C, scale);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
@@ -878,8 +914,7 @@ int gpp_sgd_step(float* master, void* shadow_bf16, const float* grad, int64_t n,
                     (reinterpret_cast<uintptr_t>(grad) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(shadow_bf16) & 7) == 0,
                 "sgd buffers must be 16-byte aligned");
-  sgd_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      master, static_cast<bf16*>(shadow_bf16), grad, n, lr);
+  launch_pdl(sgd_kernel, dim3(grid_for(n / 4 + 1, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), master, static_cast<bf16*>(shadow_bf16), grad, n, lr);
   GPP_LAUNCH_CHECK();
   return GPP_OK;
 }
@@ -901,10 +936,10 @@ int gpp_copy_rows(void* dst, int64_t lddst, const void* src, int64_t ldsrc, int6
   const bool i32 = n + 4ull * 256 * g < (1ull << 32);  // no wrap of base + u * stride either
 #define GPP_COPY_ROWS(V)                                                                          \
   if (i32)                                                                                        \
-    copy_rows_kernel<V, uint32_t><<<g, 256, 0, s>>>(static_cast<V*>(dst), db / vb,                \
+    launch_pdl(copy_rows_kernel<V, uint32_t>, dim3(g), dim3(256), 0, s, static_cast<V*>(dst), db / vb,                \
         static_cast<const V*>(src), sb / vb, static_cast<uint32_t>(cv), static_cast<uint32_t>(n)); \
   else                                                                                            \
-    copy_rows_kernel<V, uint64_t><<<g, 256, 0, s>>>(static_cast<V*>(dst), db / vb,                \
+    launch_pdl(copy_rows_kernel<V, uint64_t>, dim3(g), dim3(256), 0, s, static_cast<V*>(dst), db / vb,                \
         static_cast<const V*>(src), sb / vb, cv, n)
   switch (vb) {
     case 16: GPP_COPY_ROWS(uint4); break;
@@ -960,7 +995,7 @@ int gpp_copy_rows_multi(int n, void* const* dst, const int64_t* lddst, const voi
     // ~148*16 blocks over all slices
     int gx = grid_for(static_cast<int64_t>((big + 3) / 4), 256);
     gx = std::max(1, std::min(gx, (148 * 16 + nk - 1) / nk));
-    copy_slices_kernel<uint4><<<dim3(gx, nk), 256, 0, s>>>(d, static_cast<uint32_t>(rows));
+    launch_pdl(copy_slices_kernel<uint4>, dim3(dim3(gx, nk)), dim3(256), 0, s, d, static_cast<uint32_t>(rows));
     GPP_LAUNCH_CHECK();
   }
   return GPP_OK;
@@ -972,9 +1007,9 @@ int gpp_cast(void* dst, int dst_dtype, const void* src, int src_dtype, int64_t n
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int g = grid_for(n, 256);
   if (dst_dtype == GPP_F32 && src_dtype == GPP_BF16)
-    cast_kernel<float, bf16><<<g, 256, 0, s>>>(static_cast<float*>(dst), static_cast<const bf16*>(src), n);
+    launch_pdl(cast_kernel<float, bf16>, dim3(g), dim3(256), 0, s, static_cast<float*>(dst), static_cast<const bf16*>(src), n);
   else if (dst_dtype == GPP_BF16 && src_dtype == GPP_F32)
-    cast_kernel<bf16, float><<<g, 256, 0, s>>>(static_cast<bf16*>(dst), static_cast<const float*>(src), n);
+    launch_pdl(cast_kernel<bf16, float>, dim3(g), dim3(256), 0, s, static_cast<bf16*>(dst), static_cast<const float*>(src), n);
   else {
     set_error("gpp_cast: unsupported dtype pair");
     return GPP_ERR_ARG;

@@ -185,3 +185,22 @@ def test_dlrm_deterministic_sparse_sgd_bit_reproducible(cuda_lib, monkeypatch):
         outs.append({k: v.clone() for k, v in ex.P.items() if k[1] == "table"})
     assert outs[0].keys() and all(torch.equal(outs[0][k], outs[1][k]) for k in outs[0])
     _dlrm_check(wl, 32, steps=1)
+
+
+def test_pdl_is_bit_identical(cuda_lib):
+    """Programmatic dependent launch only moves kernel prologues ahead of the previous
+    kernel's tail: the trained weights are bit-identical with it on (all families) and off."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    root = os.path.dirname(here)
+    digests = []
+    for mask in ("0", "-1"):
+        env = dict(os.environ, GPP_PDL=mask, PYTHONPATH=os.pathsep.join([root, here]))
+        r = subprocess.run([sys.executable, os.path.join(here, "_pdl_step.py")], env=env, cwd=root,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        digests.append(r.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1]
