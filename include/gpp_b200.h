@@ -236,10 +236,10 @@ int gpp_attn_bwd(const void* qkv, const void* p, const void* o, int64_t ldo, con
 /* Recompute-based (FlashAttention-style) MMT attention: nothing of size Z x S x S in HBM.
  *   gpp_flash_attn_fwd: o[:, h*64..] = softmax(scale q k^T) v, and per (z, query row) the
  *       base-2 log-sum-exp lse2 = scale log2(e) max + log2(sum) ([m*H, S] fp32).
- *   gpp_flash_attn_bwd: dvec = rowsum(dout o o) (caller-owned [m*H, S] fp32 scratch), then
+ *   gpp_flash_attn_bwd: dvec = scale * rowsum(dout o o) (caller-owned [m*H, S] fp32 scratch), then
  *       with P recomputed from q, k, lse2: per (z, 128-key block) the dK and dV blocks of
  *       dqkv (summed over every query block in TMEM), per (z, 128-query block) dQ (summed
- *       over every key block in TMEM) -- three launches, deterministic.
+ *       over every key block in TMEM) -- two launches (prep + one persistent kernel), deterministic.
  * Same layouts and requirements (d == 64 H, S in {128, 256, 384, 512}) as gpp_attn_*;
  * they replace gpp_attn_fwd / gpp_attn_bwd and the two dV / dK batched GEMMs. */
 int gpp_flash_attn_fwd(const void* qkv, float* lse2, void* o, int64_t ldo, int64_t m, int64_t S, int64_t d,

@@ -242,12 +242,13 @@ class TorchBackend:
 
     def flash_attn_bwd(self, qkv, lse2, o, dout, dvec, dqkv, m, S, d, H, scale):
         """Emulates gpp_flash_attn_bwd: P recomputed from lse2, D = rowsum(dO o O),
-        dS = scale P (dO V^T - D); dQ = dS K, dK = dS^T Q, dV = P^T dO (bf16 operands)."""
+        dS = scale P (dO V^T - D); dQ = dS K, dK = dS^T Q, dV = P^T dO (bf16 operands).
+        dvec receives scale * D (the device kernels' pre-scaled form)."""
         dh = d // H
         q, k, v = (self._heads(qkv, m, S, H, c, dh) for c in (0, d, 2 * d))
         g, oz = self._heads(dout, m, S, H, 0, dh), self._heads(o, m, S, H, 0, dh)
         D = (g * oz).sum(2, keepdim=True)
-        dvec.copy_(D.reshape(-1))
+        dvec.copy_(scale * D.reshape(-1))
         s2 = scale * (q @ k.transpose(1, 2)) * 1.4426950408889634
         pz = torch.exp2(s2 - lse2.reshape(m * H, S, 1))
         dsz = scale * pz * (g @ v.transpose(1, 2) - D)

@@ -7,12 +7,12 @@
 //       sums them; O = E V (A operand straight from TMEM) is divided by the row sum in its
 //       epilogue.  Stores O and the row's log-sum-exp in base 2:
 //           lse2 = alpha log2e max + log2(sum),   P = exp2(alpha log2e s - lse2).
-//   attn_bwd_prep_kernel: D[q] = rowsum(dO o O) per (z, query) -- the FlashAttention
+//   attn_bwd_prep_kernel: D[q] = alpha rowsum(dO o O) per (z, query) -- the FlashAttention
 //       identity rowsum(P o dP) = rowsum(dO o O).
 //   attn_bwd_kernel     : ONE persistent launch, two CTA roles (one CTA of each per SM).
 //       dK/dV role, items (z, 128-key block), looping over 32-query blocks: S^T = K Q^T and
 //       dP^T = V dO^T in TMEM (lane = key); the softmax warps recompute
-//       P^T = exp2(alpha log2e s - lse2[q]) and dS^T = alpha P^T o (dP^T - D[q]) and write
+//       P^T = exp2(alpha log2e s - lse2[q]) and dS^T = P^T o (alpha dP^T - D[q]) and write
 //       both as bf16 pairs back over the consumed columns -- the TMEM A operands of
 //       dV += P^T dO and dK += dS^T Q, accumulated in TMEM over every query block.
 //       dQ role, items (z, 128-query block), looping over 32-key blocks: S, dP recomputed
@@ -48,6 +48,14 @@ constexpr int FW_THREADS = 64 + 32 * FW_EPI_WARPS;  // + TMA warp + MMA warp
 
 __device__ __forceinline__ void fa_mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 2^x on the SFU without exp2f's denormal range fix-up (results below 2^-126 flush to 0;
+// softmax terms that small are far below bf16 resolution of the row sum).
+__device__ __forceinline__ float fa_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 __device__ __forceinline__ uint32_t fa_pack(float a, float b) {
@@ -201,8 +209,8 @@ __global__ void __launch_bounds__(FW_THREADS, 2)
         uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float e0 = exp2f(fmaf(__uint_as_float(v[2 * j]), sl2, -mb));
-          const float e1 = exp2f(fmaf(__uint_as_float(v[2 * j + 1]), sl2, -mb));
+          const float e0 = fa_ex2(fmaf(__uint_as_float(v[2 * j]), sl2, -mb));
+          const float e1 = fa_ex2(fmaf(__uint_as_float(v[2 * j + 1]), sl2, -mb));
           sum += e0 + e1;
           pk[j] = fa_pack(e0, e1);
         }
@@ -242,12 +250,13 @@ __global__ void __launch_bounds__(FW_THREADS, 2)
   }
 }
 
-// D[z, s] = sum_c dO[row, head*64 + c] * O[row, head*64 + c]: eight lanes per (row, head),
+// D[z, s] = alpha sum_c dO[row, head*64 + c] * O[row, head*64 + c] (pre-scaled by the softmax
+// scale so that dS = P (alpha dP - D) is one FFMA + one FMUL): eight lanes per (row, head),
 // one 16-byte vector of each operand per lane (every warp load is 512 contiguous bytes),
 // reduced with three shuffles.
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(float* __restrict__ dvec, const bf16* __restrict__ o,
                                                             int64_t ldo, const bf16* __restrict__ dout, int64_t lddo,
-                                                            int64_t T, int S, int H) {
+                                                            int64_t T, int S, int H, float alpha) {
   pdl_wait();
   pdl_trigger();
   const int64_t t = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(float* __restrict__ 
   if (pair < T * H && part == 0) {
     const int64_t row = pair / H;
     const int head = static_cast<int>(pair % H);
-    dvec[(row / S * H + head) * S + row % S] = acc;
+    dvec[(row / S * H + head) * S + row % S] = alpha * acc;
   }
 }
 
@@ -282,14 +291,15 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(float* __restrict__ 
 // Backward: a PERSISTENT launch of two CTA roles, no cross-CTA reduction.  CTAs [0, P) loop
 // over the dK/dV items (z, 128-key block), CTAs [P, 2P) over the dQ items (z, 128-query
 // block); one CTA of each role per SM (256 TMEM columns each).  Inside an item the loop
-// dimension runs in blocks of BB = 32 with double-buffered S / dP TMEM tiles (the MMA warp
-// issues block j+1's S and dP while the softmax warps turn block j's into P / dS, then block
-// j's accumulating MMAs).  Across items the 32 KB "first" tiles (K, V or Q, dO) are double
+// dimension runs in blocks of BB = 32 with double-buffered S / dP TMEM tiles, one per
+// ping-pong group of softmax warps (the MMA warp issues block j+1's S and dP while group
+// j & 1 turns block j's into P / dS, then block j's accumulating MMAs; the other group works
+// on block j+1 meanwhile).  Across items the 32 KB "first" tiles (K, V or Q, dO) are double
 // buffered, so the next item's load overlaps the current item, and the TMEM accumulators are
 // handed back by an mbarrier once the epilogue warps have read them out -- per-item launch,
 // barrier-init, TMEM-alloc and first-load latencies (~50 us of the non-persistent 2048-CTA
-// grid) are paid once per CTA.  Warps: 0 TMA, 1 MMA (+ TMEM alloc), 2..9 two per TMEM lane
-// quarter (one row each), splitting a block's 32 columns in halves of 16.
+// grid) are paid once per CTA.  Warps: 0 TMA, 1 MMA (+ TMEM alloc), 2..9 two groups of one
+// warp per TMEM lane quarter (one row each, all 32 columns of the group's blocks).
 namespace {
 constexpr int BB = 32;          // loop block (queries for dK/dV, keys for dQ)
 constexpr int BW_SMW = 8;
@@ -345,7 +355,7 @@ constexpr uint32_t T_S = 0, T_P = 64, T_A0 = 128, T_A1 = 192;
 
 // DQ = false: dK, dV of items (z, 128-key block), looping over the S/32 query blocks:
 //   S^T = K Q_j^T, dP^T = V dO_j^T (lane = key); P^T = exp2(alpha log2e S^T - lse2[q]),
-//   dS^T = alpha P^T o (dP^T - D[q]) -> bf16 pairs in place; dV += P^T dO_j, dK += dS^T Q_j.
+//   dS^T = P^T o (alpha dP^T - D[q]) -> bf16 pairs in place; dV += P^T dO_j, dK += dS^T Q_j.
 // DQ = true: dQ of items (z, 128-query block), looping over the S/32 key blocks:
 //   S = Q K_j^T, dP = dO V_j^T (lane = query, lse2 / D row constants); dS in place;
 //   dQ += dS K_j.
@@ -382,7 +392,7 @@ __device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const
       mbar_init(&b_ffull[i], 1);
       mbar_init(&b_ffree[i], 1);
       mbar_init(&b_s[i], 1);
-      mbar_init(&b_p[i], BW_SMW);
+      mbar_init(&b_p[i], BW_SMW / 2);  // the four warps of group i
     }
     for (int i = 0; i < BW_STAGES; ++i) {
       mbar_init(&b_full[i], 1);
@@ -489,10 +499,14 @@ __device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const
       }
     }
   } else {
-    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 16-column half of a block
+    // two groups of four warps (one per TMEM lane quarter) in ping-pong: group c owns S / dP
+    // buffer c and turns every other loop block (j = c, c + 2, ...), all 32 columns of its
+    // row, so one group's TMEM load / store latencies overlap the other group's math
+    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, group
     const int lr = q * 32 + lane;                 // key row (dK/dV) or query row (dQ)
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    uint32_t g = 0;
+    const uint32_t ts = trow + T_S + c * BB, tp = trow + T_P + c * BB;
+    uint32_t g = 0;  // global block counter (nb is even: block g uses buffer g & 1 == c)
     for (int it = 0; it < my_items; ++it) {
       const int item = first_item + it * item_step;
       const int z = item / per_z, blk = item % per_z;
@@ -503,44 +517,47 @@ __device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const
         mls = -__ldg(lse2 + zq);
         dq = __ldg(dvec + zq);
       }
-      for (int j = 0; j < nb; ++j, ++g) {
-        const int st = g % BW_STAGES, b = g & 1;
+      for (int j = c; j < nb; j += 2) {
+        const uint32_t gb = g + j;
+        const int st = gb % BW_STAGES;
         const float* vec = reinterpret_cast<const float*>(smem + BW_RING + st * BW_STAGE_STRIDE + 2 * TILEB);
-        if (!DQ) mbar_wait(&b_full[st], (g / BW_STAGES) & 1);  // lse2 / D of the stage (TMA-written)
-        mbar_wait(&b_s[b], (g >> 1) & 1);
+        if (!DQ) mbar_wait(&b_full[st], (gb / BW_STAGES) & 1);  // lse2 / D of the stage (TMA-written)
+        mbar_wait(&b_s[c], (gb >> 1) & 1);
         tc_fence_after();
-        uint32_t sv[16], pv[16];
-        fa_tmem_ld16(trow + T_S + b * BB + c * 16, sv);
-        fa_tmem_ld16(trow + T_P + b * BB + c * 16, pv);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        uint32_t pk[8], dk[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float m0 = mls, m1 = mls, d0 = dq, d1 = dq;
-          if (!DQ) {
-            const float2 ls = *reinterpret_cast<const float2*>(vec + c * 16 + 2 * i);
-            const float2 dd = *reinterpret_cast<const float2*>(vec + 32 + c * 16 + 2 * i);
-            m0 = -ls.x;
-            m1 = -ls.y;
-            d0 = dd.x;
-            d1 = dd.y;
+        for (int h = 0; h < 2; ++h) {  // 16 columns at a time; bf16 pairs of half h -> columns 8h..8h+7
+          uint32_t sv[16], pv[16];
+          fa_tmem_ld16(ts + h * 16, sv);
+          fa_tmem_ld16(tp + h * 16, pv);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          uint32_t pk[8], dk[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float m0 = mls, m1 = mls, d0 = dq, d1 = dq;
+            if (!DQ) {
+              const float2 ls = *reinterpret_cast<const float2*>(vec + h * 16 + 2 * i);
+              const float2 dd = *reinterpret_cast<const float2*>(vec + 32 + h * 16 + 2 * i);
+              m0 = -ls.x;
+              m1 = -ls.y;
+              d0 = dd.x;
+              d1 = dd.y;
+            }
+            const float p0 = fa_ex2(fmaf(__uint_as_float(sv[2 * i]), sl2, m0));
+            const float p1 = fa_ex2(fmaf(__uint_as_float(sv[2 * i + 1]), sl2, m1));
+            pk[i] = fa_pack(p0, p1);
+            dk[i] = fa_pack(p0 * fmaf(__uint_as_float(pv[2 * i]), sh.alpha, -d0),
+                            p1 * fmaf(__uint_as_float(pv[2 * i + 1]), sh.alpha, -d1));
           }
-          const float p0 = exp2f(fmaf(__uint_as_float(sv[2 * i]), sl2, m0));
-          const float p1 = exp2f(fmaf(__uint_as_float(sv[2 * i + 1]), sl2, m1));
-          pk[i] = fa_pack(p0, p1);
-          dk[i] = fa_pack(sh.alpha * p0 * (__uint_as_float(pv[2 * i]) - d0),
-                          sh.alpha * p1 * (__uint_as_float(pv[2 * i + 1]) - d1));
+          // half 0's pairs land in columns 0..7 (already read); half 1 reads 16..31
+          if (!DQ) fa_tmem_st8(ts + h * 8, pk);
+          fa_tmem_st8((DQ ? ts : tp) + h * 8, dk);
         }
-        // bf16 pairs: rows 16c + 2i, +1 -> column 8c + i of the buffer.  Half 1's pairs land
-        // in half 0's columns, so both warps of the quarter must have read theirs first.
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-        if (!DQ) fa_tmem_st8(trow + T_S + b * BB + c * 8, pk);
-        fa_tmem_st8(trow + (DQ ? T_S : T_P) + b * BB + c * 8, dk);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) fa_mbar_arrive(&b_p[b]);
+        if (lane == 0) fa_mbar_arrive(&b_p[c]);
       }
+      g += nb;
       // the item's accumulators -> bf16 rows of dqkv, then hand them back to the MMA warp
       mbar_wait(b_done, it & 1);
       tc_fence_after();
@@ -643,7 +660,7 @@ int gpp_flash_attn_bwd(const void* qkv, const float* lse2, const void* o, int64_
   GPP_ARG_CHECK(ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(o) & 15) == 0, "16-byte aligned o");
   launch_pdl(tc::attn_bwd_prep_kernel, dim3(static_cast<unsigned>((T * H * 8 + 255) / 256)), dim3(256), 0, s, dvec,
              static_cast<const bf16*>(o), ldo, static_cast<const bf16*>(dout), lddo, T, static_cast<int>(S),
-             static_cast<int>(H));
+             static_cast<int>(H), scale);
   GPP_LAUNCH_CHECK();
   CUtensorMap mk128, mq64, mdo64, mdo128;  // qkv maps serve Q, K and V by coordinates
   if ((rc = tc::make_map_bf16(&mk128, qkv, 3 * d, T, 3 * d, 64, 128))) return rc;

@@ -391,7 +391,7 @@ def flash_attn_fwd(qkv, lse2, o, m, S, d, H, scale, stream=None):
 
 def flash_attn_bwd(qkv, lse2, o, dout, dvec, dqkv, m, S, d, H, scale, stream=None):
     """MMT attention backward with P recomputed from q, k and lse2: the Q, K and V blocks
-    of dqkv (dvec: [m*H, S] fp32 scratch for rowsum(dout o o))."""
+    of dqkv (dvec: [m*H, S] fp32 scratch for scale * rowsum(dout o o))."""
     call("gpp_flash_attn_bwd", _ptr(qkv), _ptr(lse2), _ptr(o), _ld(o), _ptr(dout), _ld(dout), _ptr(dvec),
          _ptr(dqkv), m, S, d, H, float(scale), _stream(stream))
 
