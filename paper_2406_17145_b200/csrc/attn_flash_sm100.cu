@@ -17,8 +17,9 @@
 //       dV += P^T dO and dK += dS^T Q, accumulated in TMEM over every query block.
 //       dQ role, items (z, 128-query block), looping over 32-key blocks: S, dP recomputed
 //       (lane = query, lse2 / D row constants), dS in place, dQ += dS K.
-//       S / dP TMEM tiles double-buffered (block j+1's MMAs overlap block j's softmax), the
-//       32 KB first tiles double-buffered across items, 256 TMEM columns per CTA.
+//       S / dP TMEM tiles in two (dK/dV) / three (dQ) buffers turned by two ping-pong groups
+//       of softmax warps, the 32 KB first tiles double-buffered across items, 256 TMEM
+//       columns per CTA.
 //       (A single kernel reducing per-key-block dQ partials across a 4-CTA cluster through
 //       DSMEM measured 363 us vs 149 us without the exchange -- the owner-CTA reductions
 //       serialised the cluster; recomputing S and dP in the dQ role costs less.)
@@ -288,22 +289,26 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(float* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------------------
-// Backward: a PERSISTENT launch of two CTA roles, no cross-CTA reduction.  CTAs [0, P) loop
-// over the dK/dV items (z, 128-key block), CTAs [P, 2P) over the dQ items (z, 128-query
-// block); one CTA of each role per SM (256 TMEM columns each).  Inside an item the loop
-// dimension runs in blocks of BB = 32 with double-buffered S / dP TMEM tiles, one per
-// ping-pong group of softmax warps (the MMA warp issues block j+1's S and dP while group
-// j & 1 turns block j's into P / dS, then block j's accumulating MMAs; the other group works
-// on block j+1 meanwhile).  Across items the 32 KB "first" tiles (K, V or Q, dO) are double
-// buffered, so the next item's load overlaps the current item, and the TMEM accumulators are
-// handed back by an mbarrier once the epilogue warps have read them out -- per-item launch,
-// barrier-init, TMEM-alloc and first-load latencies (~50 us of the non-persistent 2048-CTA
-// grid) are paid once per CTA.  Warps: 0 TMA, 1 MMA (+ TMEM alloc), 2..9 two groups of one
-// warp per TMEM lane quarter (one row each, all 32 columns of the group's blocks).
+// Backward: a PERSISTENT launch of two CTA roles, one CTA of each per SM (256 TMEM columns
+// each), no cross-CTA reduction.  CTAs [0, P) loop over the dK/dV items (z, 128-key block),
+// CTAs [P, 2P) over the dQ items (z, 128-query block); CTA b of a role takes items b, b + P,
+// ...  Warps: 0 TMA, 1 MMA (+ TMEM alloc), 2..9 eight softmax warps in two ping-pong groups
+// (one warp per TMEM lane quarter each, one row per lane).  The loop dimension runs in
+// blocks of BB = 32; block g's S / dP tiles live in TMEM buffer g % NBUF and are turned into
+// P / dS by group g & 1, so one group's TMEM load / store latencies overlap the other's math.
+// The MMA warp issues S / dP NBUF - 1 blocks ahead within an item before it waits for block
+// g's P / dS and issues its accumulating MMAs (NBUF = 2 for dK/dV, whose two accumulators
+// take half the columns; 3 for dQ).  The 32 KB "first" tiles (K, V or Q, dO) are
+// double-buffered across items and the accumulators are handed back to the MMA warp by an
+// mbarrier once read out, so per-item launch / barrier-init / TMEM-alloc / first-load
+// latencies are paid once per CTA.  (Issuing ahead ACROSS item boundaries measured 150 us
+// vs 124 us: the MMA warp then stalls on the next item's first tiles before it has issued
+// the current item's last accumulating MMAs.)
 namespace {
-constexpr int BB = 32;          // loop block (queries for dK/dV, keys for dQ)
-constexpr int BW_SMW = 8;
-constexpr int BW_THREADS = 64 + 32 * BW_SMW;
+constexpr int BB = 32;                              // loop block (queries for dK/dV, keys for dQ)
+constexpr int BW_SMW = 8;                           // softmax warps per role
+constexpr int BW_ROLE_WARPS = 2 + BW_SMW;
+constexpr int BW_THREADS = 32 * BW_ROLE_WARPS;      // one role per CTA: 320 threads
 constexpr int BW_STAGES = 4;
 constexpr uint32_t TILEB = BB * 128;     // 32 rows x 64 bf16 (128B-swizzled): 4 KB
 constexpr uint32_t TILE128 = 128 * 128;  // 16 KB
@@ -343,14 +348,26 @@ __device__ __forceinline__ void fa_store_row32(bf16* dst, const uint32_t (&v)[32
   }
 }
 
-// smem: first tiles [2] x 32 KB | stages [BW_STAGES] of 9 KB (two 32-row tiles + 2 x 128 B of
-// per-query lse2 / D, used by the dK/dV role) | barriers
+// smem per role (1024-aligned): first tiles [2] x 32 KB | stages [BW_STAGES] of 9 KB (two
+// 32-row tiles + 2 x 128 B of per-query lse2 / D, used by the dK/dV role) | barriers
 constexpr uint32_t BW_STAGE_STRIDE = 9 * 1024;
 constexpr uint32_t BW_RING = 2 * FIRST_BYTES;
 constexpr uint32_t BW_BAR = BW_RING + BW_STAGES * BW_STAGE_STRIDE;
-constexpr int SMEM_BW = BW_BAR + 256 + 1024;
-// TMEM columns: S[b] at 32b, dP[b] at 64 + 32b, accumulators at 128 (dV | dQ) and 192 (dK)
-constexpr uint32_t T_S = 0, T_P = 64, T_A0 = 128, T_A1 = 192;
+constexpr uint32_t BW_ROLE_SMEM = (BW_BAR + 256 + 1023) & ~1023u;
+constexpr int SMEM_BW = BW_ROLE_SMEM + 1024;
+
+// TMEM columns (256 per CTA, two CTAs per SM).  dK/dV role: S[2] at 0 / 32, dP[2] at 64 / 96,
+// dV at 128, dK at 192.  dQ role (one accumulator): S[3] at 0 / 32 / 64, dP[3] at 96 / 128 / 160,
+// dQ at 192.
+template <bool DQ>
+struct BwTmem {
+  static constexpr int NBUF = DQ ? 3 : 2;
+  static constexpr uint32_t S = 0;
+  static constexpr uint32_t P = S + NBUF * BB;
+  static constexpr uint32_t A0 = P + NBUF * BB;  // dV (dK/dV role) or dQ
+  static constexpr uint32_t A1 = A0 + FA_DH;     // dK
+};
+static_assert(BwTmem<false>::A1 + FA_DH == 256 && BwTmem<true>::A0 + FA_DH == 256, "TMEM plan");
 }  // namespace
 
 // DQ = false: dK, dV of items (z, 128-key block), looping over the S/32 query blocks:
@@ -359,62 +376,35 @@ constexpr uint32_t T_S = 0, T_P = 64, T_A0 = 128, T_A1 = 192;
 // DQ = true: dQ of items (z, 128-query block), looping over the S/32 key blocks:
 //   S = Q K_j^T, dP = dO V_j^T (lane = query, lse2 / D row constants); dS in place;
 //   dQ += dS K_j.
+// smem: this role's region; w: role-local warp; qw: the CTA warp index (TMEM lane quarter).
 template <bool DQ>
-__device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const CUtensorMap& m_qkvb,
+__device__ __forceinline__ void attn_bwd_role(uint8_t* smem, uint32_t tmem, int w, int qw, int lane,
+                                              const CUtensorMap& m_qkv128, const CUtensorMap& m_qkvb,
                                               const CUtensorMap& m_do128, const CUtensorMap& m_dob,
                                               const float* __restrict__ lse2, const float* __restrict__ dvec,
                                               bf16* __restrict__ dqkv, int64_t ld_dqkv, const FaShape& sh,
                                               int first_item, int item_step, int n_items) {
+  using L = BwTmem<DQ>;
+  constexpr int NB = L::NBUF;
   constexpr uint32_t IDESC_S = idesc_bf16<BB, false, false>();
   constexpr uint32_t IDESC_AC = idesc_bf16<FA_DH, false, true>();
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BW_BAR);
-  uint64_t* b_ffull = bar + 0;                    // [2] first tiles landed
-  uint64_t* b_ffree = bar + 2;                    // [2] first tiles free (item's MMAs done)
-  uint64_t* b_full = bar + 4;                     // [BW_STAGES]
-  uint64_t* b_free = bar + 4 + BW_STAGES;         // [BW_STAGES]
-  uint64_t* b_s = bar + 4 + 2 * BW_STAGES;        // [2] S, dP of the buffer in TMEM
-  uint64_t* b_p = bar + 6 + 2 * BW_STAGES;        // [2] bf16 P / dS of the buffer in TMEM
-  uint64_t* b_done = bar + 8 + 2 * BW_STAGES;     // the item's accumulators complete
-  uint64_t* b_acc = bar + 9 + 2 * BW_STAGES;      // accumulators read out (8 warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10 + 2 * BW_STAGES);
+  uint64_t* b_ffull = bar + 0;                 // [2] first tiles landed
+  uint64_t* b_ffree = bar + 2;                 // [2] first tiles free (item's MMAs done)
+  uint64_t* b_full = bar + 4;                  // [BW_STAGES]
+  uint64_t* b_free = b_full + BW_STAGES;       // [BW_STAGES]
+  uint64_t* b_s = b_free + BW_STAGES;          // [NB] S, dP of the buffer in TMEM
+  uint64_t* b_p = b_s + NB;                    // [NB] bf16 P / dS of the buffer in TMEM
+  uint64_t* b_done = b_p + NB;                 // the item's accumulators complete
+  uint64_t* b_acc = b_done + 1;                // accumulators read out (8 warps)
 
   const int S = sh.S, d = sh.d, H = sh.H;
   const int per_z = S / 128, nb = S / BB;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float sl2 = sh.alpha * 1.4426950408889634f;
   // my items: first_item, first_item + item_step, ... < n_items
   const int my_items = first_item < n_items ? (n_items - 1 - first_item) / item_step + 1 : 0;
 
-  if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&b_ffull[i], 1);
-      mbar_init(&b_ffree[i], 1);
-      mbar_init(&b_s[i], 1);
-      mbar_init(&b_p[i], BW_SMW / 2);  // the four warps of group i
-    }
-    for (int i = 0; i < BW_STAGES; ++i) {
-      mbar_init(&b_full[i], 1);
-      mbar_init(&b_free[i], 1);
-    }
-    mbar_init(b_done, 1);
-    mbar_init(b_acc, BW_SMW);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // prologue above overlaps the previous kernel's tail
-  pdl_trigger();
-
-  if (warp == 0) {
+  if (w == 0) {
     if (lane == 0) {
       uint32_t g = 0;  // global stage counter (continues across items)
       for (int it = 0; it < my_items; ++it) {
@@ -452,33 +442,34 @@ __device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (w == 1) {
     if (lane == 0) {
-      uint32_t g = 0;  // global block counter: stage g % BW_STAGES, TMEM buffer g & 1
+      uint32_t g = 0;  // global block counter: stage g % BW_STAGES, TMEM buffer g % NB
       for (int it = 0; it < my_items; ++it) {
         const int fb = it & 1;
         const uint32_t fa = smem_u32(smem + fb * FIRST_BYTES), fa2 = fa + TILE128;
         mbar_wait(&b_ffull[fb], (it >> 1) & 1);
-        auto issue_sp = [&](uint32_t gg) {  // S / dP of block gg into buffer gg & 1
-          const int st = gg % BW_STAGES, b = gg & 1;
+        auto issue_sp = [&](uint32_t gg) {  // S / dP of block gg into buffer gg % NB
+          const int st = gg % BW_STAGES, b = gg % NB;
           const uint32_t ta = smem_u32(smem + BW_RING + st * BW_STAGE_STRIDE), tb = ta + TILEB;
           mbar_wait(&b_full[st], (gg / BW_STAGES) & 1);
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < FA_DH / 16; ++k) {
             // dK/dV: S^T = K Q_j^T, dP^T = V dO_j^T;  dQ: S = Q K_j^T, dP = dO V_j^T
-            umma_bf16(tmem + T_S + b * BB, sdesc_sw128(fa + k * 32, 16, 1024), sdesc_sw128(ta + k * 32, 16, 1024),
+            umma_bf16(tmem + L::S + b * BB, sdesc_sw128(fa + k * 32, 16, 1024), sdesc_sw128(ta + k * 32, 16, 1024),
                       IDESC_S, k != 0);
-            umma_bf16(tmem + T_P + b * BB, sdesc_sw128(fa2 + k * 32, 16, 1024), sdesc_sw128(tb + k * 32, 16, 1024),
+            umma_bf16(tmem + L::P + b * BB, sdesc_sw128(fa2 + k * 32, 16, 1024), sdesc_sw128(tb + k * 32, 16, 1024),
                       IDESC_S, k != 0);
           }
           umma_commit(&b_s[b]);
         };
-        issue_sp(g);
+        for (int j = 0; j + 1 < NB && j < nb; ++j) issue_sp(g + j);
         for (int j = 0; j < nb; ++j, ++g) {
-          const int st = g % BW_STAGES, b = g & 1;
-          if (j + 1 < nb) issue_sp(g + 1);  // overlaps block j's softmax
-          mbar_wait(&b_p[b], (g >> 1) & 1);
+          const int st = g % BW_STAGES, b = g % NB;
+          // buffer (g + NB - 1) % NB last held block g - 1, whose MMAs were issued last iteration
+          if (j + NB - 1 < nb) issue_sp(g + NB - 1);
+          mbar_wait(&b_p[b], (g / NB) & 1);
           if (j == 0 && it > 0) mbar_wait(b_acc, (it - 1) & 1);  // previous item's accumulators read out
           tc_fence_after();
           const uint32_t ta = smem_u32(smem + BW_RING + st * BW_STAGE_STRIDE), tb = ta + TILEB;
@@ -486,10 +477,13 @@ __device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const
           for (int k = 0; k < BB / 16; ++k) {  // K = 32 rows of the block, 16 per MMA (8 packed columns)
             const uint32_t acc = (j | k) != 0;
             if (DQ) {  // B = K_j as the MN-major (key rows) operand
-              fa_umma_ts(tmem + T_A0, tmem + T_S + b * BB + k * 8, sdesc_sw128(ta + k * 2048, 8192, 1024), IDESC_AC, acc);
+              fa_umma_ts(tmem + L::A0, tmem + L::S + b * BB + k * 8, sdesc_sw128(ta + k * 2048, 8192, 1024), IDESC_AC,
+                         acc);
             } else {
-              fa_umma_ts(tmem + T_A0, tmem + T_S + b * BB + k * 8, sdesc_sw128(tb + k * 2048, 8192, 1024), IDESC_AC, acc);
-              fa_umma_ts(tmem + T_A1, tmem + T_P + b * BB + k * 8, sdesc_sw128(ta + k * 2048, 8192, 1024), IDESC_AC, acc);
+              fa_umma_ts(tmem + L::A0, tmem + L::S + b * BB + k * 8, sdesc_sw128(tb + k * 2048, 8192, 1024), IDESC_AC,
+                         acc);
+              fa_umma_ts(tmem + L::A1, tmem + L::P + b * BB + k * 8, sdesc_sw128(ta + k * 2048, 8192, 1024), IDESC_AC,
+                         acc);
             }
           }
           umma_commit(&b_free[st]);
@@ -499,14 +493,9 @@ __device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const
       }
     }
   } else {
-    // two groups of four warps (one per TMEM lane quarter) in ping-pong: group c owns S / dP
-    // buffer c and turns every other loop block (j = c, c + 2, ...), all 32 columns of its
-    // row, so one group's TMEM load / store latencies overlap the other group's math
-    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, group
-    const int lr = q * 32 + lane;                 // key row (dK/dV) or query row (dQ)
+    const int q = qw & 3, c = (w - 2) >> 2;  // lane quarter, ping-pong group
+    const int lr = q * 32 + lane;            // key row (dK/dV) or query row (dQ)
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const uint32_t ts = trow + T_S + c * BB, tp = trow + T_P + c * BB;
-    uint32_t g = 0;  // global block counter (nb is even: block g uses buffer g & 1 == c)
     for (int it = 0; it < my_items; ++it) {
       const int item = first_item + it * item_step;
       const int z = item / per_z, blk = item % per_z;
@@ -517,12 +506,13 @@ __device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const
         mls = -__ldg(lse2 + zq);
         dq = __ldg(dvec + zq);
       }
-      for (int j = c; j < nb; j += 2) {
-        const uint32_t gb = g + j;
-        const int st = gb % BW_STAGES;
+      for (int j = c; j < nb; j += 2) {  // nb is even: block gb goes to group gb & 1 == c
+        const uint32_t gb = static_cast<uint32_t>(it * nb + j);
+        const int st = gb % BW_STAGES, b = gb % NB;
+        const uint32_t ts = trow + L::S + b * BB, tp = trow + L::P + b * BB;
         const float* vec = reinterpret_cast<const float*>(smem + BW_RING + st * BW_STAGE_STRIDE + 2 * TILEB);
         if (!DQ) mbar_wait(&b_full[st], (gb / BW_STAGES) & 1);  // lse2 / D of the stage (TMA-written)
-        mbar_wait(&b_s[c], (gb >> 1) & 1);
+        mbar_wait(&b_s[b], (gb / NB) & 1);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // 16 columns at a time; bf16 pairs of half h -> columns 8h..8h+7
@@ -555,23 +545,22 @@ __device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) fa_mbar_arrive(&b_p[c]);
+        if (lane == 0) fa_mbar_arrive(&b_p[b]);
       }
-      g += nb;
       // the item's accumulators -> bf16 rows of dqkv, then hand them back to the MMA warp
       mbar_wait(b_done, it & 1);
       tc_fence_after();
       const int64_t row = static_cast<int64_t>(row0) + blk * 128 + lr;
       if (DQ) {
         uint32_t v[32];
-        tmem_ld32(trow + T_A0 + c * 32, v);
+        tmem_ld32(trow + L::A0 + c * 32, v);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) fa_mbar_arrive(b_acc);
         fa_store_row32(dqkv + row * ld_dqkv + head * FA_DH + c * 32, v);
       } else {
-        // half-0 warps write dV, half-1 warps dK
-        const uint32_t src = trow + (c == 0 ? T_A0 : T_A1);
+        // group 0 writes dV, group 1 dK
+        const uint32_t src = trow + (c == 0 ? L::A0 : L::A1);
         uint32_t v0[32], v1[32];
         tmem_ld32(src, v0);
         tmem_ld32(src + 32, v1);
@@ -584,26 +573,64 @@ __device__ __forceinline__ void attn_bwd_role(const CUtensorMap& m_qkv128, const
       }
     }
   }
+}
+
+template <bool DQ>
+__device__ __forceinline__ void attn_bwd_init_barriers(uint8_t* smem) {
+  constexpr int NB = BwTmem<DQ>::NBUF;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BW_BAR);
+  for (int i = 0; i < 4 + 2 * BW_STAGES; ++i) mbar_init(&bar[i], 1);  // ffull, ffree, full, free
+  uint64_t* b_s = bar + 4 + 2 * BW_STAGES;
+  for (int i = 0; i < NB; ++i) {
+    mbar_init(&b_s[i], 1);
+    mbar_init(&b_s[NB + i], BW_SMW / 2);  // b_p: the four warps of one group
+  }
+  mbar_init(&b_s[2 * NB], 1);           // b_done
+  mbar_init(&b_s[2 * NB + 1], BW_SMW);  // b_acc
+}
+
+// CTAs [0, P) run the dK/dV role, [P, 2P) the dQ role (one of each per SM).
+__global__ void __launch_bounds__(BW_THREADS, 2)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap m_qkv128, const __grid_constant__ CUtensorMap m_qkvb,
+                    const __grid_constant__ CUtensorMap m_do128, const __grid_constant__ CUtensorMap m_dob,
+                    const float* __restrict__ lse2, const float* __restrict__ dvec, bf16* __restrict__ dqkv,
+                    int64_t ld_dqkv, FaShape sh, int n, int P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + BW_BAR + 248);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = static_cast<int>(blockIdx.x);
+  const bool dq_role = b >= P;
+  if (threadIdx.x == 0) {
+    if (dq_role)
+      attn_bwd_init_barriers<true>(smem);
+    else
+      attn_bwd_init_barriers<false>(smem);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // prologue above overlaps the previous kernel's tail
+  pdl_trigger();
+  if (dq_role)
+    attn_bwd_role<true>(smem, tmem, warp, warp, lane, m_qkv128, m_qkvb, m_do128, m_dob, lse2, dvec, dqkv, ld_dqkv,
+                        sh, b - P, P, n);
+  else
+    attn_bwd_role<false>(smem, tmem, warp, warp, lane, m_qkv128, m_qkvb, m_do128, m_dob, lse2, dvec, dqkv, ld_dqkv,
+                         sh, b, P, n);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
   }
-}
-
-// Persistent backward: CTAs [0, P) the dK/dV role, [P, 2P) the dQ role, each striding over its
-// n items.
-__global__ void __launch_bounds__(BW_THREADS, 2)
-    attn_bwd_kernel(const __grid_constant__ CUtensorMap m_qkv128, const __grid_constant__ CUtensorMap m_qkvb,
-                    const __grid_constant__ CUtensorMap m_do128, const __grid_constant__ CUtensorMap m_dob,
-                    const float* __restrict__ lse2, const float* __restrict__ dvec, bf16* __restrict__ dqkv,
-                    int64_t ld_dqkv, FaShape sh, int n, int P) {
-  const int b = static_cast<int>(blockIdx.x);
-  if (b < P)
-    attn_bwd_role<false>(m_qkv128, m_qkvb, m_do128, m_dob, lse2, dvec, dqkv, ld_dqkv, sh, b, P, n);
-  else
-    attn_bwd_role<true>(m_qkv128, m_qkvb, m_do128, m_dob, lse2, dvec, dqkv, ld_dqkv, sh, b - P, P, n);
 }
 
 }  // namespace tc
