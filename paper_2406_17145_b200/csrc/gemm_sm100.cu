@@ -136,9 +136,11 @@ __device__ __forceinline__ void store_bf16x32_staged(bf16* base, int64_t ld, con
 // `aux` (residual / act'-saved, 32 values) is loaded by the caller BEFORE the TMEM
 // load so its global latency overlaps tcgen05.ld.
 template <int EPI>
+// `sbias`: the chunk's 32 bias values already staged in shared memory (or null: global).
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const uint32_t (&v)[32],
                                                const float (&aux)[32], int row, int col0, int M,
-                                               int N, uint8_t* stage = nullptr, int lane = 0) {
+                                               int N, uint8_t* stage = nullptr, int lane = 0,
+                                               const float* sbias = nullptr) {
   // staged (warp-collective, coalesced) bf16 stores: whole 32-column chunks of a FWD / DGRAD
   // epilogue with 16-byte-aligned rows; every lane of the warp takes part
   const int row0 = row - lane;
@@ -217,7 +219,13 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const uint32
   } else {
     if constexpr (EPI == EPI_FWD) {
       if (ep.bias != nullptr) {
-        if (full && al16(ep.bias + col0)) {
+        if (sbias != nullptr) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 b = *reinterpret_cast<const float4*>(sbias + j);
+            f[j] += b.x; f[j + 1] += b.y; f[j + 2] += b.z; f[j + 3] += b.w;
+          }
+        } else if (full && al16(ep.bias + col0)) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + j));
@@ -871,6 +879,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS + 32, 1
         }
       };
       if (AUX_TMA_EPI(EPI) && aux_tma) issue_aux(group);
+      // bias of this warp's CH chunks -> the unused second half of its aux tile, loaded before
+      // the accumulator wait (a per-chunk global load exposed its latency in every chunk)
+      const float* sbias = nullptr;
+      if constexpr (EPI == EPI_FWD) {
+        if (!aux_tma && ep.bias != nullptr) {
+          static_assert(CH * 32 <= 32 * 4 * 4, "one float4 per lane");
+          float* sb = reinterpret_cast<float*>(my_aux + 2048);
+          const int p = lane >> 3;
+          if (p < CH) {
+            const int col = n_blk * BN + (group + p * GSTEP) * 32 + (lane & 7) * 4;
+            float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (col + 4 <= N && al16(ep.bias + col)) {
+              b = __ldg(reinterpret_cast<const float4*>(ep.bias + col));
+            } else {
+              if (col < N) b.x = __ldg(ep.bias + col);
+              if (col + 1 < N) b.y = __ldg(ep.bias + col + 1);
+              if (col + 2 < N) b.z = __ldg(ep.bias + col + 2);
+              if (col + 3 < N) b.w = __ldg(ep.bias + col + 3);
+            }
+            *reinterpret_cast<float4*>(sb + p * 32 + (lane & 7) * 4) = b;
+          }
+          __syncwarp();
+          sbias = sb;
+        }
+      }
       mbar_wait(&tfull_bar[acc], aph);
       tc_fence_after();
 #pragma unroll 1
@@ -896,7 +929,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS + 32, 1
             if (AUX_TMA_EPI(EPI)) stage = my_aux;  // aux tiles unused by this launch
           }
           tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
-          epilogue_chunk<EPI>(epu, v, aux, row, n_blk * BN + c * 32, M, N, stage, lane);
+          epilogue_chunk<EPI>(epu, v, aux, row, n_blk * BN + c * 32, M, N, stage, lane,
+                              sbias != nullptr ? sbias + ((c - group) / GSTEP) * 32 : nullptr);
           if (stage != nullptr) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
       }

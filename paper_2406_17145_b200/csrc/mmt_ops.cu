@@ -5,6 +5,8 @@
 #include <algorithm>
 
 #define GPP_PDL_CLASS 4  // programmatic-dependent-launch family: LayerNorm / mean-pool
+#include <cstdlib>
+
 #include "gemm.cuh"
 
 namespace gpp {
@@ -385,6 +387,212 @@ __global__ void __launch_bounds__(256, ROWS == 1 ? 2 : 1)
   }
 }
 
+// ---- LayerNorm, software-pipelined persistent form (D = 32 PER, PER in {16, 32}) ----------
+// Warp w of the grid takes rows w, w + NW, w + 2 NW, ... (NW = every warp of the grid) and
+// loads its NEXT row into a second register set before it processes the current one, so
+// each warp keeps one row of loads in flight while it computes and stores -- reads and
+// writes stream concurrently instead of in one load phase and one store phase per wave.
+template <int PER>
+struct LnFwdRow {
+  uint4 x[PER / 8];
+};
+
+template <int PER>
+__device__ __forceinline__ void ln_fwd_load(LnFwdRow<PER>& a, const bf16* __restrict__ x, int64_t r, int D, int lane) {
+#pragma unroll
+  for (int i = 0; i < PER / 8; ++i) a.x[i] = __ldg(reinterpret_cast<const uint4*>(x + r * D) + lane + 32 * i);
+}
+
+template <int PER>
+__device__ __forceinline__ void ln_fwd_row(const LnFwdRow<PER>& a, bf16* __restrict__ y, float* __restrict__ mean,
+                                           float* __restrict__ rstd, const float* __restrict__ gs,
+                                           const float* __restrict__ bs, int64_t r, int D, float eps, int lane) {
+  constexpr int NV = PER / 8;
+  float v[PER];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) unpack8(a.x[i], v + 8 * i);
+  float sm = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) sm += v[i];
+  const float mu = wsum(sm) / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) q += (v[i] - mu) * (v[i] - mu);
+  const float rs = rsqrtf(wsum(q) / D + eps);
+  uint4* yr = reinterpret_cast<uint4*>(y + r * D);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = 8 * (lane + 32 * i);
+    const float4 g0 = *reinterpret_cast<const float4*>(gs + c), g1 = *reinterpret_cast<const float4*>(gs + c + 4);
+    const float4 b0 = *reinterpret_cast<const float4*>(bs + c), b1 = *reinterpret_cast<const float4*>(bs + c + 4);
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    float o[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) o[t] = (v[8 * i + t] - mu) * rs * gg[t] + bb[t];
+    yr[lane + 32 * i] = pack8(o);
+  }
+  if (lane == 0) {
+    mean[r] = mu;
+    rstd[r] = rs;
+  }
+}
+
+template <int PER>
+__global__ void __launch_bounds__(256, 2) ln_fwd_pipe_kernel(bf16* __restrict__ y, float* __restrict__ mean,
+                                                             float* __restrict__ rstd, const bf16* __restrict__ x,
+                                                             const float* __restrict__ g, const float* __restrict__ b,
+                                                             int64_t T, int D, float eps) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float sm[];  // gamma [D] | beta [D]
+  for (int c = threadIdx.x; c < D; c += 256) {
+    sm[c] = g[c];
+    sm[D + c] = b[c];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t NW = static_cast<int64_t>(gridDim.x) * 8;
+  int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  LnFwdRow<PER> A, B;
+  if (r < T) ln_fwd_load(A, x, r, D, lane);
+  while (r < T) {
+    if (r + NW < T) ln_fwd_load(B, x, r + NW, D, lane);
+    ln_fwd_row(A, y, mean, rstd, sm, sm + D, r, D, eps, lane);
+    r += NW;
+    if (r >= T) break;
+    if (r + NW < T) ln_fwd_load(A, x, r + NW, D, lane);
+    ln_fwd_row(B, y, mean, rstd, sm, sm + D, r, D, eps, lane);
+    r += NW;
+  }
+}
+
+template <int PER>
+struct LnBwdRow {
+  uint4 x[PER / 8], dy[PER / 8];
+  float mu, rs;
+};
+
+template <int PER>
+__device__ __forceinline__ void ln_bwd_load(LnBwdRow<PER>& a, const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                            const float* __restrict__ mean, const float* __restrict__ rstd,
+                                            int64_t r, int D, int lane) {
+#pragma unroll
+  for (int i = 0; i < PER / 8; ++i) {
+    a.x[i] = __ldg(reinterpret_cast<const uint4*>(x + r * D) + lane + 32 * i);
+    a.dy[i] = __ldg(reinterpret_cast<const uint4*>(dy + r * D) + lane + 32 * i);
+  }
+  a.mu = __ldg(mean + r);
+  a.rs = __ldg(rstd + r);
+}
+
+//   dx = rstd * (g dy - mean(g dy) - xhat * mean(g dy xhat)) [+ dres];  dg += dy xhat, db += dy
+// (the residual gradient is loaded at the row's start -- its latency hides behind the first
+// pass -- rather than prefetched a row ahead, which spilled the register-resident accumulators)
+template <int PER>
+__device__ __forceinline__ void ln_bwd_row(const LnBwdRow<PER>& a, bf16* __restrict__ dx, const float* __restrict__ gs,
+                                           const bf16* __restrict__ dres, float (&dg)[PER], float (&db)[PER],
+                                           int64_t r, int D, int lane) {
+  constexpr int NV = PER / 8;
+  const float mu = a.mu, rs = a.rs;
+  uint4 dr[NV];
+  if (dres) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) dr[i] = __ldg(reinterpret_cast<const uint4*>(dres + r * D) + lane + 32 * i);
+  }
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float xv[8], dv[8];
+    unpack8(a.x[i], xv);
+    unpack8(a.dy[i], dv);
+    const int c = 8 * (lane + 32 * i);
+    const float4 g0 = *reinterpret_cast<const float4*>(gs + c), g1 = *reinterpret_cast<const float4*>(gs + c + 4);
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float xh = (xv[t] - mu) * rs;
+      const float gy = dv[t] * gg[t];
+      dg[8 * i + t] = fmaf(dv[t], xh, dg[8 * i + t]);
+      db[8 * i + t] += dv[t];
+      s1 += gy;
+      s2 = fmaf(gy, xh, s2);
+    }
+  }
+  const float m1 = wsum(s1) / D, m2 = wsum(s2) / D;
+  uint4* dxr = reinterpret_cast<uint4*>(dx + r * D);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float xv[8], dv[8], o[8];
+    unpack8(a.x[i], xv);
+    unpack8(a.dy[i], dv);
+    const int c = 8 * (lane + 32 * i);
+    const float4 g0 = *reinterpret_cast<const float4*>(gs + c), g1 = *reinterpret_cast<const float4*>(gs + c + 4);
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float xh = (xv[t] - mu) * rs;
+      o[t] = rs * (dv[t] * gg[t] - m1 - xh * m2);
+    }
+    if (dres) {
+      float rv[8];
+      unpack8(dr[i], rv);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) o[t] += rv[t];
+    }
+    dxr[lane + 32 * i] = pack8(o);
+  }
+}
+
+// per-block partials of dgamma / dbeta -> part[blockIdx.x][2 D] (ln_bwd_final16_kernel sums them)
+template <int PER>
+__global__ void __launch_bounds__(256, PER == 32 ? 1 : 2)
+    ln_bwd_pipe_kernel(bf16* __restrict__ dx, float* __restrict__ part, const bf16* __restrict__ dy,
+                       const bf16* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
+                       const float* __restrict__ g, const bf16* __restrict__ dres, int64_t T, int D) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int NV = PER / 8;
+  extern __shared__ float sm[];  // gamma [D] | red [8 warps][2 * D]
+  float* gs = sm;
+  float* red = sm + D;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = threadIdx.x; c < D; c += 256) gs[c] = g[c];
+  __syncthreads();
+  float dg[PER], db[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) dg[i] = db[i] = 0.f;
+  const int64_t NW = static_cast<int64_t>(gridDim.x) * 8;
+  int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + w;
+  LnBwdRow<PER> A, B;
+  if (r < T) ln_bwd_load(A, dy, x, mean, rstd, r, D, lane);
+  while (r < T) {
+    if (r + NW < T) ln_bwd_load(B, dy, x, mean, rstd, r + NW, D, lane);
+    ln_bwd_row(A, dx, gs, dres, dg, db, r, D, lane);
+    r += NW;
+    if (r >= T) break;
+    if (r + NW < T) ln_bwd_load(A, dy, x, mean, rstd, r + NW, D, lane);
+    ln_bwd_row(B, dx, gs, dres, dg, db, r, D, lane);
+    r += NW;
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = 8 * (lane + 32 * i);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      red[w * 2 * D + c + t] = dg[8 * i + t];
+      red[w * 2 * D + D + c + t] = db[8 * i + t];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 2 * D; c += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k * 2 * D + c];
+    part[static_cast<int64_t>(blockIdx.x) * 2 * D + c] = t;
+  }
+}
+
 // Column sums of the [nblocks, 2D] partials, 16 columns per block x 16 row groups (every
 // thread's loads independent and in flight together), fixed-order smem reduction.
 __global__ void __launch_bounds__(256) ln_bwd_final16_kernel(float* __restrict__ dgamma, float* __restrict__ dbeta,
@@ -540,6 +748,22 @@ using namespace gpp;
 
 static bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+static int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+// GPP_LN_PIPE=0: the one-wave LayerNorm kernels (ln_fwd_vec2 / ln_bwd_vec) instead of the
+// software-pipelined persistent ones, for A/B measurement
+static bool ln_pipe() {
+  static const bool on = [] { const char* e = std::getenv("GPP_LN_PIPE"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
 extern "C" {
 
 int gpp_layernorm_fwd(void* y, float* mean, float* rstd, const void* x, const float* gamma,
@@ -549,6 +773,18 @@ int gpp_layernorm_fwd(void* y, float* mean, float* rstd, const void* x, const fl
   const unsigned grid = static_cast<unsigned>((T + 7) / 8);
   const int d = static_cast<int>(D);
   GPP_ARG_CHECK(D == 128 || (a16(y) && a16(x) && a16(gamma) && a16(beta)), "16-byte aligned rows / affine params");
+  if ((D == 512 || D == 1024) && ln_pipe()) {
+    const unsigned pg = static_cast<unsigned>(std::min<int64_t>((T + 7) / 8, 2 * sm_count()));
+    const size_t smem = 2 * D * sizeof(float);
+    if (D == 1024)
+      launch_pdl(ln_fwd_pipe_kernel<32>, dim3(pg), dim3(256), smem, s, static_cast<bf16*>(y), mean, rstd,
+                 static_cast<const bf16*>(x), gamma, beta, T, d, eps);
+    else
+      launch_pdl(ln_fwd_pipe_kernel<16>, dim3(pg), dim3(256), smem, s, static_cast<bf16*>(y), mean, rstd,
+                 static_cast<const bf16*>(x), gamma, beta, T, d, eps);
+    GPP_LAUNCH_CHECK();
+    return GPP_OK;
+  }
   switch (D) {
     case 128: launch_pdl(ln_fwd_kernel<4>, dim3(grid), dim3(256), 0, s, static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
     case 256: launch_pdl(ln_fwd_vec_kernel<8>, dim3(grid), dim3(256), 0, s, static_cast<bf16*>(y), mean, rstd, static_cast<const bf16*>(x), gamma, beta, T, d, eps); break;
@@ -576,6 +812,33 @@ int gpp_layernorm_bwd(void* dx, float* dgamma, float* dbeta, const void* dy, con
   auto* dyp = static_cast<const bf16*>(dy);
   auto* xp = static_cast<const bf16*>(x);
   auto* drp = static_cast<const bf16*>(dres);
+  if ((D == 512 || D == 1024) && a16(dx) && a16(dy) && a16(x) && (!dres || a16(dres)) && ln_pipe()) {
+    // persistent, one (D = 1024) or two (D = 512) blocks per SM, rows strided over all warps
+    const int nblk = static_cast<int>(std::min<int64_t>((T + 7) / 8, sm_count() * (D == 1024 ? 1 : 2)));
+    float* part = ln_scratch(static_cast<size_t>(nblk) * 2 * D, s);
+    if (!part) return GPP_ERR_CUDA;
+    const size_t smem = (D + 8 * 2 * D) * sizeof(float);
+    if (D == 1024) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(ln_bwd_pipe_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        attr = true;
+      }
+      launch_pdl(ln_bwd_pipe_kernel<32>, dim3(nblk), dim3(256), smem, s, dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d);
+    } else {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(ln_bwd_pipe_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        attr = true;
+      }
+      launch_pdl(ln_bwd_pipe_kernel<16>, dim3(nblk), dim3(256), smem, s, dxp, part, dyp, xp, mean, rstd, gamma, drp, T, d);
+    }
+    GPP_LAUNCH_CHECK();
+    launch_pdl(ln_bwd_final16_kernel, dim3(static_cast<unsigned>((2 * D + 15) / 16)), dim3(256), 0, s, dgamma, dbeta,
+               part, nblk, d, accumulate);
+    GPP_LAUNCH_CHECK();
+    return GPP_OK;
+  }
   if ((D == 512 || D == 1024) && a16(dx) && a16(dy) && a16(x) && (!dres || a16(dres))) {
     // D = 1024: one block per SM, two rows per warp in flight; D = 512: two blocks per SM,
     // one row per warp.  Rows per block rounded up to the rows one pass of 8 warps covers.
