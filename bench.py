@@ -231,7 +231,18 @@ def _gemm_traffic(workload: str) -> dict:
     step (profiles/ncu_step_gemms_r1d_summary.csv), averaged over the step's launch mix
     (28 tower fw, 21 tower dgrad, 28 tower wgrad+SGD, one of each tail GEMM), beside the
     algorithmic bytes of the same mix (operands + outputs + fp32 master read/write + bf16
-    shadow).  Only the CANDLE step was captured; other workloads report null."""
+    shadow).  MMT: the GEMM-family DRAM bytes of one captured iteration (1 branch x 2 layers,
+    the bench's per-layer shapes; tools/ncu_mmt_layer.py) per logical GEMM (12 per layer),
+    beside the same mix's algorithmic bytes.  DLRM reports null."""
+    if workload == "mmt":
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_mmt_layer_r2_gemm.json")
+        try:
+            d = json.load(open(path))
+        except (OSError, ValueError):
+            return {"traffic": None}
+        return {"traffic": d["traffic_MB_per_logical_gemm"], "traffic_unit": "MB per GEMM launch (ncu dram read+write, layer mix)",
+                "algorithmic_MB_per_launch": d["algorithmic_MB_per_logical_gemm"],
+                "traffic_source": "profiles/ncu_mmt_layer_r2_gemm.json"}
     if workload != "candle":
         return {"traffic": None}
     import csv
