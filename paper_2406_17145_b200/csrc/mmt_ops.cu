@@ -688,6 +688,38 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(bf16* __restrict__ ds,
 }
 
 // ---- token mean-pool over S rows per sample (branch output of MMT) ------------------------
+// out[m, c] = mean over the S rows of sample m.  Vector form (D % 64 == 0, 16-byte rows):
+// one block per (sample, 64 columns); 8 threads x 8 columns cover the 64 columns, 32 row
+// slices split the S rows (every thread's 16-byte loads independent), fixed-order smem
+// reduction over the slices.  The scalar form (one thread per column, S dependent loads)
+// kept 6% of the warps busy: 35 us for 16.8 MB.
+__global__ void __launch_bounds__(256) meanpool_fwd_vec_kernel(bf16* __restrict__ out, int64_t ldo,
+                                                               const bf16* __restrict__ x, int64_t M, int S, int D) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[32][65];
+  const int m = blockIdx.y, cg = threadIdx.x & 7, sl = threadIdx.x >> 3;
+  const int c0 = blockIdx.x * 64 + cg * 8;
+  const bf16* xm = x + static_cast<int64_t>(m) * S * D + c0;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+  for (int t = sl; t < S; t += 32) {
+    float v[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(xm + static_cast<int64_t>(t) * D)), v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] += v[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[sl][cg * 8 + i] = acc[i];
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    float t = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) t += red[k][threadIdx.x];
+    out[static_cast<int64_t>(m) * ldo + blockIdx.x * 64 + threadIdx.x] = __float2bfloat16_rn(t / S);
+  }
+}
+
 __global__ void meanpool_fwd_kernel(bf16* __restrict__ out, int64_t ldo, const bf16* __restrict__ x,
                                     int64_t M, int S, int D) {
   pdl_wait();
@@ -699,6 +731,26 @@ __global__ void meanpool_fwd_kernel(bf16* __restrict__ out, int64_t ldo, const b
   float s = 0.f;
   for (int t = 0; t < S; ++t) s += __bfloat162float(xm[static_cast<int64_t>(t) * D]);
   out[m * ldo + c] = __float2bfloat16_rn(s / S);
+}
+
+// dx[m, t, :] = dout[m, :] / S; vector form: 8 columns (one 16-byte store) per thread.
+__global__ void __launch_bounds__(256) meanpool_bwd_vec_kernel(bf16* __restrict__ dx, const bf16* __restrict__ dout,
+                                                               int64_t lddo, int64_t M, int S, int D) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t n8 = M * S * D / 8;
+  const float inv = 1.f / S;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t e = i * 8;
+    const int64_t m = e / (static_cast<int64_t>(S) * D);
+    const int c = static_cast<int>(e % D);
+    float v[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(dout + m * lddo + c)), v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] *= inv;
+    reinterpret_cast<uint4*>(dx)[i] = pack8(v);
+  }
 }
 
 __global__ void meanpool_bwd_kernel(bf16* __restrict__ dx, const bf16* __restrict__ dout,
@@ -922,6 +974,13 @@ int gpp_softmax_bwd(void* ds, const void* p, const float* dp, int64_t R, int64_t
 int gpp_meanpool_fwd(void* out, int64_t ldo, const void* x, int64_t M, int64_t S, int64_t D,
                      void* stream) {
   GPP_ARG_CHECK(out && x && M > 0 && S > 0 && D > 0, "bad argument");
+  if (D % 64 == 0 && a16(x)) {
+    launch_pdl(meanpool_fwd_vec_kernel, dim3(static_cast<unsigned>(D / 64), static_cast<unsigned>(M)), dim3(256), 0,
+               static_cast<cudaStream_t>(stream), static_cast<bf16*>(out), ldo, static_cast<const bf16*>(x), M,
+               static_cast<int>(S), static_cast<int>(D));
+    GPP_LAUNCH_CHECK();
+    return GPP_OK;
+  }
   dim3 grid(static_cast<unsigned>((D + 127) / 128), static_cast<unsigned>(M));
   launch_pdl(meanpool_fwd_kernel, dim3(grid), dim3(128), 0, static_cast<cudaStream_t>(stream), static_cast<bf16*>(out), ldo, static_cast<const bf16*>(x), M, static_cast<int>(S), static_cast<int>(D));
   GPP_LAUNCH_CHECK();
@@ -932,6 +991,13 @@ int gpp_meanpool_bwd(void* dx, const void* dout, int64_t lddo, int64_t M, int64_
                      void* stream) {
   GPP_ARG_CHECK(dx && dout && M > 0, "bad argument");
   int64_t n = M * S * D;
+  if (D % 8 == 0 && lddo % 8 == 0 && a16(dx) && a16(dout)) {
+    const int64_t g8 = std::min<int64_t>((n / 8 + 255) / 256, 148 * 8);
+    launch_pdl(meanpool_bwd_vec_kernel, dim3(static_cast<unsigned>(g8)), dim3(256), 0, static_cast<cudaStream_t>(stream),
+               static_cast<bf16*>(dx), static_cast<const bf16*>(dout), lddo, M, static_cast<int>(S), static_cast<int>(D));
+    GPP_LAUNCH_CHECK();
+    return GPP_OK;
+  }
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
   launch_pdl(meanpool_bwd_kernel, dim3(static_cast<unsigned>(g)), dim3(256), 0, static_cast<cudaStream_t>(stream), static_cast<bf16*>(dx), static_cast<const bf16*>(dout), lddo, M, static_cast<int>(S), static_cast<int>(D));

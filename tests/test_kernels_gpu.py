@@ -337,6 +337,25 @@ def test_embbag_bad_indices_skipped_and_reported(cuda_lib):
     cuda_lib.embbag_check_indices()  # reset by the previous read: no error
 
 
+@pytest.mark.parametrize("D", [96, 1024])
+def test_meanpool_kernels(cuda_lib, D):
+    """Token mean-pool fw (into a strided concat slice) and bw against fp32 torch; D = 1024
+    takes the 16-byte vector kernels, D = 96 the scalar ones."""
+    M, S = 3, 128
+    x = torch.randn(M * S, D, device="cuda").bfloat16()
+    cat = torch.zeros(M, 3 * D, device="cuda", dtype=torch.bfloat16)
+    out = cat[:, D:2 * D]
+    cuda_lib.meanpool_fwd(out, x, M, S, D)
+    ref = x.float().reshape(M, S, D).mean(1)
+    torch.testing.assert_close(out.float(), ref, rtol=1e-2, atol=1e-2)
+    assert torch.count_nonzero(cat[:, :D]) == 0 and torch.count_nonzero(cat[:, 2 * D:]) == 0
+    dcat = torch.randn(M, 3 * D, device="cuda").bfloat16()
+    dx = torch.empty(M * S, D, device="cuda", dtype=torch.bfloat16)
+    cuda_lib.meanpool_bwd(dx, dcat[:, D:2 * D], M, S, D)
+    refd = (dcat[:, D:2 * D].float() / S).repeat_interleave(S, 0)
+    torch.testing.assert_close(dx.float(), refd, rtol=1e-2, atol=1e-4)
+
+
 @pytest.mark.parametrize("D", [128, 1024])
 def test_layernorm_kernels(cuda_lib, D):
     g = torch.Generator(device="cuda").manual_seed(D)
