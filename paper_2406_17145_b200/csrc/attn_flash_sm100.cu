@@ -251,6 +251,196 @@ __global__ void __launch_bounds__(FW_THREADS, 2)
   }
 }
 
+// Streamed forward (default): 256 TMEM columns and ~83 KB of shared memory per CTA, so TWO
+// CTAs run per SM and one's softmax overlaps the other's MMAs (the kernel above holds the
+// whole 128 x S score block in 512 columns: one CTA computes per SM at a time).  K / V
+// arrive as 64-key tiles through a 4-slot TMA ring.  Pass 1: S_j = Q K_j^T per 64-key block
+// (double-buffered in TMEM) -> row max.  Pass 2: S_j recomputed, e = exp2(alpha log2e (s -
+// max)) packed bf16 over the consumed columns (the TMEM A operand), O += E_j V_j; the row
+// sum, O / sum and the base-2 LSE at the end.  Warps: 0 TMA, 1 MMA, 2..9 two per TMEM lane
+// quarter, each taking 32 of a block's 64 keys.
+namespace {
+constexpr int F2_SLOTS = 4;
+constexpr uint32_t F2_TILE = 64 * 128;            // 64 keys x 64 dims bf16, 128B-swizzled: 8 KB
+constexpr uint32_t F2_RING = 16 * 1024;           // after Q (16 KB)
+constexpr uint32_t F2_BAR = F2_RING + F2_SLOTS * F2_TILE;
+constexpr int SMEM_FW2 = F2_BAR + 2048 + 1024;
+constexpr uint32_t F2_O = 128;                     // O accumulator columns [128, 192)
+}  // namespace
+
+__global__ void __launch_bounds__(FW_THREADS, 2)
+    attn_fwd_stream_kernel(const __grid_constant__ CUtensorMap m_q, const __grid_constant__ CUtensorMap m_kv,
+                           float* __restrict__ lse2, bf16* __restrict__ o, int64_t ldo, FaShape sh) {
+  constexpr uint32_t IDESC_S = idesc_bf16<64, false, false>();
+  constexpr uint32_t IDESC_O = idesc_bf16<FA_DH, false, true>();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sq = smem;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + F2_BAR);
+  uint64_t* b_q = bar + 0;                  // Q landed
+  uint64_t* b_full = bar + 1;               // [F2_SLOTS]
+  uint64_t* b_empty = b_full + F2_SLOTS;    // [F2_SLOTS]
+  uint64_t* b_s = b_empty + F2_SLOTS;       // [2] S of TMEM buffer b complete
+  uint64_t* b_c = b_s + 2;                  // [2] softmax warps done with buffer b (max read / E written)
+  uint64_t* b_o = b_c + 2;                  // all E V MMAs complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_o + 1);
+  float* red = reinterpret_cast<float*>(smem + F2_BAR + 128);
+
+  const int S = sh.S, d = sh.d, H = sh.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mblocks = S / 128;
+  const int z = static_cast<int>(blockIdx.x) / mblocks;
+  const int m_blk = static_cast<int>(blockIdx.x) % mblocks;
+  const int sample = z / H, head = z % H;
+  const int row0 = sample * S;
+  const int nb = S / 64;  // 64-key blocks
+  const int ntiles = 3 * nb;  // pass 1: K_0..K_{nb-1}; pass 2: K_0, V_0, K_1, V_1, ...
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(b_q, 1);
+    for (int i = 0; i < F2_SLOTS; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&b_s[i], 1);
+      mbar_init(&b_c[i], FW_EPI_WARPS);
+    }
+    mbar_init(b_o, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // qkv is the previous kernel's output
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(b_q, 128 * 128);
+      tma_load_2d(sq, &m_q, b_q, head * FA_DH, row0 + m_blk * 128);
+      for (int t = 0; t < ntiles; ++t) {
+        const int sl = t % F2_SLOTS;
+        mbar_wait(&b_empty[sl], ((t / F2_SLOTS) & 1) ^ 1);
+        const int u = t - nb;  // pass-2 index
+        const int key_blk = t < nb ? t : u >> 1;
+        const int col = (t >= nb && (u & 1)) ? 2 * d : d;  // V or K columns of the head
+        mbar_expect_tx(&b_full[sl], F2_TILE);
+        tma_load_2d(smem + F2_RING + sl * F2_TILE, &m_kv, &b_full[sl], col + head * FA_DH, row0 + key_blk * 64);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      mbar_wait(b_q, 0);
+      const uint32_t qa = smem_u32(sq);
+      // S of block g (g < nb: pass 1 block g; else pass 2 block g - nb) from ring tile t
+      auto issue_s = [&](int g, int t) {
+        const int b = g & 1, sl = t % F2_SLOTS;
+        if (g >= 2) mbar_wait(&b_c[b], ((g - 2) >> 1) & 1);  // softmax warps done with the buffer
+        mbar_wait(&b_full[sl], (t / F2_SLOTS) & 1);
+        tc_fence_after();
+        const uint32_t ka = smem_u32(smem + F2_RING + sl * F2_TILE);
+#pragma unroll
+        for (int k = 0; k < FA_DH / 16; ++k)
+          umma_bf16(tmem + b * 64, sdesc_sw128(qa + k * 32, 16, 1024), sdesc_sw128(ka + k * 32, 16, 1024), IDESC_S,
+                    k != 0);
+        umma_commit(&b_s[b]);
+        umma_commit(&b_empty[sl]);
+      };
+      for (int g = 0; g < nb; ++g) issue_s(g, g);  // pass 1
+      // pass 2: S of block j + 1 is issued before E_j V_j
+      issue_s(nb, nb);
+      for (int j = 0; j < nb; ++j) {
+        const int g = nb + j;
+        if (j + 1 < nb) issue_s(g + 1, nb + 2 * (j + 1));
+        const int b = g & 1, tv = nb + 2 * j + 1, sl = tv % F2_SLOTS;
+        mbar_wait(&b_c[b], (g >> 1) & 1);  // E_j in TMEM
+        mbar_wait(&b_full[sl], (tv / F2_SLOTS) & 1);
+        tc_fence_after();
+        const uint32_t va = smem_u32(smem + F2_RING + sl * F2_TILE);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // keys 16 kk..: packed E of warp half kk / 2 at b*64 + hf*32 + (kk&1)*8
+          const uint32_t acol = b * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+          fa_umma_ts(tmem + F2_O, tmem + acol, sdesc_sw128(va + kk * 2048, 8192, 1024), IDESC_O, (j | kk) != 0);
+        }
+        umma_commit(&b_empty[sl]);
+      }
+      umma_commit(b_o);
+    }
+  } else {
+    const int q = warp & 3, hf = (warp - 2) / 4;
+    const int lr = q * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    float mx = -INFINITY;
+    for (int g = 0; g < nb; ++g) {
+      const int b = g & 1;
+      mbar_wait(&b_s[b], (g >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32(trow + b * 64 + hf * 32, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) fa_mbar_arrive(&b_c[b]);
+    }
+    mx = fa_combine(red, hf, lr, mx, true);
+    const float sl2 = sh.alpha * 1.4426950408889634f;
+    const float mb = mx * sl2;
+    float sum = 0.f;
+    for (int j = 0; j < nb; ++j) {
+      const int g = nb + j, b = g & 1;
+      mbar_wait(&b_s[b], (g >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32(trow + b * 64 + hf * 32, v);
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float e0 = fa_ex2(fmaf(__uint_as_float(v[2 * i]), sl2, -mb));
+        const float e1 = fa_ex2(fmaf(__uint_as_float(v[2 * i + 1]), sl2, -mb));
+        sum += e0 + e1;
+        pk[i] = fa_pack(e0, e1);
+      }
+      fa_tmem_st16(trow + b * 64 + hf * 32, pk);  // over this warp's consumed columns
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) fa_mbar_arrive(&b_c[b]);
+    }
+    sum = fa_combine(red, hf, lr, sum, false);
+    const int64_t grow = static_cast<int64_t>(row0) + m_blk * 128 + lr;
+    if (hf == 0) lse2[static_cast<int64_t>(z) * S + m_blk * 128 + lr] = mb + __log2f(sum);
+    const float inv = 1.f / sum;
+    mbar_wait(b_o, 0);
+    tc_fence_after();
+    uint32_t v[32];
+    tmem_ld32(trow + F2_O + hf * 32, v);
+    bf16* dst = o + grow * ldo + head * FA_DH + hf * 32;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 pk;
+      pk.x = fa_pack(__uint_as_float(v[8 * i + 0]) * inv, __uint_as_float(v[8 * i + 1]) * inv);
+      pk.y = fa_pack(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv);
+      pk.z = fa_pack(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv);
+      pk.w = fa_pack(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv);
+      *reinterpret_cast<uint4*>(dst + 8 * i) = pk;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  }
+}
+
 // D[z, s] = alpha sum_c dO[row, head*64 + c] * O[row, head*64 + c] (pre-scaled by the softmax
 // scale so that dS = P (alpha dP - D) is one FFMA + one FMUL): eight lanes per (row, head),
 // one 16-byte vector of each operand per lane (every warp load is 512 contiguous bytes),
@@ -662,12 +852,27 @@ int gpp_flash_attn_fwd(const void* qkv, float* lse2, void* o, int64_t ldo, int64
   if ((rc = tc::make_map_bf16(&mq, qkv, 3 * d, T, 3 * d, 64, 128))) return rc;
   if ((rc = tc::make_map_bf16(&mk, qkv, 3 * d, T, 3 * d, 64, 256))) return rc;
   if ((rc = tc::make_map_bf16(&mv, qkv, 3 * d, T, 3 * d, 64, 64))) return rc;
+  tc::FaShape sh{static_cast<int>(S), static_cast<int>(d), static_cast<int>(H), scale};
+  // GPP_ATTN_FWD=resident: the 512-column kernel (whole score block in TMEM) for A/B runs
+  static const bool resident = [] { const char* e = std::getenv("GPP_ATTN_FWD"); return e && e[0] == 'r'; }();
+  if (!resident) {
+    CUtensorMap mkv;
+    if ((rc = tc::make_map_bf16(&mkv, qkv, 3 * d, T, 3 * d, 64, 64))) return rc;
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(tc::attn_fwd_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_FW2);
+      attr2 = true;
+    }
+    launch_pdl(tc::attn_fwd_stream_kernel, dim3(static_cast<unsigned>(Z * (S / 128))), dim3(tc::FW_THREADS),
+               tc::SMEM_FW2, static_cast<cudaStream_t>(stream), mq, mkv, lse2, static_cast<bf16*>(o), ldo, sh);
+    GPP_LAUNCH_CHECK();
+    return GPP_OK;
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc::attn_fwd_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_FWL);
     attr = true;
   }
-  tc::FaShape sh{static_cast<int>(S), static_cast<int>(d), static_cast<int>(H), scale};
   launch_pdl(tc::attn_fwd_lse_kernel, dim3(static_cast<unsigned>(Z * (S / 128))), dim3(tc::FW_THREADS), tc::SMEM_FWL,
              static_cast<cudaStream_t>(stream), mq, mk, mv, lse2, static_cast<bf16*>(o), ldo, sh);
   GPP_LAUNCH_CHECK();
