@@ -14,7 +14,21 @@ import torch
 from paper_2406_17145_b200.runtime import lib
 
 
+def qkv():
+    """--qkv: the QKV projection forward (8192 x 3072 x 1024, bias epilogue), three launches."""
+    dev = torch.device("cuda", 0)
+    x = torch.randn(8192, 1024, device=dev).bfloat16()
+    w = (torch.randn(3072, 1024, device=dev) / 32).bfloat16()
+    b = torch.zeros(3072, device=dev)
+    y = torch.empty(8192, 3072, device=dev, dtype=torch.bfloat16)
+    for _ in range(3):
+        lib.linear_fwd(y, x, w, bias=b, act="none")
+    torch.cuda.synchronize()
+
+
 def main():
+    if "--qkv" in sys.argv:
+        return qkv()
     dev = torch.device("cuda", 0)
     T, N, K = 8192, 4096, 1024
     x = torch.randn(T, K, device=dev).bfloat16()
