@@ -356,7 +356,7 @@ def test_meanpool_kernels(cuda_lib, D):
     torch.testing.assert_close(dx.float(), refd, rtol=1e-2, atol=1e-4)
 
 
-@pytest.mark.parametrize("D", [128, 1024])
+@pytest.mark.parametrize("D", [128, 512, 1024])
 def test_layernorm_kernels(cuda_lib, D):
     g = torch.Generator(device="cuda").manual_seed(D)
     T = 777
