@@ -175,3 +175,17 @@ def test_dlrm_dp2_embedding_stage(backend):
     """DLRM: the embedding tables as a DP-2 stage (replicas all-gather indices and pooled
     gradients and apply every replica's sparse update), MLPs on their own ranks."""
     _run(backend, _dlrm, [([0, 1, 2, 3], 16, [0]), ([4, 5, 6, 7], 32, [1, 2]), ([8, 9, 10, 11, 12], 16, [3])])
+
+
+def _mmt4():
+    # ops: branches 0..3 (one layer each), concat 4, CE head 5
+    return W.mmt(B=8, branches=4, layers=1, S=128, d=128, H=2, ffn=256, classes=64)
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_mmt_eight_rank_branch_dp2_layout(backend):
+    """The shape of the frozen MMT plan at 8 GPUs (profiles/strategies/mmt-*_gpp_n8_*): one
+    stage per branch, each a DP-2 stage over two ranks, the last also holding concat + CE
+    head -- eight executor ranks (sharing one GPU with the cuda backend), per-rank gradients
+    vs the oracle.  The 8-GPU box itself is the driver's SCALE run."""
+    _run(backend, _mmt4, [([0], 8, [0, 1]), ([1], 8, [2, 3]), ([2], 8, [4, 5]), ([3, 4, 5], 8, [6, 7])])
