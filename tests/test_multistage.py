@@ -189,3 +189,12 @@ def test_mmt_eight_rank_branch_dp2_layout(backend):
     head -- eight executor ranks (sharing one GPU with the cuda backend), per-rank gradients
     vs the oracle.  The 8-GPU box itself is the driver's SCALE run."""
     _run(backend, _mmt4, [([0], 8, [0, 1]), ([1], 8, [2, 3]), ([2], 8, [4, 5]), ([3, 4, 5], 8, [6, 7])])
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_dlrm_eight_rank_plan_layout(backend):
+    """The shape of the frozen DLRM plan at 8 GPUs (profiles/strategies/dlrm-*_gpp_n8_*): the
+    bottom MLP a DP-2 stage, the embedding tables split over four single-rank stages, the
+    interaction + top MLP + BCE head a DP-2 stage; four micro-batches."""
+    _run(backend, _dlrm, [([0, 1, 2, 3], 16, [0, 1]), ([4], 16, [2]), ([5], 16, [3]), ([6], 16, [4]), ([7], 16, [5]),
+                          ([8, 9, 10, 11, 12], 16, [6, 7])])
