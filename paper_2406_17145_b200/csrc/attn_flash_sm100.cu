@@ -441,6 +441,214 @@ __global__ void __launch_bounds__(FW_THREADS, 2)
   }
 }
 
+// Online forward (one pass over the keys): the eight softmax warps form two ping-pong groups
+// of one warp per TMEM lane quarter; group g owns 64-key blocks j = g, g + 2, ... of every
+// row, keeps its own running max / sum per row in registers and its own O accumulator in TMEM
+// (O_g += E_j V_j), and rescales O_g only when a block raises its row max by more than 2^8
+// (waiting for its previous E V MMA first).  The two groups' (max, sum, O) are merged once at
+// the end.  TMEM: S buffers [0, 64) / [64, 128) (group 0 / 1), O_0 [128, 192), O_1 [192, 256).
+namespace {
+constexpr float F3_SLACK = 8.f;  // log2 units a row max may grow before O is rescaled
+}  // namespace
+
+__global__ void __launch_bounds__(FW_THREADS, 2)
+    attn_fwd_online_kernel(const __grid_constant__ CUtensorMap m_q, const __grid_constant__ CUtensorMap m_kv,
+                           float* __restrict__ lse2, bf16* __restrict__ o, int64_t ldo, FaShape sh) {
+  constexpr uint32_t IDESC_S = idesc_bf16<64, false, false>();
+  constexpr uint32_t IDESC_O = idesc_bf16<FA_DH, false, true>();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sq = smem;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + F2_BAR);
+  uint64_t* b_q = bar + 0;                  // Q landed
+  uint64_t* b_full = bar + 1;               // [F2_SLOTS]
+  uint64_t* b_empty = b_full + F2_SLOTS;    // [F2_SLOTS]
+  uint64_t* b_s = b_empty + F2_SLOTS;       // [2] S of group g's buffer complete
+  uint64_t* b_c = b_s + 2;                  // [2] group g's E written (buffer consumed)
+  uint64_t* b_pv = b_c + 2;                 // [2] group g's E V MMAs complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_pv + 2);
+  float* red = reinterpret_cast<float*>(smem + F2_BAR + 128);  // [2 groups][2][128] max, sum
+
+  const int S = sh.S, d = sh.d, H = sh.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mblocks = S / 128;
+  const int z = static_cast<int>(blockIdx.x) / mblocks;
+  const int m_blk = static_cast<int>(blockIdx.x) % mblocks;
+  const int sample = z / H, head = z % H;
+  const int row0 = sample * S;
+  const int nb = S / 64;  // 64-key blocks (even)
+  const int ntiles = 2 * nb;  // K_0, V_0, K_1, V_1, ...
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(b_q, 1);
+    for (int i = 0; i < F2_SLOTS; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&b_s[i], 1);
+      mbar_init(&b_c[i], FW_EPI_WARPS / 2);
+      mbar_init(&b_pv[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // qkv is the previous kernel's output
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(b_q, 128 * 128);
+      tma_load_2d(sq, &m_q, b_q, head * FA_DH, row0 + m_blk * 128);
+      for (int t = 0; t < ntiles; ++t) {
+        const int sl = t % F2_SLOTS;
+        mbar_wait(&b_empty[sl], ((t / F2_SLOTS) & 1) ^ 1);
+        const int col = (t & 1) ? 2 * d : d;  // V or K columns of the head
+        mbar_expect_tx(&b_full[sl], F2_TILE);
+        tma_load_2d(smem + F2_RING + sl * F2_TILE, &m_kv, &b_full[sl], col + head * FA_DH, row0 + (t >> 1) * 64);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      mbar_wait(b_q, 0);
+      const uint32_t qa = smem_u32(sq);
+      auto issue_s = [&](int j) {  // S_j = Q K_j^T into group (j & 1)'s buffer
+        const int b = j & 1, t = 2 * j, sl = t % F2_SLOTS;
+        if (j >= 2) mbar_wait(&b_c[b], ((j - 2) >> 1) & 1);  // E_{j-2} written (and its E V issued)
+        mbar_wait(&b_full[sl], (t / F2_SLOTS) & 1);
+        tc_fence_after();
+        const uint32_t ka = smem_u32(smem + F2_RING + sl * F2_TILE);
+#pragma unroll
+        for (int k = 0; k < FA_DH / 16; ++k)
+          umma_bf16(tmem + b * 64, sdesc_sw128(qa + k * 32, 16, 1024), sdesc_sw128(ka + k * 32, 16, 1024), IDESC_S,
+                    k != 0);
+        umma_commit(&b_s[b]);
+        umma_commit(&b_empty[sl]);
+      };
+      issue_s(0);
+      for (int j = 0; j < nb; ++j) {
+        if (j + 1 < nb) issue_s(j + 1);
+        const int b = j & 1, tv = 2 * j + 1, sl = tv % F2_SLOTS;
+        mbar_wait(&b_c[b], (j >> 1) & 1);  // E_j in TMEM (and O_b rescaled if it had to be)
+        mbar_wait(&b_full[sl], (tv / F2_SLOTS) & 1);
+        tc_fence_after();
+        const uint32_t va = smem_u32(smem + F2_RING + sl * F2_TILE);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // keys 16 kk.. : packed E columns 8 kk.. of the buffer
+          fa_umma_ts(tmem + 128 + b * 64, tmem + b * 64 + kk * 8, sdesc_sw128(va + kk * 2048, 8192, 1024), IDESC_O,
+                     (j >= 2 || kk != 0) ? 1u : 0u);
+        umma_commit(&b_pv[b]);
+        umma_commit(&b_empty[sl]);
+      }
+    }
+  } else {
+    const int q = warp & 3, g = (warp - 2) / 4;  // lane quarter, group
+    const int lr = q * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t tb = trow + g * 64, to = trow + 128 + g * 64;
+    const float sl2 = sh.alpha * 1.4426950408889634f;
+    float mrun = -INFINITY;  // running row max (raw score units) of this group's blocks
+    float sum = 0.f;
+    int kth = 0;  // blocks of this group processed
+    for (int j = g; j < nb; j += 2, ++kth) {
+      mbar_wait(&b_s[g], kth & 1);
+      tc_fence_after();
+      float mx = mrun;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // row max over the block's 64 columns, 32 at a time
+        uint32_t v[32];
+        tmem_ld32(tb + h * 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+      }
+      if (kth == 0) {
+        mrun = mx;
+      } else if (__any_sync(0xffffffffu, (mx - mrun) * sl2 > F3_SLACK)) {
+        // warp-uniform (tcgen05.ld / st are .sync.aligned): every lane moves its max up to the
+        // block's and rescales its O_g row and sum; the last E V MMA of the group must be done
+        mbar_wait(&b_pv[g], (kth - 1) & 1);
+        tc_fence_after();
+        const float f = fa_ex2((mrun - mx) * sl2);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t ov[32];
+          tmem_ld32(to + h * 32, ov);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * f);
+          fa_tmem_st16(to + h * 32, *reinterpret_cast<uint32_t(*)[16]>(&ov[0]));
+          fa_tmem_st16(to + h * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&ov[16]));
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        sum *= f;
+        mrun = mx;
+      }
+      const float mb = mrun * sl2;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // exponentials 32 columns at a time; bf16 pairs of half h -> columns 16 h..
+        uint32_t v[32], pk[16];
+        tmem_ld32(tb + h * 32, v);  // (half 0's pairs only overwrite half 0's consumed columns)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float e0 = fa_ex2(fmaf(__uint_as_float(v[2 * i]), sl2, -mb));
+          const float e1 = fa_ex2(fmaf(__uint_as_float(v[2 * i + 1]), sl2, -mb));
+          sum += e0 + e1;
+          pk[i] = fa_pack(e0, e1);
+        }
+        fa_tmem_st16(tb + h * 16, pk);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) fa_mbar_arrive(&b_c[g]);
+    }
+    // merge the two groups: (max, sum) through shared memory, O from both TMEM accumulators
+    red[(g * 2 + 0) * 128 + lr] = mrun;
+    red[(g * 2 + 1) * 128 + lr] = sum;
+    mbar_wait(&b_pv[g], (kth - 1) & 1);  // this group's last E V MMA complete
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * FW_EPI_WARPS) : "memory");
+    tc_fence_after();
+    const float m0 = red[0 * 128 + lr], s0 = red[1 * 128 + lr];
+    const float m1 = red[2 * 128 + lr], s1 = red[3 * 128 + lr];
+    const float mm = fmaxf(m0, m1);
+    const float f0 = fa_ex2((m0 - mm) * sl2), f1 = fa_ex2((m1 - mm) * sl2);
+    const float tot = s0 * f0 + s1 * f1;
+    const float inv = 1.f / tot;
+    const int64_t grow = static_cast<int64_t>(row0) + m_blk * 128 + lr;
+    if (g == 0) lse2[static_cast<int64_t>(z) * S + m_blk * 128 + lr] = mm * sl2 + __log2f(tot);
+    uint32_t a[32], bb[32];  // this group's half of the 64 output dims from both accumulators
+    tmem_ld32(trow + 128 + g * 32, a);
+    tmem_ld32(trow + 192 + g * 32, bb);
+    bf16* dst = o + grow * ldo + head * FA_DH + g * 32;
+    const float c0 = f0 * inv, c1 = f1 * inv;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float w[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) w[t] = fmaf(__uint_as_float(a[8 * i + t]), c0, __uint_as_float(bb[8 * i + t]) * c1);
+      uint4 pkk;
+      pkk.x = fa_pack(w[0], w[1]);
+      pkk.y = fa_pack(w[2], w[3]);
+      pkk.z = fa_pack(w[4], w[5]);
+      pkk.w = fa_pack(w[6], w[7]);
+      *reinterpret_cast<uint4*>(dst + 8 * i) = pkk;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  }
+}
+
 // D[z, s] = alpha sum_c dO[row, head*64 + c] * O[row, head*64 + c] (pre-scaled by the softmax
 // scale so that dS = P (alpha dP - D) is one FFMA + one FMUL): eight lanes per (row, head),
 // one 16-byte vector of each operand per lane (every warp load is 512 contiguous bytes),
@@ -854,7 +1062,22 @@ int gpp_flash_attn_fwd(const void* qkv, float* lse2, void* o, int64_t ldo, int64
   if ((rc = tc::make_map_bf16(&mv, qkv, 3 * d, T, 3 * d, 64, 64))) return rc;
   tc::FaShape sh{static_cast<int>(S), static_cast<int>(d), static_cast<int>(H), scale};
   // GPP_ATTN_FWD=resident: the 512-column kernel (whole score block in TMEM) for A/B runs
-  static const bool resident = [] { const char* e = std::getenv("GPP_ATTN_FWD"); return e && e[0] == 'r'; }();
+  // default: the online kernel; GPP_ATTN_FWD=stream (two-pass streamed) / resident for A/B runs
+  static const char fwd_kind = [] { const char* e = std::getenv("GPP_ATTN_FWD"); return e ? e[0] : 'o'; }();
+  const bool resident = fwd_kind == 'r';
+  if (fwd_kind == 'o') {  // one pass, two ping-pong groups, conditional rescale
+    CUtensorMap mkv;
+    if ((rc = tc::make_map_bf16(&mkv, qkv, 3 * d, T, 3 * d, 64, 64))) return rc;
+    static bool attr3 = false;
+    if (!attr3) {
+      cudaFuncSetAttribute(tc::attn_fwd_online_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_FW2);
+      attr3 = true;
+    }
+    launch_pdl(tc::attn_fwd_online_kernel, dim3(static_cast<unsigned>(Z * (S / 128))), dim3(tc::FW_THREADS),
+               tc::SMEM_FW2, static_cast<cudaStream_t>(stream), mq, mkv, lse2, static_cast<bf16*>(o), ldo, sh);
+    GPP_LAUNCH_CHECK();
+    return GPP_OK;
+  }
   if (!resident) {
     CUtensorMap mkv;
     if ((rc = tc::make_map_bf16(&mkv, qkv, 3 * d, T, 3 * d, 64, 64))) return rc;

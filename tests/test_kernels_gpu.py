@@ -649,6 +649,28 @@ def test_flash_attention_fwd_bwd(cuda_lib, m, S, H):
     assert torch.equal(again, dqkv)
 
 
+def test_flash_attention_fwd_growing_scores(cuda_lib):
+    """Keys of later 64-key blocks scaled up so every row's running max grows block after
+    block: the online forward must rescale its O accumulators (csrc/attn_flash_sm100.cu,
+    attn_fwd_online_kernel) and still match fp32 torch in O and the base-2 LSE."""
+    m, S, H = 2, 512, 2
+    g = torch.Generator(device="cuda").manual_seed(11)
+    d = 64 * H
+    qkv = torch.randn(m * S, 3 * d, device="cuda", generator=g)
+    growth = (1 + torch.arange(S, device="cuda") // 64).float().repeat(m)  # key block kb -> x (kb + 1)
+    qkv[:, d:2 * d] *= growth[:, None]
+    qkv = qkv.bfloat16()
+    dout = torch.randn(m * S, d, device="cuda", generator=g).bfloat16()
+    scale = 0.125
+    o = torch.empty(m * S, d, device="cuda", dtype=torch.bfloat16)
+    lse2 = torch.empty(m * H * S, device="cuda")
+    cuda_lib.flash_attn_fwd(qkv, lse2, o, m, S, d, H, scale)
+    torch.cuda.synchronize()
+    o_ref, _, lse_ref = _attn_ref(qkv, dout, m, S, H, scale)
+    assert _rel(o, o_ref) < 1e-2
+    assert torch.allclose(lse2, lse_ref, atol=2e-2, rtol=1e-3)
+
+
 @pytest.mark.parametrize("kind", ["mse", "bce"])
 @pytest.mark.parametrize("K,dt", [(1024, torch.bfloat16), (4096, torch.bfloat16), (300, torch.float32)])
 def test_rowdot_loss_fused(cuda_lib, kind, K, dt):
