@@ -775,6 +775,19 @@ static_assert(BwTmem<false>::A1 + FA_DH == 256 && BwTmem<true>::A0 + FA_DH == 25
 //   S = Q K_j^T, dP = dO V_j^T (lane = query, lse2 / D row constants); dS in place;
 //   dQ += dS K_j.
 // smem: this role's region; w: role-local warp; qw: the CTA warp index (TMEM lane quarter).
+#ifdef GPP_ATTN_TRACE
+// Phase timestamps (SM clock) of the first 64 blocks of CTA 0's dK/dV role (probe builds only).
+__device__ long long g_attn_trace[6 * 64];
+#define ATR(ev, gb, on)                                                       \
+  do {                                                                        \
+    if ((on) && blockIdx.x == 0 && (gb) < 64) g_attn_trace[(ev) * 64 + (gb)] = clock64(); \
+  } while (0)
+#else
+#define ATR(ev, gb, on) \
+  do {                  \
+  } while (0)
+#endif
+
 template <bool DQ>
 __device__ __forceinline__ void attn_bwd_role(uint8_t* smem, uint32_t tmem, int w, int qw, int lane,
                                               const CUtensorMap& m_qkv128, const CUtensorMap& m_qkvb,
@@ -825,6 +838,7 @@ __device__ __forceinline__ void attn_bwd_role(uint8_t* smem, uint32_t tmem, int 
         for (int j = 0; j < nb; ++j, ++g) {
           const int st = g % BW_STAGES;
           mbar_wait(&b_free[st], ((g / BW_STAGES) & 1) ^ 1);
+          ATR(5, g, !DQ);
           uint8_t* sb = smem + BW_RING + st * BW_STAGE_STRIDE;
           if (DQ) {
             mbar_expect_tx(&b_full[st], 2 * TILEB);
@@ -851,6 +865,7 @@ __device__ __forceinline__ void attn_bwd_role(uint8_t* smem, uint32_t tmem, int 
           const int st = gg % BW_STAGES, b = gg % NB;
           const uint32_t ta = smem_u32(smem + BW_RING + st * BW_STAGE_STRIDE), tb = ta + TILEB;
           mbar_wait(&b_full[st], (gg / BW_STAGES) & 1);
+          ATR(0, gg, !DQ);
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < FA_DH / 16; ++k) {
@@ -861,6 +876,7 @@ __device__ __forceinline__ void attn_bwd_role(uint8_t* smem, uint32_t tmem, int 
                       IDESC_S, k != 0);
           }
           umma_commit(&b_s[b]);
+          ATR(1, gg, !DQ);
         };
         for (int j = 0; j + 1 < NB && j < nb; ++j) issue_sp(g + j);
         for (int j = 0; j < nb; ++j, ++g) {
@@ -868,6 +884,7 @@ __device__ __forceinline__ void attn_bwd_role(uint8_t* smem, uint32_t tmem, int 
           // buffer (g + NB - 1) % NB last held block g - 1, whose MMAs were issued last iteration
           if (j + NB - 1 < nb) issue_sp(g + NB - 1);
           mbar_wait(&b_p[b], (g / NB) & 1);
+          ATR(4, g, !DQ);
           if (j == 0 && it > 0) mbar_wait(b_acc, (it - 1) & 1);  // previous item's accumulators read out
           tc_fence_after();
           const uint32_t ta = smem_u32(smem + BW_RING + st * BW_STAGE_STRIDE), tb = ta + TILEB;
@@ -911,6 +928,7 @@ __device__ __forceinline__ void attn_bwd_role(uint8_t* smem, uint32_t tmem, int 
         const float* vec = reinterpret_cast<const float*>(smem + BW_RING + st * BW_STAGE_STRIDE + 2 * TILEB);
         if (!DQ) mbar_wait(&b_full[st], (gb / BW_STAGES) & 1);  // lse2 / D of the stage (TMA-written)
         mbar_wait(&b_s[b], (gb / NB) & 1);
+        ATR(2, gb, !DQ && lane == 0 && q == 0);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // 16 columns at a time; bf16 pairs of half h -> columns 8h..8h+7
@@ -943,6 +961,7 @@ __device__ __forceinline__ void attn_bwd_role(uint8_t* smem, uint32_t tmem, int 
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
+        ATR(3, gb, !DQ && lane == 0 && q == 0);
         if (lane == 0) fa_mbar_arrive(&b_p[b]);
       }
       // the item's accumulators -> bf16 rows of dqkv, then hand them back to the MMA warp
@@ -1017,6 +1036,10 @@ __global__ void __launch_bounds__(BW_THREADS, 2)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // prologue above overlaps the previous kernel's tail
   pdl_trigger();
+#ifdef GPP_ATTN_TRACE_SOLO  // probe builds: the dK/dV role alone
+  if (dq_role) {
+  } else
+#endif
   if (dq_role)
     attn_bwd_role<true>(smem, tmem, warp, warp, lane, m_qkv128, m_qkvb, m_do128, m_dob, lse2, dvec, dqkv, ld_dqkv,
                         sh, b - P, P, n);
@@ -1032,6 +1055,12 @@ __global__ void __launch_bounds__(BW_THREADS, 2)
 }
 
 }  // namespace tc
+
+#ifdef GPP_ATTN_TRACE
+extern "C" int gpp_attn_trace_read(long long* out) {
+  return cudaMemcpyFromSymbol(out, tc::g_attn_trace, sizeof(tc::g_attn_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 namespace {
 int flash_checks(const void* qkv, int64_t m, int64_t S, int64_t d, int64_t H) {
