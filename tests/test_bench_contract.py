@@ -2,6 +2,7 @@
 
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -29,8 +30,9 @@ def test_gpus_flag_spawns_ranks_dry_run():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
                        capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
-    ranks = sorted(l for l in r.stderr.splitlines() if l.startswith("[bench] rank "))
-    assert [l.split()[2] for l in ranks] == ["0/2", "1/2"], r.stderr[-2000:]
+    # the two ranks share the launcher's stderr, so their lines may interleave mid-line
+    ranks = sorted(set(re.findall(r"\[bench\] rank (\d+/\d+)", r.stderr)))
+    assert ranks == ["0/2", "1/2"], r.stderr[-2000:]
     assert json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0]) == {"dry_run": True, "n_gpus": 2}
 
 
